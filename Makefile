@@ -7,7 +7,7 @@ SITE      := $(shell $(PY) -c "import sysconfig;print(sysconfig.get_paths()['pur
 NCCL_DIR  := $(SITE)/nvidia/nccl
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
-             -Iinclude -I$(NCCL_DIR)/include --expt-relaxed-constexpr -Xptxas -v
+             -Iinclude -I$(NCCL_DIR)/include --expt-relaxed-constexpr -Xptxas -v --fmad=false
 PKG       := paper_1606_04473_b200
 CSRC      := $(PKG)/csrc
 CU_SRCS   := $(CSRC)/ara_host.cu $(CSRC)/ara_kernel.cu $(CSRC)/densify.cu $(CSRC)/metrics.cu
@@ -27,7 +27,7 @@ build/%.o: $(CSRC)/%.cu $(CSRC)/ara_internal.cuh include/ara.h
 
 $(PKG)/libara.so: $(CU_OBJS)
 	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $(CU_OBJS) \
-	    -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_DIR)/lib -lcudart
+	    -L$(NCCL_DIR)/lib -l:libnccl.so.2 -Xlinker -rpath=$(NCCL_DIR)/lib
 
 $(PKG)/libara_mb.so: $(CSRC)/microbench.cu
 	$(NVCC) $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -shared -Iinclude -o $@ $<

@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""bench.py — Aggregate Risk Analysis hot path on B200 (arxiv 1606.04473).
+
+One step = one pass of the whole hot path over the
+workload: ELT densify (+ NVLink broadcast when N > 1), YET ingest, the ARA
+trial kernel, the YLT all-gather (N > 1) and device PML/TVaR.
+
+  value : trials/s of the whole job with inputs already resident in HBM
+          (sparse ELT lists + YET CSR on the device; the library borrows them)
+  e2e   : the same step through the C-ABI with HOST buffers — pinned sparse
+          ELTs + YET streamed in chunks (copy/compute overlap) and the YLT +
+          metrics read back — H2D/D2H inside the timed region
+
+N > 1: one process per GPU (torchrun); trials are sharded by ara_partition
+(strong scaling of the paper-shaped layer, BASELINE config 3), the YLT is
+all-gathered over NVLink.  Timing: CUDA events on the launching stream, barrier
++ synchronize on both sides, max over ranks.
+
+--impl reference: the CPU oracle (this tier's reference arm), timed on host
+cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "trials/sec and ELT lookups/sec at 1/2/4/8 B200; % of HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="paper")
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--e2e-mode", default="chunked", choices=["chunked", "all"])
+    ap.add_argument("--chunk-trials", type=int, default=65536)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--l2-persist", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def host_info():
+    cpu = "?"
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu": cpu, "python": platform.python_version()}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.gpu)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                smax.append(float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
+        load = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": float(max(smax)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str) -> int:
+    """per event 4 B of id + the 32-B sectors of every
+    layer window; per trial 8 B of offsets + 8 B per YLT row written."""
+    eps = 4 if precision == "f64" else 8
+    sec = 0
+    for L in w.layers:
+        sec += (L.elt_end + eps - 1) // eps - L.elt_begin // eps
+    return n_events * (4 + 32 * sec) + n_trials * (8 + 8 * (len(w.layers) + 1))
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
+        return {}
+
+
+def load_traffic(w, precision):
+    """dram bytes per launch of the ARA kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ara_kernel_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d.get(f"{w.name}/{precision}", {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+# ------------------------------------------------------------------ oracle (cpu baseline / reference arm)
+def oracle_sample_rate(w, seconds: float, precision: str):
+    """The oracle as it stands (single thread, dense direct-access lookups) on
+    the first trials of the workload; sized to ~`seconds` of CPU work."""
+    import oracle
+    eo, ev, ls = synth.gen_elts(w)
+    E = oracle.Elts(eo, ev, ls)
+    dense = oracle.direct_access(E, w.catalog)
+    d, li = w.elt_terms()
+    lay = oracle.layers_from_specs(w.layers)
+
+    def run(n):
+        off, ids = synth.gen_yet(w, first=0, n=n)
+        t0 = time.perf_counter()
+        oracle.ara(off, ids, E, w.catalog, d, li, lay, lookup="dense", dense=dense,
+                   fp32_storage=precision == "f32")
+        return time.perf_counter() - t0, int(off[-1])
+
+    t, _ = run(200)
+    n = int(max(200, min(w.n_trials, 200 * seconds / max(t, 1e-6))))
+    t, ev_n = run(n)
+    return {"trials": n, "seconds": t, "trials_per_s": n / t, "events": ev_n,
+            "lookups_per_s": ev_n * sum(L.elt_end - L.elt_begin for L in w.layers) / t}
+
+
+def reference_arm(a, rank, world):
+    if rank != 0:
+        return
+    w = synth.get_config(a.config)
+    per_step = max(2.0, 60.0 / max(1, a.steps + a.warmup))
+    res = []
+    for i in range(a.warmup + a.steps):
+        r = oracle_sample_rate(w, per_step, a.precision)
+        if i >= a.warmup:
+            res.append(r)
+    tps = float(np.median([r["trials_per_s"] for r in res]))
+    sample = f"first {res[0]['trials']} trials of the {w.name} workload per step, dense direct-access lookups"
+    line = {"impl": "reference", "metric": METRIC, "value": tps, "unit": "trials/s", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * w.n_trials / tps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": a.precision,
+            "data": "synthetic", "config": {"workload": w.name, "n_trials": w.n_trials},
+            "lookups_per_sec": float(np.median([r["lookups_per_s"] for r in res])),
+            "cpu_baseline": {"value": tps, "unit": "trials/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": tps, "unit": "trials/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "host": host_info()}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return reference_arm(a, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1606_04473_b200 import ara
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = synth.get_config(a.config)
+    T = w.n_trials
+    first, count = ara.ara_partition(T, world, rank)
+    stream = torch.cuda.current_stream()
+
+    nccl_id = None
+    if world > 1:
+        obj = [ara.ara_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- inputs: this rank's YET shard generated straight into pinned memory
+    t_gen = time.time()
+    n_off = count + 1
+    off_pin = torch.empty(n_off, dtype=torch.int64, pin_memory=True)
+    synth.gen_offsets(w, first, count, out=off_pin.numpy().view(np.uint64))
+    n_ev = int(off_pin[-1])
+    ids_pin = torch.empty(max(n_ev, 1), dtype=torch.int32, pin_memory=True)
+    synth.gen_events(w, synth.event_base(w, first), n_ev, out=ids_pin.numpy().view(np.uint32))
+    if rank == 0:
+        eo, ev, ls = synth.gen_elts(w)
+        eo_pin = torch.from_numpy(eo.view(np.int64)).pin_memory()
+        ev_pin = torch.from_numpy(ev.view(np.int32)).pin_memory()
+        ls_pin = torch.from_numpy(ls).pin_memory()
+        d_eo, d_ev, d_ls = eo_pin.to(dev), ev_pin.to(dev), ls_pin.to(dev)
+    else:
+        eo_pin = ev_pin = ls_pin = d_eo = d_ev = d_ls = None
+    d_off = off_pin.to(dev)
+    d_ids = ids_pin[:n_ev].to(dev) if n_ev else ids_pin.to(dev)
+    torch.cuda.synchronize()
+    gen_s = time.time() - t_gen
+    terms = w.elt_terms()
+    R = list(w.return_periods)
+    L = len(w.layers)
+
+    # ---- device-resident arm (value)
+    ctx = ara.Context(w.catalog, device=local, precision=a.precision, stream=stream, rank=rank, world=world,
+                      nccl_id=nccl_id, l2_persist=a.l2_persist)
+    kern_ms, ag_ms, met_ms, launches = [], [], [], []
+
+    def step(record):
+        ctx.load_elts(d_eo, d_ev, d_ls, terms, n_elts=w.n_elts)          # a0 (+ NVLink broadcast)
+        ctx.load_yet(T, first, d_off, d_ids)                             # a1 (device: borrowed)
+        st = ctx.run(w.layers)                                           # a2-a9
+        k, pml, tvar, mms = ctx.metrics(R)                               # a10
+        if record:
+            kern_ms.append(st["kernel_ms"])
+            ag_ms.append(st["allgather_ms"])
+            met_ms.append(mms)
+            launches.append(st["n_kernel_launches"])
+        return st, pml, tvar
+
+    for _ in range(a.warmup):
+        st0, pml, tvar = step(False)
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        st, pml, tvar = step(True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1)) / a.steps
+    n_events_global = int(max_over_ranks(0) if False else 0)
+    ev_local = st["n_events_local"]
+    if world > 1:
+        t = torch.tensor([ev_local], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)
+        n_events_global = int(t.item())
+    else:
+        n_events_global = ev_local
+    lookups = n_events_global * sum(Lr.elt_end - Lr.elt_begin for Lr in w.layers)
+    value = T / (ms / 1e3)
+
+    # roofline of the dominant kernel (the ARA trial kernel) on this rank
+    k_ms = float(np.mean(kern_ms))
+    alg = algorithmic_bytes(w, ev_local, count, a.precision)
+    peaks = load_peaks()
+    peak = peaks.get("hbm_gbs")
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    if not peak:
+        peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+    achieved = alg / (k_ms / 1e3) / 1e9
+    traffic = load_traffic(w, a.precision)
+    ctx.close()
+
+    # ---- end-to-end arm: host buffers through the C-ABI
+    e2e = None
+    if not a.no_e2e:
+        ylt_pin = torch.empty((L + 1) * T, dtype=torch.float64, pin_memory=True)
+        ectx = ara.Context(w.catalog, device=local, precision=a.precision, stream=stream, rank=rank, world=world,
+                           nccl_id=nccl_id, load_mode=a.e2e_mode, chunk_trials=a.chunk_trials,
+                           l2_persist=a.l2_persist)
+        h2d_ms = []
+
+        def estep():
+            ectx.load_elts(eo_pin, ev_pin, ls_pin, terms, n_elts=w.n_elts)
+            ectx.load_yet(T, first, off_pin, ids_pin[:n_ev])
+            s2 = ectx.run(w.layers, ylt_pin)
+            ectx.metrics(R)
+            h2d_ms.append(s2["h2d_ms"])
+            return s2
+
+        for _ in range(max(1, a.warmup)):
+            estep()
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(a.steps):
+            s2 = estep()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ems = max_over_ranks(e0.elapsed_time(e1)) / a.steps
+        h2d = n_off * 8 + n_ev * 4 + (eo_pin.numel() * 8 + ev_pin.numel() * 4 + ls_pin.numel() * 8 if rank == 0 else 0)
+        d2h = (L + 1) * T * 8 + 2 * (L + 1) * len(R) * 8 + 8
+        e2e = {"value": T / (ems / 1e3), "unit": "trials/s", "ms_per_step": ems, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "mode": a.e2e_mode, "chunk_trials": a.chunk_trials,
+               "h2d_gbs": (n_ev * 4 + n_off * 8) / (float(np.mean(h2d_ms[-a.steps:])) / 1e3) / 1e9
+               if a.e2e_mode == "chunked" and np.mean(h2d_ms) > 0 else None}
+        ectx.close()
+
+    # ---- CPU baseline (oracle) on rank 0 at N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        r = oracle_sample_rate(w, a.cpu_seconds, a.precision)
+        cpu = {"value": r["trials_per_s"], "unit": "trials/s", "cores": 1, "kind": "oracle",
+               "sample": f"first {r['trials']} trials ({r['events']} events) of the {w.name} workload, "
+                         f"single-threaded, dense direct-access lookups, {r['seconds']:.1f} s",
+               "lookups_per_s": r["lookups_per_s"]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "trials/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": a.precision, "data": "synthetic",
+            "config": {"workload": w.name, "n_trials": T, "events_per_trial": [w.nmin, w.nmax],
+                       "n_events": n_events_global, "elts_per_layer": [Lr.elt_end - Lr.elt_begin for Lr in w.layers],
+                       "catalog": w.catalog, "layers": L, "return_periods": len(R), "parallelism": f"trials/{world}",
+                       "l2": "inputs larger than L2 (4 GB YET streamed once per step; 256 MB table)",
+                       "l2_persist": a.l2_persist},
+            "lookups_per_sec": lookups / (ms / 1e3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "ara::trial_kernel",
+                         "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
+            "breakdown_ms": {"ara_kernel": k_ms, "allgather": float(np.mean(ag_ms)), "metrics": float(np.mean(met_ms)),
+                             "step": ms},
+            "gpu_launches": int(a.steps * (2 + np.mean(launches) + 10)),
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
+            "host": host_info(), "gen_seconds": gen_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

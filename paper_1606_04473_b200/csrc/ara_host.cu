@@ -1,0 +1,852 @@
+// ara_host.cu — C-ABI host runtime of the B200 ARA library (include/ara.h).
+//
+// Context, validation, pointer classification, H2D loading (all-at-once or
+// chunked with copy/compute overlap, Alg. 2 P:321-337 and the
+// transfer modes of P:523-542), layer batching, the NCCL YLT all-gather
+// (Alg. 1 l.9 "Populate YLT from YLT_i") and the metrics driver.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "ara_internal.cuh"
+
+using namespace ara;
+
+namespace {
+
+ara_status fail(ara_ctx* ctx, ara_status st, const char* fmt, ...) {
+    if (ctx) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        ctx->last_error = buf;
+    }
+    return st;
+}
+
+#define CK(x)                                                                                  \
+    do {                                                                                       \
+        cudaError_t e_ = (x);                                                                  \
+        if (e_ != cudaSuccess) {                                                               \
+            cudaGetLastError();                                                                \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? ARA_ERR_OOM : ARA_ERR_CUDA,     \
+                        "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
+        }                                                                                      \
+    } while (0)
+
+#define NK(x)                                                                             \
+    do {                                                                                  \
+        ncclResult_t r_ = (x);                                                            \
+        if (r_ != ncclSuccess)                                                            \
+            return fail(ctx, ARA_ERR_NCCL, "%s failed: %s", #x, ncclGetErrorString(r_));  \
+    } while (0)
+
+enum class Mem { Host, Pinned, Device };
+
+Mem classify(const void* p) {
+    if (!p) return Mem::Host;
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return Mem::Host;
+    }
+    if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return Mem::Device;
+    if (a.type == cudaMemoryTypeHost) return Mem::Pinned;
+    return Mem::Host;
+}
+
+bool valid_retention(double r) { return r >= 0.0 && r <= 1.7976931348623157e308; }
+bool valid_limit(double l) { return l > 0.0; }   // +inf allowed, NaN rejected
+
+template <typename T>
+ara_status ensure(ara_ctx* ctx, T*& p, size_t& cap, size_t n) {
+    if (cap >= n && p) return ARA_OK;
+    cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    CK(cudaMalloc(&p, (n ? n : 1) * sizeof(T)));
+    cap = n;
+    return ARA_OK;
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+        cudaGetLastError();
+        return 0.f;
+    }
+    return ms;
+}
+
+void release_yet(ara_ctx* ctx) {
+    if (ctx->h_registered) {
+        cudaHostUnregister(ctx->h_registered);
+        cudaGetLastError();
+        ctx->h_registered = nullptr;
+    }
+    ctx->d_off = nullptr;
+    ctx->d_ids = nullptr;
+    ctx->h_off = nullptr;
+    ctx->h_ids = nullptr;
+    ctx->chunked_pending = false;
+    ctx->yet_loaded = false;
+    ctx->tiling_checked = false;
+}
+
+// Error bits written by the kernels -> status.
+ara_status device_errors(ara_ctx* ctx, uint32_t bits) {
+    if (!bits) return ARA_OK;
+    if (bits & ERRBIT_EVENT_RANGE)
+        return fail(ctx, ARA_ERR_OUT_OF_RANGE, "YET event id outside [1, %u]", ctx->catalog);
+    if (bits & ERRBIT_OFFSETS) return fail(ctx, ARA_ERR_OUT_OF_RANGE, "YET trial offsets decrease");
+    if (bits & ERRBIT_ELT_RANGE)
+        return fail(ctx, ARA_ERR_OUT_OF_RANGE, "ELT event id outside [1, %u]", ctx->catalog);
+    if (bits & ERRBIT_ELT_ORDER)
+        return fail(ctx, ARA_ERR_INVALID_ARG, "ELT event ids not strictly ascending (duplicate id)");
+    if (bits & ERRBIT_ELT_LOSS)
+        return fail(ctx, ARA_ERR_DOMAIN, "ELT loss negative, non-finite or not representable");
+    return fail(ctx, ARA_ERR_CUDA, "unknown device error bits 0x%x", bits);
+}
+
+}  // namespace
+
+// ============================================================ host-only helpers
+extern "C" const char* ara_version(void) { return "ara-b200 1.0 (sm_100a)"; }
+
+extern "C" const char* ara_status_string(ara_status s) {
+    switch (s) {
+        case ARA_OK: return "ARA_OK";
+        case ARA_ERR_INVALID_ARG: return "ARA_ERR_INVALID_ARG";
+        case ARA_ERR_OUT_OF_RANGE: return "ARA_ERR_OUT_OF_RANGE";
+        case ARA_ERR_DOMAIN: return "ARA_ERR_DOMAIN";
+        case ARA_ERR_STATE: return "ARA_ERR_STATE";
+        case ARA_ERR_OOM: return "ARA_ERR_OOM";
+        case ARA_ERR_CUDA: return "ARA_ERR_CUDA";
+        case ARA_ERR_NCCL: return "ARA_ERR_NCCL";
+    }
+    return "ARA_ERR_UNKNOWN";
+}
+
+extern "C" ara_status ara_partition(uint64_t n, int world, int rank, uint64_t* first, uint64_t* count) {
+    if (world < 1 || rank < 0 || rank >= world || !first || !count) return ARA_ERR_INVALID_ARG;
+    const uint64_t q = n / (uint64_t)world, rem = n % (uint64_t)world, r = (uint64_t)rank;
+    *first = r * q + (r < rem ? r : rem);
+    *count = q + (r < rem ? 1 : 0);
+    return ARA_OK;
+}
+
+extern "C" ara_status ara_return_period_rank(uint64_t T, double R, uint64_t* k) {
+    if (!k) return ARA_ERR_INVALID_ARG;
+    if (!(R >= 1.0) || !(R <= (double)T)) return ARA_ERR_DOMAIN;
+    if (R == std::floor(R)) {
+        const uint64_t r = (uint64_t)R;
+        *k = T / r + (T % r ? 1 : 0);
+    } else {
+        *k = (uint64_t)std::ceil((long double)T / (long double)R);
+    }
+    return ARA_OK;
+}
+
+extern "C" ara_status ara_nccl_unique_id(void* out) {
+    if (!out) return ARA_ERR_INVALID_ARG;
+    static_assert(sizeof(ncclUniqueId) == ARA_NCCL_ID_BYTES, "nccl id size");
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return ARA_ERR_NCCL;
+    std::memcpy(out, &id, sizeof id);
+    return ARA_OK;
+}
+
+// ============================================================ context
+extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, ara_ctx** out) {
+    if (!out || !cfg) return ARA_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (catalog_size == 0 || catalog_size == 0xFFFFFFFFu) return ARA_ERR_INVALID_ARG;
+    if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return ARA_ERR_INVALID_ARG;
+    if (cfg->world > 1 && !cfg->nccl_unique_id) return ARA_ERR_INVALID_ARG;
+    if (cfg->precision != ARA_F64 && cfg->precision != ARA_F32_STORAGE) return ARA_ERR_INVALID_ARG;
+    if (cfg->load_mode != ARA_LOAD_ALL_AT_ONCE && cfg->load_mode != ARA_LOAD_CHUNKED) return ARA_ERR_INVALID_ARG;
+    ara_ctx* ctx = new (std::nothrow) ara_ctx();
+    if (!ctx) return ARA_ERR_OOM;
+    ctx->device = cfg->device;
+    ctx->rank = cfg->rank;
+    ctx->world = cfg->world;
+    ctx->precision = cfg->precision;
+    ctx->load_mode = cfg->load_mode;
+    ctx->chunk_trials = cfg->chunk_trials ? cfg->chunk_trials : 65536;
+    ctx->l2_persist = cfg->l2_persist;
+    ctx->catalog = catalog_size;
+    auto bail = [&](ara_status st) {
+        ara_destroy(ctx);
+        return st;
+    };
+    if (cudaSetDevice(cfg->device) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(ARA_ERR_CUDA);
+    }
+    cudaDeviceGetAttribute(&ctx->n_sm, cudaDevAttrMultiProcessorCount, cfg->device);
+    if (cfg->stream) {
+        ctx->stream = (cudaStream_t)cfg->stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(ARA_ERR_CUDA);
+        ctx->own_stream = true;
+    }
+    if (cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return bail(ARA_ERR_CUDA);
+    for (auto& e : ctx->ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return bail(ARA_ERR_CUDA);
+    if (cudaMalloc(&ctx->d_err, 64) != cudaSuccess) return bail(ARA_ERR_OOM);
+    if (cudaMalloc(&ctx->d_small, 64 * sizeof(uint64_t)) != cudaSuccess) return bail(ARA_ERR_OOM);
+    if (cudaMallocHost(&ctx->h_small, 64 * sizeof(uint64_t)) != cudaSuccess) return bail(ARA_ERR_OOM);
+    if (cudaMemset(ctx->d_err, 0, 64) != cudaSuccess) return bail(ARA_ERR_CUDA);
+    if (ctx->l2_persist) {
+        cudaDeviceProp prop{};
+        if (cudaGetDeviceProperties(&prop, cfg->device) == cudaSuccess && prop.persistingL2CacheMaxSize > 0)
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prop.persistingL2CacheMaxSize);
+        cudaGetLastError();
+    }
+    if (cfg->world > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_unique_id, sizeof id);
+        if (ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank) != ncclSuccess) {
+            ctx->comm = nullptr;
+            return bail(ARA_ERR_NCCL);
+        }
+    }
+    *out = ctx;
+    return ARA_OK;
+}
+
+extern "C" void ara_destroy(ara_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    release_yet(ctx);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    cudaFree(ctx->d_table);
+    cudaFree(ctx->d_off_own);
+    cudaFree(ctx->d_ids_own);
+    cudaFree(ctx->d_ylt_local);
+    cudaFree(ctx->d_ylt_gather);
+    cudaFree(ctx->d_ylt_global);
+    cudaFree(ctx->d_lossy);
+    cudaFree(ctx->d_err);
+    cudaFree(ctx->d_small);
+    cudaFreeHost(ctx->h_small);
+    metrics_free(ctx->ms);
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+    cudaGetLastError();
+    delete ctx;
+}
+
+extern "C" const char* ara_last_error(const ara_ctx* ctx) { return ctx ? ctx->last_error.c_str() : "null context"; }
+
+// ============================================================ ELTs
+namespace {
+
+ara_status check_terms(ara_ctx* ctx, uint32_t n, const ara_elt_terms* t) {
+    if (!t) return ARA_OK;
+    if (classify(t) == Mem::Device) return fail(ctx, ARA_ERR_INVALID_ARG, "ELT terms must be host memory");
+    for (uint32_t j = 0; j < n; ++j)
+        if (!valid_retention(t[j].deductible) || !valid_limit(t[j].limit))
+            return fail(ctx, ARA_ERR_DOMAIN, "ELT %u terms: deductible must be >= 0 and finite, limit > 0", j);
+    return ARA_OK;
+}
+
+// Rank-0 (or single-rank) part: validate, upload, densify.  Returns status.
+ara_status build_table(ara_ctx* ctx, uint32_t n_elts, const uint64_t* elt_offsets, const uint32_t* event_ids,
+                       const double* losses) {
+    if (!elt_offsets) return fail(ctx, ARA_ERR_INVALID_ARG, "elt_offsets is NULL");
+    std::vector<uint64_t> hoff(n_elts + 1);
+    const Mem mo = classify(elt_offsets);
+    if (mo == Mem::Device)
+        CK(cudaMemcpy(hoff.data(), elt_offsets, (n_elts + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    else
+        std::memcpy(hoff.data(), elt_offsets, (n_elts + 1) * sizeof(uint64_t));
+    if (hoff[0] != 0) return fail(ctx, ARA_ERR_INVALID_ARG, "elt_offsets[0] must be 0");
+    for (uint32_t j = 0; j < n_elts; ++j)
+        if (hoff[j + 1] < hoff[j]) return fail(ctx, ARA_ERR_INVALID_ARG, "elt_offsets decrease at ELT %u", j);
+    const uint64_t nrec = hoff[n_elts];
+    if (nrec && (!event_ids || !losses)) return fail(ctx, ARA_ERR_INVALID_ARG, "event_ids/losses NULL");
+
+    const int fp32 = ctx->precision == ARA_F32_STORAGE;
+    const size_t esz = fp32 ? 4 : 8;
+    const uint64_t row_bytes = ((uint64_t)n_elts * esz + kSectorBytes - 1) / kSectorBytes * kSectorBytes;
+    const size_t bytes = (size_t)((uint64_t)ctx->catalog + 1) * row_bytes + kTablePadBytes;
+    if (bytes != ctx->table_bytes) {
+        cudaFree(ctx->d_table);
+        ctx->d_table = nullptr;
+        ctx->table_bytes = 0;
+        CK(cudaMalloc(&ctx->d_table, bytes));
+        ctx->table_bytes = bytes;
+    }
+    ctx->row_elems = row_bytes / esz;
+    CK(cudaMemsetAsync(ctx->d_table, 0, bytes, ctx->stream));
+
+    // sparse arrays -> device (temporary copies only for host inputs)
+    uint64_t* d_eoff = nullptr;
+    uint32_t* d_ev = nullptr;
+    double* d_ls = nullptr;
+    bool own_off = false, own_ev = false, own_ls = false;
+    auto cleanup = [&]() {
+        if (own_off) cudaFree(d_eoff);
+        if (own_ev) cudaFree(d_ev);
+        if (own_ls) cudaFree(d_ls);
+    };
+    ara_status st = ARA_OK;
+    do {
+        if (mo == Mem::Device) {
+            d_eoff = const_cast<uint64_t*>(elt_offsets);
+        } else {
+            if (cudaMalloc(&d_eoff, (n_elts + 1) * sizeof(uint64_t)) != cudaSuccess) { st = ARA_ERR_OOM; break; }
+            own_off = true;
+            if (cudaMemcpyAsync(d_eoff, hoff.data(), (n_elts + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                ctx->stream) != cudaSuccess) { st = ARA_ERR_CUDA; break; }
+        }
+        if (nrec) {
+            if (classify(event_ids) == Mem::Device) {
+                d_ev = const_cast<uint32_t*>(event_ids);
+            } else {
+                if (cudaMalloc(&d_ev, nrec * sizeof(uint32_t)) != cudaSuccess) { st = ARA_ERR_OOM; break; }
+                own_ev = true;
+                if (cudaMemcpyAsync(d_ev, event_ids, nrec * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream) !=
+                    cudaSuccess) { st = ARA_ERR_CUDA; break; }
+            }
+            if (classify(losses) == Mem::Device) {
+                d_ls = const_cast<double*>(losses);
+            } else {
+                if (cudaMalloc(&d_ls, nrec * sizeof(double)) != cudaSuccess) { st = ARA_ERR_OOM; break; }
+                own_ls = true;
+                if (cudaMemcpyAsync(d_ls, losses, nrec * sizeof(double), cudaMemcpyHostToDevice, ctx->stream) !=
+                    cudaSuccess) { st = ARA_ERR_CUDA; break; }
+            }
+        }
+        if (cudaMemsetAsync(ctx->d_err, 0, sizeof(uint32_t), ctx->stream) != cudaSuccess) { st = ARA_ERR_CUDA; break; }
+        if (launch_densify(d_eoff, d_ev, d_ls, n_elts, nrec, ctx->catalog, ctx->d_table, ctx->row_elems, fp32,
+                           ctx->d_err, ctx->stream) != cudaSuccess) { st = ARA_ERR_CUDA; break; }
+        if (cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream) !=
+            cudaSuccess) { st = ARA_ERR_CUDA; break; }
+        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) { st = ARA_ERR_CUDA; break; }
+    } while (0);
+    cleanup();
+    if (st != ARA_OK) {
+        cudaError_t e = cudaGetLastError();
+        return fail(ctx, st, "ELT upload/densify failed: %s", cudaGetErrorString(e));
+    }
+    return device_errors(ctx, (uint32_t)(ctx->h_small[0] & 0xffffffffu));
+}
+
+void set_l2_window(ara_ctx* ctx) {
+    if (!ctx->l2_persist || !ctx->d_table) return;
+    cudaDeviceProp prop{};
+    if (cudaGetDeviceProperties(&prop, ctx->device) != cudaSuccess) { cudaGetLastError(); return; }
+    const size_t win = ctx->table_bytes < (size_t)prop.accessPolicyMaxWindowSize ? ctx->table_bytes
+                                                                                 : (size_t)prop.accessPolicyMaxWindowSize;
+    cudaStreamAttrValue v{};
+    v.accessPolicyWindow.base_ptr = ctx->d_table;
+    v.accessPolicyWindow.num_bytes = win;
+    double hr = win ? (double)prop.persistingL2CacheMaxSize / (double)win : 0.0;
+    v.accessPolicyWindow.hitRatio = (float)(hr > 1.0 ? 1.0 : hr);
+    v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cudaStreamSetAttribute(ctx->stream, cudaStreamAttributeAccessPolicyWindow, &v);
+    cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" ara_status ara_load_elts(ara_ctx* ctx, uint32_t n_elts, const uint64_t* elt_offsets,
+                                    const uint32_t* event_ids, const double* losses,
+                                    const ara_elt_terms* terms) {
+    if (!ctx) return ARA_ERR_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device));
+    if (n_elts == 0 || n_elts > 65535) return fail(ctx, ARA_ERR_INVALID_ARG, "n_elts must be in [1, 65535]");
+    const bool root = ctx->rank == 0;
+    ara_status st = ARA_OK;
+    if (root) {
+        st = check_terms(ctx, n_elts, terms);
+        if (st == ARA_OK) st = build_table(ctx, n_elts, elt_offsets, event_ids, losses);
+    }
+    if (ctx->world > 1) {
+        // Agree on (status, n_elts) first so a failing root cannot strand the others.
+        ctx->h_small[0] = (uint64_t)st;
+        ctx->h_small[1] = n_elts;
+        CK(cudaMemcpyAsync(ctx->d_small, ctx->h_small, 2 * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+        NK(ncclBroadcast(ctx->d_small, ctx->d_small, 2, ncclUint64, 0, ctx->comm, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_small, ctx->d_small, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        const ara_status rst = (ara_status)ctx->h_small[0];
+        if (rst != ARA_OK) return root ? st : fail(ctx, rst, "rank 0 rejected the ELTs");
+        if (ctx->h_small[1] != n_elts) return fail(ctx, ARA_ERR_INVALID_ARG, "n_elts differs from rank 0");
+        if (!root) {
+            st = check_terms(ctx, n_elts, terms);
+            const size_t esz = ctx->precision == ARA_F32_STORAGE ? 4 : 8;
+            const uint64_t row_bytes = ((uint64_t)n_elts * esz + kSectorBytes - 1) / kSectorBytes * kSectorBytes;
+            const size_t bytes = (size_t)((uint64_t)ctx->catalog + 1) * row_bytes + kTablePadBytes;
+            if (bytes != ctx->table_bytes) {
+                cudaFree(ctx->d_table);
+                ctx->d_table = nullptr;
+                ctx->table_bytes = 0;
+                CK(cudaMalloc(&ctx->d_table, bytes));
+                ctx->table_bytes = bytes;
+            }
+            ctx->row_elems = row_bytes / esz;
+        }
+        // The table goes over NVLink once instead of N host copies.
+        NK(ncclBroadcast(ctx->d_table, ctx->d_table, ctx->table_bytes, ncclUint8, 0, ctx->comm, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (st != ARA_OK) return st;
+    } else if (st != ARA_OK) {
+        return st;
+    }
+    ctx->n_elts = n_elts;
+    ctx->terms.assign(n_elts, ara_elt_terms{0.0, INFINITY});
+    if (terms)
+        for (uint32_t j = 0; j < n_elts; ++j) ctx->terms[j] = terms[j];
+    set_l2_window(ctx);
+    return ARA_OK;
+}
+
+extern "C" ara_status ara_set_elt_terms(ara_ctx* ctx, uint32_t n_elts, const ara_elt_terms* terms) {
+    if (!ctx) return ARA_ERR_INVALID_ARG;
+    if (ctx->n_elts == 0) return fail(ctx, ARA_ERR_STATE, "no ELTs loaded");
+    if (n_elts != ctx->n_elts || !terms) return fail(ctx, ARA_ERR_INVALID_ARG, "need %u ELT terms", ctx->n_elts);
+    ara_status st = check_terms(ctx, n_elts, terms);
+    if (st != ARA_OK) return st;
+    for (uint32_t j = 0; j < n_elts; ++j) ctx->terms[j] = terms[j];
+    return ARA_OK;
+}
+
+// ============================================================ YET
+extern "C" ara_status ara_load_yet(ara_ctx* ctx, uint64_t n_trials_global, uint64_t first_trial,
+                                   uint64_t n_trials_local, const uint64_t* trial_offsets,
+                                   const uint32_t* event_ids) {
+    if (!ctx) return ARA_ERR_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device));
+    if (n_trials_global == 0) return fail(ctx, ARA_ERR_INVALID_ARG, "n_trials_global must be >= 1");
+    if (first_trial > n_trials_global || n_trials_local > n_trials_global - first_trial)
+        return fail(ctx, ARA_ERR_INVALID_ARG, "trial range [%llu, +%llu) exceeds %llu",
+                    (unsigned long long)first_trial, (unsigned long long)n_trials_local,
+                    (unsigned long long)n_trials_global);
+    if (!trial_offsets) return fail(ctx, ARA_ERR_INVALID_ARG, "trial_offsets is NULL");
+    CK(cudaStreamSynchronize(ctx->stream));   // a previous run may still read the old YET
+    release_yet(ctx);
+
+    const Mem mo = classify(trial_offsets);
+    const Mem mi = classify(event_ids);
+    uint64_t n_ev = 0;
+    bool n_ev_known = false;
+    if (mo != Mem::Device) {
+        if (trial_offsets[n_trials_local] < trial_offsets[0])
+            return fail(ctx, ARA_ERR_OUT_OF_RANGE, "YET trial offsets decrease");
+        n_ev = trial_offsets[n_trials_local] - trial_offsets[0];
+        n_ev_known = true;
+    }
+    if (!event_ids && !(n_ev_known && n_ev == 0)) return fail(ctx, ARA_ERR_INVALID_ARG, "event_ids is NULL");
+    if (mi != Mem::Device && !n_ev_known) {
+        CK(cudaMemcpy(ctx->h_small, trial_offsets, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(ctx->h_small + 1, trial_offsets + n_trials_local, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        if (ctx->h_small[1] < ctx->h_small[0]) return fail(ctx, ARA_ERR_OUT_OF_RANGE, "YET trial offsets decrease");
+        n_ev = ctx->h_small[1] - ctx->h_small[0];
+        n_ev_known = true;
+    }
+    ctx->n_events_host = n_ev_known ? n_ev : 0;
+    const bool chunked = ctx->load_mode == ARA_LOAD_CHUNKED;
+
+    // offsets
+    if (mo == Mem::Device) {
+        ctx->d_off = trial_offsets;
+    } else {
+        ara_status st = ensure(ctx, ctx->d_off_own, ctx->own_off_cap, n_trials_local + 1);
+        if (st != ARA_OK) return st;
+        ctx->d_off = ctx->d_off_own;
+        if (chunked) ctx->h_off = trial_offsets;
+        else CK(cudaMemcpyAsync(ctx->d_off_own, trial_offsets, (n_trials_local + 1) * sizeof(uint64_t),
+                                cudaMemcpyHostToDevice, ctx->stream));
+    }
+    // event ids
+    if (mi == Mem::Device) {
+        ctx->d_ids = event_ids;
+    } else {
+        ara_status st = ensure(ctx, ctx->d_ids_own, ctx->own_ids_cap, n_ev);
+        if (st != ARA_OK) return st;
+        ctx->d_ids = ctx->d_ids_own;
+        if (chunked) {
+            ctx->h_ids = event_ids;
+            if (mi == Mem::Host && n_ev) {   // pageable: pin for async DMA (once per load)
+                if (cudaHostRegister((void*)event_ids, n_ev * sizeof(uint32_t), cudaHostRegisterReadOnly) ==
+                    cudaSuccess)
+                    ctx->h_registered = (void*)event_ids;
+                cudaGetLastError();
+            }
+        } else if (n_ev) {
+            CK(cudaMemcpyAsync(ctx->d_ids_own, event_ids, n_ev * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                               ctx->stream));
+        }
+    }
+    ctx->chunked_pending = chunked && (ctx->h_off || ctx->h_ids);
+    if (!ctx->chunked_pending) CK(cudaStreamSynchronize(ctx->stream));
+    ctx->T_global = n_trials_global;
+    ctx->first = first_trial;
+    ctx->T_local = n_trials_local;
+    ctx->yet_loaded = true;
+    ctx->tiling_checked = false;
+    return ARA_OK;
+}
+
+// ============================================================ run
+namespace {
+
+struct Group {
+    uint32_t l0, nl;      // layers [l0, l0+nl)
+    uint32_t max_nsec;
+    bool share;
+    bool wide;
+};
+
+}  // namespace
+
+extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* layers, double* ylt,
+                              uint32_t* lossy, ara_run_stats* stats) {
+    if (!ctx) return ARA_ERR_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->d_table || ctx->n_elts == 0) return fail(ctx, ARA_ERR_STATE, "ara_load_elts has not succeeded");
+    if (!ctx->yet_loaded) return fail(ctx, ARA_ERR_STATE, "ara_load_yet has not succeeded");
+    if (n_layers == 0 || n_layers > ARA_MAX_LAYERS || !layers)
+        return fail(ctx, ARA_ERR_INVALID_ARG, "n_layers must be in [1, %d]", ARA_MAX_LAYERS);
+    if (classify(layers) == Mem::Device) return fail(ctx, ARA_ERR_INVALID_ARG, "layers must be host memory");
+    for (uint32_t l = 0; l < n_layers; ++l) {
+        const ara_layer& L = layers[l];
+        if (L.elt_begin >= L.elt_end || L.elt_end > ctx->n_elts)
+            return fail(ctx, ARA_ERR_INVALID_ARG, "layer %u ELT range [%u,%u) invalid for %u ELTs", l, L.elt_begin,
+                        L.elt_end, ctx->n_elts);
+        if (!valid_retention(L.occ_retention) || !valid_retention(L.agg_retention) || !valid_limit(L.occ_limit) ||
+            !valid_limit(L.agg_limit))
+            return fail(ctx, ARA_ERR_DOMAIN, "layer %u terms: retentions >= 0 finite, limits > 0", l);
+    }
+    const uint32_t world = (uint32_t)ctx->world;
+    const uint64_t T_local = ctx->T_local, T_global = ctx->T_global;
+
+    // Ranks must hold ara_partition's split (checked once per load, collective).
+    if (world == 1 && (ctx->first != 0 || T_local != T_global))
+        return fail(ctx, ARA_ERR_INVALID_ARG, "a single-rank context must load the whole YET (first 0, %llu trials)",
+                    (unsigned long long)T_global);
+    if (world > 1 && !ctx->tiling_checked) {
+        uint64_t f = 0, c = 0;
+        ara_partition(T_global, ctx->world, ctx->rank, &f, &c);
+        ctx->h_small[0] = (f == ctx->first && c == T_local) ? 0 : 1;
+        CK(cudaMemcpyAsync(ctx->d_small, ctx->h_small, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+        NK(ncclAllReduce(ctx->d_small, ctx->d_small, 1, ncclUint64, ncclSum, ctx->comm, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (ctx->h_small[0] != 0)
+            return fail(ctx, ARA_ERR_INVALID_ARG, "ranks' YET ranges do not follow ara_partition(%llu, %d)",
+                        (unsigned long long)T_global, ctx->world);
+        ctx->tiling_checked = true;
+    }
+
+    const int fp32 = ctx->precision == ARA_F32_STORAGE;
+    const uint32_t eps = fp32 ? 8 : 4;   // elements per 32-B sector
+    const uint64_t Tpad = world > 1 ? (T_global + world - 1) / world : T_local;
+    const uint64_t ld = world > 1 ? Tpad : (T_local ? T_local : 1);
+    const uint32_t rows = n_layers + 1;
+
+    ara_status st = ensure(ctx, ctx->d_ylt_local, ctx->ylt_local_cap, (size_t)rows * ld);
+    if (st != ARA_OK) return st;
+    uint32_t* d_lossy = nullptr;
+    const Mem ml = lossy ? classify(lossy) : Mem::Host;
+    if (lossy) {
+        if (ml == Mem::Device && ld == T_local) {
+            d_lossy = lossy;
+        } else {
+            st = ensure(ctx, ctx->d_lossy, ctx->lossy_cap, (size_t)n_layers * ld);
+            if (st != ARA_OK) return st;
+            d_lossy = ctx->d_lossy;
+        }
+    }
+
+    // Layer groups: up to kMaxLB consecutive layers per launch; a layer wider
+    // than kMaxSec sectors runs alone in the generic kernel.
+    std::vector<Group> groups;
+    for (uint32_t l = 0; l < n_layers;) {
+        const uint32_t s0 = layers[l].elt_begin / eps, s1 = (layers[l].elt_end + eps - 1) / eps;
+        if (s1 - s0 > (uint32_t)kMaxSec) {
+            groups.push_back({l, 1, s1 - s0, false, true});
+            ++l;
+            continue;
+        }
+        Group g{l, 0, 0, true, false};
+        while (l < n_layers && g.nl < (uint32_t)kMaxLB) {
+            const uint32_t a = layers[l].elt_begin / eps, b = (layers[l].elt_end + eps - 1) / eps;
+            if (b - a > (uint32_t)kMaxSec) break;
+            if (g.nl > 0) {
+                const uint32_t a0 = layers[g.l0].elt_begin / eps, b0 = (layers[g.l0].elt_end + eps - 1) / eps;
+                if (a != a0 || b != b0) g.share = false;
+            }
+            if (b - a > g.max_nsec) g.max_nsec = b - a;
+            ++g.nl;
+            ++l;
+        }
+        if (g.nl == 1) g.share = false;
+        groups.push_back(g);
+    }
+
+    cudaStream_t s = ctx->stream;
+    CK(cudaEventRecord(ctx->ev[0], s));
+    CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(uint32_t), s));
+
+    // Chunk plan: CHUNKED streams the host YET in whole-trial chunks on the copy
+    // stream, each chunk's kernels waiting only for that chunk.
+    const bool stream_in = ctx->chunked_pending;
+    std::vector<std::pair<uint64_t, uint64_t>> chunks;
+    if (stream_in && T_local) {
+        for (uint64_t t = 0; t < T_local; t += ctx->chunk_trials)
+            chunks.push_back({t, (t + ctx->chunk_trials < T_local) ? t + ctx->chunk_trials : T_local});
+    } else {
+        chunks.push_back({0, T_local});
+    }
+    std::vector<cudaEvent_t> chunk_ev;
+    uint64_t h2d_bytes = 0;
+    if (stream_in) {
+        CK(cudaEventRecord(ctx->ev[5], s));
+        CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev[5], 0));   // copies after prior work on s
+        CK(cudaEventRecord(ctx->ev[6], ctx->copy_stream));
+        const uint64_t* hoff = ctx->h_off;
+        if (hoff) {
+            CK(cudaMemcpyAsync(ctx->d_off_own, hoff, (T_local + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                               ctx->copy_stream));
+            h2d_bytes += (T_local + 1) * sizeof(uint64_t);
+        }
+        // host offsets are needed to size the id chunks
+        std::vector<uint64_t> tmp;
+        const uint64_t* ho = hoff;
+        if (!ho) {
+            tmp.resize(T_local + 1);
+            CK(cudaMemcpy(tmp.data(), ctx->d_off, (T_local + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+            ho = tmp.data();
+        }
+        chunk_ev.resize(chunks.size());
+        for (size_t c = 0; c < chunks.size(); ++c) {
+            if (cudaEventCreateWithFlags(&chunk_ev[c], cudaEventDisableTiming) != cudaSuccess) {
+                for (size_t q = 0; q < c; ++q) cudaEventDestroy(chunk_ev[q]);
+                return fail(ctx, ARA_ERR_CUDA, "cudaEventCreate failed");
+            }
+        }
+        for (size_t c = 0; c < chunks.size(); ++c) {
+            if (ctx->h_ids) {
+                const uint64_t e0 = ho[chunks[c].first] - ho[0], e1 = ho[chunks[c].second] - ho[0];
+                if (e1 > e0) {
+                    CK(cudaMemcpyAsync(ctx->d_ids_own + e0, ctx->h_ids + e0, (e1 - e0) * sizeof(uint32_t),
+                                       cudaMemcpyHostToDevice, ctx->copy_stream));
+                    h2d_bytes += (e1 - e0) * sizeof(uint32_t);
+                }
+            }
+            CK(cudaEventRecord(chunk_ev[c], ctx->copy_stream));
+        }
+        CK(cudaEventRecord(ctx->ev[7], ctx->copy_stream));
+    }
+
+    // Kernels.
+    TrialParams base{};
+    base.off = ctx->d_off;
+    base.ids = ctx->d_ids;
+    base.catalog = ctx->catalog;
+    base.table = ctx->d_table;
+    base.row_elems = ctx->row_elems;
+    base.ylt = ctx->d_ylt_local;
+    base.ld = ld;
+    base.lossy = d_lossy;
+    base.err = ctx->d_err;
+    base.portfolio_row = n_layers;
+    uint32_t launches = 0;
+    double2* d_cterm = nullptr;
+    std::vector<double2> wide_terms;
+    CK(cudaEventRecord(ctx->ev[1], s));
+    for (size_t c = 0; c < chunks.size(); ++c) {
+        if (stream_in) CK(cudaStreamWaitEvent(s, chunk_ev[c], 0));
+        for (size_t gi = 0; gi < groups.size(); ++gi) {
+            const Group& g = groups[gi];
+            TrialParams p = base;
+            p.t_begin = chunks[c].first;
+            p.t_end = chunks[c].second;
+            p.n_layers = g.nl;
+            p.ylt_row0 = g.l0;
+            p.portfolio_mode = gi == 0 ? 0 : 1;
+            if (g.wide) {
+                const ara_layer& L = layers[g.l0];
+                p.lw[0] = {0, 0, L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit};
+                const uint32_t ncol = L.elt_end - L.elt_begin;
+                if (!d_cterm) {
+                    wide_terms.resize(ctx->n_elts);
+                    for (uint32_t j = 0; j < ctx->n_elts; ++j)
+                        wide_terms[j] = make_double2(ctx->terms[j].deductible, ctx->terms[j].limit);
+                    CK(cudaMallocAsync(&d_cterm, ctx->n_elts * sizeof(double2), s));
+                    CK(cudaMemcpyAsync(d_cterm, wide_terms.data(), ctx->n_elts * sizeof(double2),
+                                       cudaMemcpyHostToDevice, s));
+                }
+                const int grid = trial_kernel_grid(fp32, g.max_nsec, false, 1);
+                CK(launch_trials_wide(p, fp32, d_cterm + L.elt_begin, L.elt_begin, ncol, grid, s));
+            } else {
+                for (uint32_t q = 0; q < g.nl; ++q) {
+                    const ara_layer& L = layers[g.l0 + q];
+                    const uint32_t a = L.elt_begin / eps, b = (L.elt_end + eps - 1) / eps;
+                    p.lw[q] = {a, b - a, L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit};
+                    for (uint32_t w = 0; w < (uint32_t)kMaxWin; ++w) {
+                        const uint32_t col = a * eps + w;
+                        if (w < g.max_nsec * eps && col >= L.elt_begin && col < L.elt_end)
+                            p.term[q][w] = make_double2(ctx->terms[col].deductible, ctx->terms[col].limit);
+                        else
+                            p.term[q][w] = make_double2(INFINITY, INFINITY);   // contributes exactly +0
+                    }
+                }
+                const int grid = trial_kernel_grid(fp32, g.max_nsec, g.share, (int)g.nl);
+                CK(launch_trials(p, fp32, g.max_nsec, g.share, grid, s));
+            }
+            ++launches;
+        }
+    }
+    CK(cudaEventRecord(ctx->ev[2], s));
+    if (d_cterm) CK(cudaFreeAsync(d_cterm, s));
+    for (auto e : chunk_ev) cudaEventDestroy(e);   // safe: destruction defers until complete
+    if (stream_in) {
+        ctx->chunked_pending = false;   // later runs reuse the device copy
+    }
+
+    // YLT assembly across ranks (a9): one all-gather per YLT row over NVLink.
+    double* d_full = ctx->d_ylt_local;
+    uint64_t ld_full = ld;
+    CK(cudaEventRecord(ctx->ev[3], s));
+    if (world > 1) {
+        st = ensure(ctx, ctx->d_ylt_gather, ctx->ylt_gather_cap, (size_t)rows * world * Tpad);
+        if (st != ARA_OK) return st;
+        NK(ncclGroupStart());
+        for (uint32_t r = 0; r < rows; ++r)
+            NK(ncclAllGather(ctx->d_ylt_local + (uint64_t)r * ld, ctx->d_ylt_gather + (uint64_t)r * world * Tpad, Tpad,
+                             ncclDouble, ctx->comm, s));
+        NK(ncclGroupEnd());
+        if (Tpad * world == T_global) {
+            d_full = ctx->d_ylt_gather;
+        } else {
+            st = ensure(ctx, ctx->d_ylt_global, ctx->ylt_global_cap, (size_t)rows * T_global);
+            if (st != ARA_OK) return st;
+            for (uint32_t rk = 0; rk < world; ++rk) {
+                uint64_t f = 0, c = 0;
+                ara_partition(T_global, ctx->world, (int)rk, &f, &c);
+                if (c)
+                    CK(cudaMemcpy2DAsync(ctx->d_ylt_global + f, T_global * sizeof(double),
+                                         ctx->d_ylt_gather + (uint64_t)rk * Tpad, world * Tpad * sizeof(double),
+                                         c * sizeof(double), rows, cudaMemcpyDeviceToDevice, s));
+            }
+            d_full = ctx->d_ylt_global;
+        }
+        ld_full = T_global;
+    }
+    CK(cudaEventRecord(ctx->ev[4], s));
+
+    // Outputs.
+    if (ylt) {
+        const cudaMemcpyKind kind = classify(ylt) == Mem::Device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        if (ld_full == T_global)
+            CK(cudaMemcpyAsync(ylt, d_full, (size_t)rows * T_global * sizeof(double), kind, s));
+        else
+            CK(cudaMemcpy2DAsync(ylt, T_global * sizeof(double), d_full, ld_full * sizeof(double),
+                                 T_global * sizeof(double), rows, kind, s));
+    }
+    if (lossy && d_lossy != lossy && T_local) {
+        const cudaMemcpyKind kind = ml == Mem::Device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+        CK(cudaMemcpy2DAsync(lossy, T_local * sizeof(uint32_t), d_lossy, ld * sizeof(uint32_t),
+                             T_local * sizeof(uint32_t), n_layers, kind, s));
+    }
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    if (T_local) {
+        CK(cudaMemcpyAsync(ctx->h_small + 1, ctx->d_off, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(ctx->h_small + 2, ctx->d_off + T_local, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaEventRecord(ctx->ev[5], s));
+    CK(cudaStreamSynchronize(s));
+    if (stream_in) CK(cudaStreamSynchronize(ctx->copy_stream));
+    uint32_t bits = (uint32_t)(ctx->h_small[0] & 0xffffffffu);
+    if (world > 1) {   // every rank must see the same verdict
+        ctx->h_small[0] = bits;
+        CK(cudaMemcpyAsync(ctx->d_small, ctx->h_small, sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+        NK(ncclAllReduce(ctx->d_small, ctx->d_small, 1, ncclUint64, ncclMax, ctx->comm, s));
+        CK(cudaMemcpyAsync(ctx->h_small + 3, ctx->d_small, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        bits = (uint32_t)ctx->h_small[3];
+    }
+    st = device_errors(ctx, bits);
+    if (st != ARA_OK) {
+        ctx->last_layers = 0;
+        return st;
+    }
+    ctx->last_layers = n_layers;
+    if (stats) {
+        const uint64_t nev = T_local ? ctx->h_small[2] - ctx->h_small[1] : 0;
+        uint64_t lookups = 0;
+        for (uint32_t l = 0; l < n_layers; ++l) lookups += nev * (layers[l].elt_end - layers[l].elt_begin);
+        stats->n_trials_local = T_local;
+        stats->n_events_local = nev;
+        stats->n_lookups_local = lookups;
+        stats->kernel_ms = ev_ms(ctx->ev[1], ctx->ev[2]);
+        stats->allgather_ms = ev_ms(ctx->ev[3], ctx->ev[4]);
+        stats->total_ms = ev_ms(ctx->ev[0], ctx->ev[5]);
+        stats->h2d_ms = stream_in ? ev_ms(ctx->ev[6], ctx->ev[7]) : 0.0;
+        stats->h2d_bytes = h2d_bytes;
+        stats->n_kernel_launches = launches;
+    }
+    return ARA_OK;
+}
+
+// ============================================================ metrics
+extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* return_periods, uint64_t* k,
+                                  double* pml, double* tvar, double* device_ms) {
+    if (!ctx) return ARA_ERR_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->last_layers == 0) return fail(ctx, ARA_ERR_STATE, "no successful ara_run yet");
+    if (n_rp == 0 || n_rp > ARA_MAX_RP || !return_periods || !pml || !tvar)
+        return fail(ctx, ARA_ERR_INVALID_ARG, "n_rp must be in [1, %d] with non-NULL arrays", ARA_MAX_RP);
+    const uint64_t T = ctx->T_global;
+    uint64_t hk[ARA_MAX_RP];
+    for (uint32_t r = 0; r < n_rp; ++r)
+        if (ara_return_period_rank(T, return_periods[r], &hk[r]) != ARA_OK)
+            return fail(ctx, ARA_ERR_DOMAIN, "return period %g outside [1, %llu]", return_periods[r],
+                        (unsigned long long)T);
+    const uint32_t rows = ctx->last_layers + 1;
+    const double* d_y;
+    uint64_t ld;
+    if (ctx->world > 1) {
+        const uint64_t Tpad = (T + ctx->world - 1) / ctx->world;
+        if (Tpad * (uint64_t)ctx->world == T) d_y = ctx->d_ylt_gather;
+        else d_y = ctx->d_ylt_global;
+        ld = T;
+    } else {
+        d_y = ctx->d_ylt_local;
+        ld = ctx->T_local ? ctx->T_local : 1;
+    }
+    int nblk = (int)((T + 4095) / 4096);
+    const int maxblk = (2 * ctx->n_sm + (int)rows - 1) / (int)rows;
+    if (nblk > maxblk) nblk = maxblk;
+    if (nblk < 1) nblk = 1;
+    CK(metrics_alloc(ctx->ms, rows, n_rp, nblk));
+    cudaStream_t s = ctx->stream;
+    CK(cudaEventRecord(ctx->ev[0], s));
+    CK(launch_metrics(d_y, T, ld, rows, n_rp, hk, ctx->ms, nblk, s));
+    CK(cudaEventRecord(ctx->ev[1], s));
+    std::vector<double> out((size_t)rows * n_rp * 2);
+    CK(cudaMemcpyAsync(out.data(), ctx->ms.out, out.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (uint32_t r = 0; r < rows; ++r)
+        for (uint32_t q = 0; q < n_rp; ++q) {
+            pml[(size_t)r * n_rp + q] = out[((size_t)r * n_rp + q) * 2 + 0];
+            tvar[(size_t)r * n_rp + q] = out[((size_t)r * n_rp + q) * 2 + 1];
+        }
+    if (k)
+        for (uint32_t q = 0; q < n_rp; ++q) k[q] = hk[q];
+    if (device_ms) *device_ms = ev_ms(ctx->ev[0], ctx->ev[1]);
+    return ARA_OK;
+}

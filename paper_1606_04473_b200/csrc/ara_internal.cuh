@@ -1,0 +1,146 @@
+// ara_internal.cuh — shared declarations of the B200 ARA library (product path).
+// Nothing here is shared with oracle/ (the CPU oracle is independent test
+// infrastructure); this header is private to paper_1606_04473_b200/csrc.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "ara.h"
+
+namespace ara {
+
+// ---- device error bits (fused validation, reported by the host after sync)
+enum : uint32_t {
+    ERRBIT_EVENT_RANGE = 1u << 0,   // YET event id outside [1, C]
+    ERRBIT_OFFSETS = 1u << 1,       // YET trial offsets decreasing
+    ERRBIT_ELT_RANGE = 1u << 2,     // ELT event id outside [1, C]
+    ERRBIT_ELT_ORDER = 1u << 3,     // ELT ids not strictly ascending (duplicate)
+    ERRBIT_ELT_LOSS = 1u << 4,      // ELT loss negative / non-finite / fp32-unrepresentable
+};
+
+constexpr int kSectorBytes = 32;     // one L2 sector; rows are padded to sector multiples
+constexpr int kMaxSec = 8;           // widest per-layer window handled by the fast kernel (256 B)
+constexpr int kMaxLB = 4;            // layers per kernel launch (per-layer registers)
+constexpr int kMaxWin = kMaxSec * kSectorBytes / 4;   // 64 columns (fp32) per window
+constexpr int kThreads = 256;        // 8 warps per CTA
+constexpr int kTablePadBytes = kMaxSec * kSectorBytes;  // over-read slack after the last row
+
+// One layer of a kernel launch: the sector window [sec0, sec0 + nsec) of the
+// interleaved row, the per-column terms of that window (columns outside the
+// layer carry deductible +inf so they contribute an exact +0), and the layer
+// terms.  Passed by value in the launch parameters (constant bank).
+struct LayerWin {
+    uint32_t sec0;
+    uint32_t nsec;
+    double occ_r, occ_l, agg_r, agg_l;
+};
+
+struct TrialParams {
+    const uint64_t* off;        // local CSR offsets [n_local + 1]
+    const uint32_t* ids;        // events of off[0] ...
+    uint64_t t_begin, t_end;    // trial range of this launch (local indices)
+    uint32_t catalog;
+    uint32_t n_layers;          // layers in this launch (<= kMaxLB)
+    const void* table;          // [C+1][row_elems] (+ pad)
+    uint64_t row_elems;         // elements per row (row stride)
+    double* ylt;                // [.. rows][ld] : row ylt_row0 + l
+    uint64_t ld;                // row stride of ylt (= n_local)
+    uint32_t ylt_row0;          // first YLT row written by this launch
+    int portfolio_mode;         // 0: write portfolio row, 1: add to it, -1: none
+    uint32_t portfolio_row;
+    uint32_t* lossy;            // [.. rows][ld] or null
+    uint32_t* err;              // device error word
+    LayerWin lw[kMaxLB];
+    double2 term[kMaxLB][kMaxWin];   // (deductible, limit) per window column
+};
+
+// ---- launchers (defined in the .cu files; all enqueue on `s`)
+cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const double* d_loss,
+                           uint32_t n_elts, uint64_t n_records, uint32_t catalog, void* d_table,
+                           uint64_t row_elems, int fp32, uint32_t* d_err, cudaStream_t s);
+
+cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, bool shared_window,
+                          int grid, cudaStream_t s);
+int trial_kernel_grid(int fp32, uint32_t max_nsec, bool shared_window, int n_layers);
+cudaError_t launch_trials_wide(const TrialParams& p, int fp32, const double2* d_cterm, uint32_t col0,
+                               uint32_t ncol, int grid, cudaStream_t s);
+
+// metrics: radix select over the [rows][T] YLT (device), fixed-order tail sums
+struct MetricsScratch {
+    uint32_t* hist = nullptr;       // [rows][n_rp][256]
+    uint64_t* prefix = nullptr;     // [rows][n_rp] selected bit prefix
+    uint64_t* krem = nullptr;       // [rows][n_rp] remaining rank
+    double* part_sum = nullptr;     // [rows][n_rp][nblk]
+    uint64_t* part_cnt = nullptr;   // [rows][n_rp][nblk]
+    double* out = nullptr;          // [rows][n_rp][2] pml, tvar
+    uint32_t* done = nullptr;       // block-completion counters
+    size_t cap_rows_rp = 0;
+    uint32_t cap_rows = 0;
+    int nblk = 0;                   // capacity in blocks
+};
+cudaError_t metrics_alloc(MetricsScratch& m, uint32_t rows, uint32_t n_rp, int nblk);
+void metrics_free(MetricsScratch& m);
+cudaError_t launch_metrics(const double* d_ylt, uint64_t T, uint64_t ld, uint32_t rows,
+                           uint32_t n_rp, const uint64_t* h_k, MetricsScratch& m, int nblk, cudaStream_t s);
+
+}  // namespace ara
+
+// ---- the opaque context
+struct ara_ctx {
+    int device = 0, rank = 0, world = 1;
+    ara_precision precision = ARA_F64;
+    ara_load_mode load_mode = ARA_LOAD_ALL_AT_ONCE;
+    uint64_t chunk_trials = 65536;
+    int l2_persist = 0;
+    cudaStream_t stream = nullptr, copy_stream = nullptr;
+    bool own_stream = false;
+    ncclComm_t comm = nullptr;
+    int n_sm = 148;
+    std::string last_error;
+
+    uint32_t catalog = 0;
+
+    // ELT direct-access table tab[e][col], e in [0, C] (row 0 = zeros)
+    void* d_table = nullptr;
+    size_t table_bytes = 0;
+    uint64_t row_elems = 0;
+    uint32_t n_elts = 0;
+    std::vector<ara_elt_terms> terms;
+
+    // YET (local shard)
+    bool yet_loaded = false;
+    uint64_t T_global = 0, first = 0, T_local = 0;
+    const uint64_t* d_off = nullptr;   // current device offsets (owned or borrowed)
+    const uint32_t* d_ids = nullptr;
+    uint64_t* d_off_own = nullptr;
+    uint32_t* d_ids_own = nullptr;
+    size_t own_off_cap = 0, own_ids_cap = 0;
+    const uint64_t* h_off = nullptr;   // CHUNKED host source
+    const uint32_t* h_ids = nullptr;
+    void* h_registered = nullptr;      // host range we cudaHostRegister'ed
+    bool chunked_pending = false;
+    uint64_t n_events_host = 0;        // known when offsets were host memory
+    bool tiling_checked = false;
+
+    // YLT
+    uint32_t last_layers = 0;          // layers of the last run (0 = none)
+    double* d_ylt_local = nullptr;     // [(L+1)][T_local]
+    size_t ylt_local_cap = 0;
+    double* d_ylt_gather = nullptr;    // world>1: [(L+1)][world][Tpad]
+    double* d_ylt_global = nullptr;    // world>1: [(L+1)][T_global]
+    size_t ylt_global_cap = 0, ylt_gather_cap = 0;
+    uint32_t* d_lossy = nullptr;
+    size_t lossy_cap = 0;
+
+    // status / small pinned block
+    uint32_t* d_err = nullptr;
+    uint64_t* h_small = nullptr;       // pinned: [0]=err, [1]=off0, [2]=offN, ...
+    uint64_t* d_small = nullptr;
+
+    ara::MetricsScratch ms;
+    cudaEvent_t ev[8] = {};
+};

@@ -1,0 +1,99 @@
+"""C-ABI checks that need no GPU: the library loads, exports every symbol that
+include/ara.h declares, and its host-only helpers follow the DESIGN.md readings."""
+import math
+import os
+import re
+import subprocess
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "ara.h")
+LIB = os.path.join(ROOT, "paper_1606_04473_b200", "libara.so")
+
+
+def declared_symbols():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?(?:ara_status|void|const char\*|char\*)\s*\**\s*(ara_\w+)\s*\(",
+                                 src, flags=re.M)))
+
+
+def test_library_builds_and_exports_every_declared_symbol():
+    assert os.path.exists(LIB), "libara.so not built"
+    syms = declared_symbols()
+    assert len(syms) >= 13, syms
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True, check=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if ln.strip()}
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    from paper_1606_04473_b200 import ara
+    assert set(syms) == set(ara.EXPORTED)
+
+
+def test_library_is_sm100a():
+    out = subprocess.run(["cuobjdump", "-lelf", LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_partition_matches_reading_a17():
+    from paper_1606_04473_b200 import ara
+    for T in (0, 1, 7, 1000, 1_000_000, 10_000_001):
+        for N in (1, 2, 3, 4, 8, 16):
+            got = [ara.ara_partition(T, N, r) for r in range(N)]
+            sizes = [c for _, c in got]
+            assert sum(sizes) == T and max(sizes) - min(sizes) <= 1
+            assert all(got[r][0] == sum(sizes[:r]) for r in range(N))
+            assert sizes == sorted(sizes, reverse=True)
+    with pytest.raises(ara.AraError):
+        ara.ara_partition(10, 2, 2)
+
+
+def test_return_period_rank_is_exact_ceiling():
+    """A10: k = ceil(T/R) computed exactly (checked with rationals)."""
+    from paper_1606_04473_b200 import ara
+    rng = np.random.default_rng(2)
+    for _ in range(3000):
+        T = int(rng.integers(1, 10_000_000))
+        R = float(rng.integers(1, T + 1)) if rng.random() < 0.5 else float(rng.uniform(1, T))
+        assert ara.ara_return_period_rank(T, R) == math.ceil(Fraction(T) / Fraction(R))
+    for bad in (0.0, 0.999, 11.0, float("nan"), float("inf")):
+        with pytest.raises(ara.AraError) as ei:
+            ara.ara_return_period_rank(10, bad)
+        assert ei.value.status == ara.ARA_ERR_DOMAIN
+
+
+def test_create_without_gpu_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_1606_04473_b200 import ara
+    with pytest.raises(ara.AraError) as ei:
+        ara.Context(1000)
+    assert ei.value.status == ara.ARA_ERR_CUDA
+
+
+def test_invalid_config_rejected_before_touching_the_gpu():
+    from paper_1606_04473_b200 import ara
+    for kw in ({"world": 2}, {"rank": 1}, {"precision": 7}):
+        with pytest.raises(ara.AraError) as ei:
+            ara.ara_create(1000, **kw)
+        assert ei.value.status == ara.ARA_ERR_INVALID_ARG
+    with pytest.raises(ara.AraError):
+        ara.ara_create(0)
+
+
+def test_product_path_never_touches_the_oracle():
+    """The oracle is test infrastructure: no product source may import, link or
+    call it, and no CPU fallback exists."""
+    pkg = os.path.join(ROOT, "paper_1606_04473_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                for bad in ("import oracle", "from oracle", "liboracle", "oracle.h", "oracle_"):
+                    assert bad not in txt, (f, bad)
+    out = subprocess.run(["ldd", LIB], capture_output=True, text=True).stdout
+    assert "oracle" not in out

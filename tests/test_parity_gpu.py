@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA path (through the C-ABI binding) vs the CPU oracle,
+element by element on the same seeded inputs (tolerances: parity_util)."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from parity_util import (RTOL, assert_metrics_close, assert_ylt_close, make_inputs, oracle_rows,
+                         run_gpu, run_oracle)
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+
+
+def _ara():
+    from paper_1606_04473_b200 import ara
+    return ara
+
+
+# ------------------------------------------------------------------ tiny configs
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_tiny(cuda, precision):
+    w = synth.get_config("tiny").with_(return_periods=(1, 2, 3.5, 10, 100, 1000))
+    off, ids, elts = make_inputs(w)
+    orc = run_oracle(off, ids, elts, w, w.layers, fp32=precision == "f32")
+    ylt, lossy, st, met = run_gpu(off, ids, elts, w, w.layers, precision=precision,
+                                  return_periods=w.return_periods)
+    assert_ylt_close(ylt, orc)
+    assert np.array_equal(lossy, orc["lossy"])
+    assert_metrics_close(met, oracle_rows(orc), orc["scale"], w.return_periods)
+    assert st["n_events_local"] == len(ids) and st["n_lookups_local"] == len(ids) * w.n_elts
+
+
+@pytest.mark.parametrize("precision,cap", [("f64", 2.0 ** 31), ("f32", 2.0 ** 24)])
+def test_tiny_integer_valued_is_bitwise(cuda, precision, cap):
+    """P10: integer-valued losses and terms make every sum exact, so the GPU
+    must match the oracle bit for bit in any summation order (YLT, portfolio,
+    lossy counts, PML, TVaR)."""
+    w = synth.get_config("tiny").with_(int_cap=cap, return_periods=(1, 2, 5, 10, 50, 1000))
+    off, ids, elts = make_inputs(w)
+    orc = run_oracle(off, ids, elts, w, w.layers, fp32=precision == "f32")
+    ylt, lossy, _, met = run_gpu(off, ids, elts, w, w.layers, precision=precision,
+                                 return_periods=w.return_periods)
+    assert np.array_equal(ylt[:-1], orc["ylt"]) and np.array_equal(ylt[-1], orc["portfolio"])
+    assert np.array_equal(lossy, orc["lossy"])
+    assert_metrics_close(met, oracle_rows(orc), orc["scale"], w.return_periods, exact=True)
+
+
+def test_device_pointer_inputs_match_host_inputs(cuda):
+    w = synth.get_config("tiny")
+    off, ids, elts = make_inputs(w)
+    a = run_gpu(off, ids, elts, w, w.layers)
+    b = run_gpu(off, ids, elts, w, w.layers, device_inputs=True)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+# ------------------------------------------------------------------ edge cases
+def _edge_yet(C, rng):
+    lens = [0, 1, 2, 31, 32, 33, 0, 127, 128, 129, 255, 256, 257, 5000, 3, 0]
+    off = np.zeros(len(lens) + 1, dtype=np.uint64)
+    off[1:] = np.cumsum(lens)
+    ids = rng.integers(1, C + 1, size=int(off[-1])).astype(np.uint32)
+    ids[:3] = [1, C, 1]
+    ids[-3:] = [C, C, 1]
+    return off, ids
+
+
+def test_edge_trials_and_unaligned_layers(cuda):
+    rng = np.random.default_rng(9)
+    w = synth.get_config("tiny").with_(n_elts=5, catalog=777, rho=0.5, n_trials=16)
+    _, _, elts = make_inputs(w)
+    off, ids = _edge_yet(w.catalog, rng)
+    layers = (synth.LayerSpec(0, 5, 2.5e4, 5e5, 6.5e5, 2.5e6), synth.LayerSpec(1, 4, 0.0, INF, 0.0, INF),
+              synth.LayerSpec(3, 5, 1e5, 2e5, 1e6, 3e6), synth.LayerSpec(2, 3, 0.0, 1e4, 1e4, INF))
+    for precision in ("f64", "f32"):
+        orc = run_oracle(off, ids, elts, w, layers, fp32=precision == "f32")
+        ylt, lossy, _, _ = run_gpu(off, ids, elts, w, layers, precision=precision)
+        assert_ylt_close(ylt, orc)
+        assert np.array_equal(lossy, orc["lossy"])
+        assert (ylt[:, [0, 6, 15]] == 0).all()
+
+
+def test_wide_windows_tower_and_many_layers(cuda):
+    """40 ELTs: aligned, unaligned, 8-sector, >8-sector (generic kernel) and
+    single-ELT layers; 4 identical windows (shared-load path); 9 layers ->
+    three launches with the portfolio accumulated across them."""
+    w = synth.get_config("tiny").with_(n_elts=40, catalog=3000, rho=0.2, n_trials=700, nmin=1, nmax=300)
+    off, ids, elts = make_inputs(w)
+    rng = np.random.default_rng(4)
+    d = rng.uniform(0, 2e4, w.n_elts)
+    li = np.where(rng.random(w.n_elts) < 0.3, INF, rng.uniform(1e5, 2e6, w.n_elts))
+    layers = (synth.LayerSpec(0, 16, 2.5e4, 7.5e5, 1.2e6, 8e6), synth.LayerSpec(3, 19, 1e5, 4e5, 6.5e5, 4e6),
+              synth.LayerSpec(0, 32, 0.0, INF, 1e6, INF), synth.LayerSpec(5, 38, 2.5e5, 5e5, 4e5, 3.5e6),
+              synth.LayerSpec(39, 40, 0.0, INF, 0.0, INF),
+              synth.LayerSpec(8, 24, 1e4, 1e6, 0.0, 2e6), synth.LayerSpec(8, 24, 5e4, 2e5, 1e5, 1e6),
+              synth.LayerSpec(8, 24, 1e5, 1e5, 3e5, INF), synth.LayerSpec(8, 24, 0.0, 7e4, 0.0, 9e5))
+    for precision in ("f64", "f32"):
+        orc = run_oracle(off, ids, elts, w, layers, fp32=precision == "f32", terms=(d, li))
+        ylt, lossy, st, _ = run_gpu(off, ids, elts, w, layers, precision=precision, terms=(d, li))
+        assert_ylt_close(ylt, orc)
+        assert np.array_equal(lossy, orc["lossy"])
+        assert st["n_kernel_launches"] >= 3
+
+
+def test_single_elt_single_event_lookup(cuda):
+    """P12 on the GPU: one ELT, one event per trial, identity terms -> Y_t = L[e_t] exactly."""
+    w = synth.get_config("tiny").with_(n_elts=1, n_trials=4000, nmin=1, nmax=1)
+    off, ids, elts = make_inputs(w)
+    dense = oracle.direct_access(oracle.Elts(*elts), w.catalog)
+    ylt, _, _, _ = run_gpu(off, ids, elts, w, (synth.LayerSpec(0, 1, 0.0, INF, 0.0, INF),),
+                           terms=(np.zeros(1), np.full(1, INF)))
+    assert np.array_equal(ylt[0], dense[0, ids])
+
+
+# ------------------------------------------------------------------ invariants
+def test_partition_and_alignment_invariance(cuda):
+    """P11 on the GPU: shards loaded as independent YETs (different base
+    alignment of every trial) reproduce the unsharded YLT bit for bit."""
+    w = synth.get_config("tiny").with_(n_trials=1001)
+    off, ids, elts = make_inputs(w)
+    full, _, _, _ = run_gpu(off, ids, elts, w, w.layers)
+    ara = _ara()
+    for N in (2, 3, 8, 16):
+        parts = []
+        for r in range(N):
+            f, c = ara.ara_partition(w.n_trials, N, r)
+            so = off[f:f + c + 1].copy()
+            si = ids[int(off[f]):int(off[f + c])]
+            if r % 2:                      # misalign the shard by one element
+                si = np.concatenate([np.zeros(1, np.uint32), si])[1:]
+            y, _, _, _ = run_gpu(so, si, elts, w, w.layers)
+            parts.append(y[:, :c])
+        assert np.array_equal(np.concatenate(parts, axis=1), full)
+
+
+def test_monotone_in_retentions_and_bounded(cuda):
+    """P9 on the GPU, exact comparisons: raising a retention never raises any Y_t."""
+    w = synth.get_config("tiny")
+    off, ids, elts = make_inputs(w)
+    base, _, _, _ = run_gpu(off, ids, elts, w, w.layers)
+    L0 = w.layers[0]
+    assert (base[0] >= 0).all() and (base[0] <= L0.agg_limit).all()
+    for bumped in (L0.__class__(0, 3, L0.occ_retention * 2, L0.occ_limit, L0.agg_retention, L0.agg_limit),
+                   L0.__class__(0, 3, L0.occ_retention, L0.occ_limit, L0.agg_retention * 1.3, L0.agg_limit)):
+        y, _, _, _ = run_gpu(off, ids, elts, w, (bumped,))
+        assert (y[0] <= base[0]).all() and (y[0] < base[0]).any()
+    d, li = w.elt_terms()
+    d2 = d.copy()
+    d2[1] *= 4
+    y, _, _, _ = run_gpu(off, ids, elts, w, w.layers, terms=(d2, li))
+    assert (y[0] <= base[0]).all() and (y[0] < base[0]).any()
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_chunked_h2d_equals_all_at_once(cuda, pinned):
+    import torch
+    w = synth.get_config("tiny").with_(n_trials=3000)
+    off, ids, elts = make_inputs(w)
+    ref, ref_lossy, _, _ = run_gpu(off, ids, elts, w, w.layers)
+    if pinned:
+        po = torch.from_numpy(off.view(np.int64)).pin_memory()
+        pi = torch.from_numpy(ids.view(np.int32)).pin_memory()
+        off_h, ids_h = po.numpy().view(np.uint64), pi.numpy().view(np.uint32)
+    else:
+        off_h, ids_h = off.copy(), ids.copy()
+    for chunk in (1, 7, 333, 10 ** 7):
+        ylt, lossy, st, _ = run_gpu(off_h, ids_h, elts, w, w.layers, load_mode="chunked", chunk_trials=chunk)
+        assert np.array_equal(ylt, ref) and np.array_equal(lossy, ref_lossy)
+        assert st["h2d_bytes"] == ids.nbytes + off.nbytes
+
+
+def test_set_elt_terms_equals_fresh_load(cuda):
+    ara = _ara()
+    w = synth.get_config("tiny")
+    off, ids, elts = make_inputs(w)
+    d, li = w.elt_terms()
+    d2, li2 = d * 0.5, li * 2
+    fresh, _, _, _ = run_gpu(off, ids, elts, w, w.layers, terms=(d2, li2))
+    with ara.Context(w.catalog) as ctx:
+        ctx.load_elts(*elts, terms=(d, li))
+        ctx.load_yet(w.n_trials, 0, off, ids)
+        a, _, _ = ctx.run_host(w.layers)
+        ctx.set_elt_terms((d2, li2))
+        b, _, _ = ctx.run_host(w.layers)
+    assert np.array_equal(b, fresh) and not np.array_equal(a, b)
+
+
+def test_metrics_ties_extremes(cuda):
+    """Many ties (capped and zero years) plus R = 1 (k = T, min / mean) and R = T (max)."""
+    w = synth.get_config("tiny").with_(int_cap=2.0 ** 31)
+    off, ids, elts = make_inputs(w)
+    layers = (synth.LayerSpec(0, 3, 2.5e4, 5e5, 6.5e6, 2.5e5), synth.LayerSpec(0, 3, 0, INF, 0, INF))
+    orc = run_oracle(off, ids, elts, w, layers)
+    R = (1, 1.5, 2, 7.25, 999.9, 1000)
+    _, _, _, met = run_gpu(off, ids, elts, w, layers, return_periods=R)
+    assert (orc["ylt"][0] == 2.5e5).mean() > 0.2
+    assert_metrics_close(met, oracle_rows(orc), orc["scale"], R, exact=True)
+
+
+# ------------------------------------------------------------------ errors
+def test_errors_are_reported_and_context_survives(cuda):
+    ara = _ara()
+    w = synth.get_config("tiny")
+    off, ids, elts = make_inputs(w)
+    eo, ev, ls = elts
+    C = w.catalog
+    with ara.Context(C) as ctx:
+        with pytest.raises(ara.AraError) as e:
+            ctx.run(w.layers)
+        assert e.value.status == ara.ARA_ERR_STATE
+        for bad_ev, bad_ls, status in ((np.where(np.arange(len(ev)) == 5, C + 1, ev).astype(np.uint32), ls,
+                                        ara.ARA_ERR_OUT_OF_RANGE),
+                                       (ev[::-1].copy(), ls, ara.ARA_ERR_INVALID_ARG),
+                                       (ev, np.where(np.arange(len(ls)) == 3, -1.0, ls), ara.ARA_ERR_DOMAIN),
+                                       (ev, np.where(np.arange(len(ls)) == 3, np.nan, ls), ara.ARA_ERR_DOMAIN)):
+            with pytest.raises(ara.AraError) as e:
+                ctx.load_elts(eo, bad_ev, bad_ls)
+            assert e.value.status == status
+        ctx.load_elts(eo, ev, ls, w.elt_terms())
+        for bad in (0, C + 1):
+            bi = ids.copy()
+            bi[1234] = bad
+            ctx.load_yet(w.n_trials, 0, off, bi)
+            with pytest.raises(ara.AraError) as e:
+                ctx.run(w.layers)
+            assert e.value.status == ara.ARA_ERR_OUT_OF_RANGE
+        bo = off.copy()
+        bo[10], bo[11] = bo[11], bo[10]
+        ctx.load_yet(w.n_trials, 0, bo, ids)
+        with pytest.raises(ara.AraError) as e:
+            ctx.run(w.layers)
+        assert e.value.status == ara.ARA_ERR_OUT_OF_RANGE
+        with pytest.raises(ara.AraError) as e:
+            ctx.metrics([2.0])
+        assert e.value.status == ara.ARA_ERR_STATE
+        ctx.load_yet(w.n_trials, 0, off, ids)
+        for L, status in (((0, 4, 0, 1, 0, 1),), ara.ARA_ERR_INVALID_ARG), (((1, 1, 0, 1, 0, 1),), ara.ARA_ERR_INVALID_ARG), \
+                         (((0, 3, -1, 1, 0, 1),), ara.ARA_ERR_DOMAIN), (((0, 3, 0, 0.0, 0, 1),), ara.ARA_ERR_DOMAIN):
+            with pytest.raises(ara.AraError) as e:
+                ctx.run(L)
+            assert e.value.status == status
+        ylt, lossy, _ = ctx.run_host(w.layers)          # still usable
+        orc = run_oracle(off, ids, elts, w, w.layers)
+        assert_ylt_close(ylt, orc)
+        with pytest.raises(ara.AraError) as e:
+            ctx.metrics([w.n_trials + 1.0])
+        assert e.value.status == ara.ARA_ERR_DOMAIN
