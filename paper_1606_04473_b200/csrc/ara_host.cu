@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <new>
 
 #include "ara_internal.cuh"
@@ -80,6 +81,47 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
         return 0.f;
     }
     return ms;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)f;
+        cudaGetLastError();
+    }
+    return fn;
+}
+
+// TMA map of one column block as a 2D tensor [C+1 rows][epb cols]; the box is
+// one row of `box_sec` sectors, swizzled so each lane's row read is
+// bank-conflict free (see trial_kernel_tma).
+bool make_block_map(const ara_ctx* ctx, uint32_t blk, uint32_t box_sec, CUtensorMap* map) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    const TableGeo& g = ctx->geo;
+    const uint32_t eps = kSectorBytes / g.esz;
+    cuuint64_t dims[2] = {g.epb, (cuuint64_t)ctx->catalog + 1};
+    cuuint64_t strides[1] = {(cuuint64_t)g.epb * g.esz};
+    cuuint32_t box[2] = {box_sec * eps, 1};
+    cuuint32_t est[2] = {1, 1};
+    const uint32_t rowb = box_sec * kSectorBytes;
+    CUtensorMapSwizzle sw = rowb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : rowb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                         : CU_TENSOR_MAP_SWIZZLE_32B;
+    void* base = static_cast<char*>(ctx->d_table) + (size_t)blk * g.block_elems * g.esz;
+    return enc(map, g.esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims,
+               strides, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 void release_yet(ara_ctx* ctx) {
@@ -179,6 +221,9 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
     ctx->chunk_trials = cfg->chunk_trials ? cfg->chunk_trials : 65536;
     ctx->l2_persist = cfg->l2_persist;
     ctx->catalog = catalog_size;
+    if (const char* v = getenv("ARA_GRID_MULT")) ctx->grid_mult = atof(v);
+    if (const char* v = getenv("ARA_KERNEL")) ctx->kernel_variant = atoi(v);
+    if (const char* v = getenv("ARA_PFN")) ctx->pf_sectors = atoi(v);
     auto bail = [&](ara_status st) {
         ara_destroy(ctx);
         return st;
@@ -258,6 +303,20 @@ ara_status check_terms(ara_ctx* ctx, uint32_t n, const ara_elt_terms* t) {
     return ARA_OK;
 }
 
+// (Re)allocate the column-blocked table for n_elts ELTs (ara::TableGeo).
+ara_status alloc_table(ara_ctx* ctx, uint32_t n_elts) {
+    const TableGeo g = table_geometry(n_elts, ctx->catalog, ctx->precision == ARA_F32_STORAGE);
+    if (g.bytes != ctx->table_bytes) {
+        cudaFree(ctx->d_table);
+        ctx->d_table = nullptr;
+        ctx->table_bytes = 0;
+        CK(cudaMalloc(&ctx->d_table, g.bytes));
+        ctx->table_bytes = g.bytes;
+    }
+    ctx->geo = g;
+    return ARA_OK;
+}
+
 // Rank-0 (or single-rank) part: validate, upload, densify.  Returns status.
 ara_status build_table(ara_ctx* ctx, uint32_t n_elts, const uint64_t* elt_offsets, const uint32_t* event_ids,
                        const double* losses) {
@@ -275,18 +334,9 @@ ara_status build_table(ara_ctx* ctx, uint32_t n_elts, const uint64_t* elt_offset
     if (nrec && (!event_ids || !losses)) return fail(ctx, ARA_ERR_INVALID_ARG, "event_ids/losses NULL");
 
     const int fp32 = ctx->precision == ARA_F32_STORAGE;
-    const size_t esz = fp32 ? 4 : 8;
-    const uint64_t row_bytes = ((uint64_t)n_elts * esz + kSectorBytes - 1) / kSectorBytes * kSectorBytes;
-    const size_t bytes = (size_t)((uint64_t)ctx->catalog + 1) * row_bytes + kTablePadBytes;
-    if (bytes != ctx->table_bytes) {
-        cudaFree(ctx->d_table);
-        ctx->d_table = nullptr;
-        ctx->table_bytes = 0;
-        CK(cudaMalloc(&ctx->d_table, bytes));
-        ctx->table_bytes = bytes;
-    }
-    ctx->row_elems = row_bytes / esz;
-    CK(cudaMemsetAsync(ctx->d_table, 0, bytes, ctx->stream));
+    ara_status ast = alloc_table(ctx, n_elts);
+    if (ast != ARA_OK) return ast;
+    CK(cudaMemsetAsync(ctx->d_table, 0, ctx->table_bytes, ctx->stream));
 
     // sparse arrays -> device (temporary copies only for host inputs)
     uint64_t* d_eoff = nullptr;
@@ -327,7 +377,7 @@ ara_status build_table(ara_ctx* ctx, uint32_t n_elts, const uint64_t* elt_offset
             }
         }
         if (cudaMemsetAsync(ctx->d_err, 0, sizeof(uint32_t), ctx->stream) != cudaSuccess) { st = ARA_ERR_CUDA; break; }
-        if (launch_densify(d_eoff, d_ev, d_ls, n_elts, nrec, ctx->catalog, ctx->d_table, ctx->row_elems, fp32,
+        if (launch_densify(d_eoff, d_ev, d_ls, n_elts, nrec, ctx->catalog, ctx->d_table, ctx->geo, fp32,
                            ctx->d_err, ctx->stream) != cudaSuccess) { st = ARA_ERR_CUDA; break; }
         if (cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream) !=
             cudaSuccess) { st = ARA_ERR_CUDA; break; }
@@ -385,17 +435,8 @@ extern "C" ara_status ara_load_elts(ara_ctx* ctx, uint32_t n_elts, const uint64_
         if (ctx->h_small[1] != n_elts) return fail(ctx, ARA_ERR_INVALID_ARG, "n_elts differs from rank 0");
         if (!root) {
             st = check_terms(ctx, n_elts, terms);
-            const size_t esz = ctx->precision == ARA_F32_STORAGE ? 4 : 8;
-            const uint64_t row_bytes = ((uint64_t)n_elts * esz + kSectorBytes - 1) / kSectorBytes * kSectorBytes;
-            const size_t bytes = (size_t)((uint64_t)ctx->catalog + 1) * row_bytes + kTablePadBytes;
-            if (bytes != ctx->table_bytes) {
-                cudaFree(ctx->d_table);
-                ctx->d_table = nullptr;
-                ctx->table_bytes = 0;
-                CK(cudaMalloc(&ctx->d_table, bytes));
-                ctx->table_bytes = bytes;
-            }
-            ctx->row_elems = row_bytes / esz;
+            ara_status ast = alloc_table(ctx, n_elts);
+            if (ast != ARA_OK) return ast;
         }
         // The table goes over NVLink once instead of N host copies.
         NK(ncclBroadcast(ctx->d_table, ctx->d_table, ctx->table_bytes, ncclUint8, 0, ctx->comm, ctx->stream));
@@ -503,10 +544,9 @@ extern "C" ara_status ara_load_yet(ara_ctx* ctx, uint64_t n_trials_global, uint6
 namespace {
 
 struct Group {
-    uint32_t l0, nl;      // layers [l0, l0+nl)
-    uint32_t max_nsec;
-    bool share;
-    bool wide;
+    uint32_t l0, nl;      // layers [l0, l0+nl), all on one sector window
+    uint32_t q0, nsec;    // window = column sectors [q0, q0 + nsec)
+    bool wide;            // nsec > kMaxSec: generic kernel
 };
 
 }  // namespace
@@ -570,32 +610,22 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
         }
     }
 
-    // Layer groups: up to kMaxLB consecutive layers per launch; a layer wider
+    // Layer groups: consecutive layers on the same sector window share one
+    // launch (one row load serves up to kMaxLB tower layers); a layer wider
     // than kMaxSec sectors runs alone in the generic kernel.
     std::vector<Group> groups;
-    for (uint32_t l = 0; l < n_layers;) {
-        const uint32_t s0 = layers[l].elt_begin / eps, s1 = (layers[l].elt_end + eps - 1) / eps;
-        if (s1 - s0 > (uint32_t)kMaxSec) {
-            groups.push_back({l, 1, s1 - s0, false, true});
-            ++l;
-            continue;
-        }
-        Group g{l, 0, 0, true, false};
-        while (l < n_layers && g.nl < (uint32_t)kMaxLB) {
-            const uint32_t a = layers[l].elt_begin / eps, b = (layers[l].elt_end + eps - 1) / eps;
-            if (b - a > (uint32_t)kMaxSec) break;
-            if (g.nl > 0) {
-                const uint32_t a0 = layers[g.l0].elt_begin / eps, b0 = (layers[g.l0].elt_end + eps - 1) / eps;
-                if (a != a0 || b != b0) g.share = false;
+    for (uint32_t l = 0; l < n_layers; ++l) {
+        const uint32_t q0 = layers[l].elt_begin / eps, q1 = (layers[l].elt_end + eps - 1) / eps;
+        const bool wide = q1 - q0 > (uint32_t)kMaxSec;
+        if (!wide && !groups.empty()) {
+            Group& g = groups.back();
+            if (!g.wide && g.q0 == q0 && g.nsec == q1 - q0 && g.nl < (uint32_t)kMaxLB) {
+                ++g.nl;
+                continue;
             }
-            if (b - a > g.max_nsec) g.max_nsec = b - a;
-            ++g.nl;
-            ++l;
         }
-        if (g.nl == 1) g.share = false;
-        groups.push_back(g);
+        groups.push_back({l, 1, q0, q1 - q0, wide});
     }
-
     cudaStream_t s = ctx->stream;
     CK(cudaEventRecord(ctx->ev[0], s));
     CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(uint32_t), s));
@@ -652,16 +682,20 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
     }
 
     // Kernels.
+    const TableGeo& geo = ctx->geo;
+    const uint32_t spb = geo.epb / eps;   // sectors per block row
     TrialParams base{};
     base.off = ctx->d_off;
     base.ids = ctx->d_ids;
     base.catalog = ctx->catalog;
     base.table = ctx->d_table;
-    base.row_elems = ctx->row_elems;
+    base.row_stride = geo.epb;
+    base.block_stride = geo.block_elems;
     base.ylt = ctx->d_ylt_local;
     base.ld = ld;
     base.lossy = d_lossy;
     base.err = ctx->d_err;
+    base.pf_sectors = ctx->pf_sectors;
     base.portfolio_row = n_layers;
     uint32_t launches = 0;
     double2* d_cterm = nullptr;
@@ -677,10 +711,12 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
             p.n_layers = g.nl;
             p.ylt_row0 = g.l0;
             p.portfolio_mode = gi == 0 ? 0 : 1;
+            for (uint32_t q = 0; q < g.nl; ++q) {
+                const ara_layer& L = layers[g.l0 + q];
+                p.lw[q] = {L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit};
+            }
             if (g.wide) {
                 const ara_layer& L = layers[g.l0];
-                p.lw[0] = {0, 0, L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit};
-                const uint32_t ncol = L.elt_end - L.elt_begin;
                 if (!d_cterm) {
                     wide_terms.resize(ctx->n_elts);
                     for (uint32_t j = 0; j < ctx->n_elts; ++j)
@@ -689,23 +725,40 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
                     CK(cudaMemcpyAsync(d_cterm, wide_terms.data(), ctx->n_elts * sizeof(double2),
                                        cudaMemcpyHostToDevice, s));
                 }
-                const int grid = trial_kernel_grid(fp32, g.max_nsec, false, 1);
-                CK(launch_trials_wide(p, fp32, d_cterm + L.elt_begin, L.elt_begin, ncol, grid, s));
+                const int grid = trial_kernel_grid(fp32, g.nsec, 1, 0);
+                CK(launch_trials_wide(p, fp32, d_cterm + L.elt_begin, L.elt_begin, L.elt_end - L.elt_begin, grid,
+                                      s));
             } else {
+                for (uint32_t sct = 0; sct < (uint32_t)kMaxSec; ++sct) {
+                    const uint32_t qq = g.q0 + (sct < g.nsec ? sct : 0);
+                    p.sec_off[sct] = (uint64_t)(qq / spb) * geo.block_elems + (uint64_t)(qq % spb) * eps;
+                }
                 for (uint32_t q = 0; q < g.nl; ++q) {
                     const ara_layer& L = layers[g.l0 + q];
-                    const uint32_t a = L.elt_begin / eps, b = (L.elt_end + eps - 1) / eps;
-                    p.lw[q] = {a, b - a, L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit};
                     for (uint32_t w = 0; w < (uint32_t)kMaxWin; ++w) {
-                        const uint32_t col = a * eps + w;
-                        if (w < g.max_nsec * eps && col >= L.elt_begin && col < L.elt_end)
+                        const uint32_t col = g.q0 * eps + w;
+                        if (w / eps < g.nsec && col >= L.elt_begin && col < L.elt_end)
                             p.term[q][w] = make_double2(ctx->terms[col].deductible, ctx->terms[col].limit);
                         else
                             p.term[q][w] = make_double2(INFINITY, INFINITY);   // contributes exactly +0
                     }
                 }
-                const int grid = trial_kernel_grid(fp32, g.max_nsec, g.share, (int)g.nl);
-                CK(launch_trials(p, fp32, g.max_nsec, g.share, grid, s));
+                // Kernel choice (measured, profiles/r01_*): the register-pipelined LDG
+                // kernel at 3 CTAs/SM for single-layer launches, 2 CTAs/SM for shared-window
+                // towers.  The TMA gather4 ring (8) and the cp.async ring (1) are kept as
+                // ARA_KERNEL-selectable alternatives; both are slower on B200 today.
+                int variant = ctx->kernel_variant;
+                const uint32_t box_sec = g.nsec <= 1 ? 1 : (g.nsec <= 2 ? 2 : 4);
+                const bool tma_ok = g.nsec <= 4 && (g.q0 % spb) + g.nsec <= spb && encode_tiled() != nullptr;
+                if (variant < 0) variant = g.nl == 1 ? 5 : 0;
+                if (variant == 8 && !tma_ok) variant = g.nl == 1 ? 5 : 0;
+                if (variant == 8) {
+                    if (!make_block_map(ctx, g.q0 / spb, box_sec, &p.tmap))
+                        return fail(ctx, ARA_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+                    p.tma_col = (g.q0 % spb) * eps;
+                }
+                const int grid = (int)(trial_kernel_grid(fp32, g.nsec, (int)g.nl, variant) * ctx->grid_mult);
+                CK(launch_trials(p, fp32, g.nsec, grid > 0 ? grid : 1, variant, s));
             }
             ++launches;
         }

@@ -2,6 +2,7 @@
 // Nothing here is shared with oracle/ (the CPU oracle is independent test
 // infrastructure); this header is private to paper_1606_04473_b200/csrc.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdint.h>
@@ -22,31 +23,62 @@ enum : uint32_t {
     ERRBIT_ELT_LOSS = 1u << 4,      // ELT loss negative / non-finite / fp32-unrepresentable
 };
 
-constexpr int kSectorBytes = 32;     // one L2 sector; rows are padded to sector multiples
+constexpr int kSectorBytes = 32;     // one L2 sector; windows are sector-granular
+constexpr int kBlockBytes = 128;     // column-block width of the direct-access table
 constexpr int kMaxSec = 8;           // widest per-layer window handled by the fast kernel (256 B)
-constexpr int kMaxLB = 4;            // layers per kernel launch (per-layer registers)
+constexpr int kMaxLB = 4;            // layers sharing one window per launch
 constexpr int kMaxWin = kMaxSec * kSectorBytes / 4;   // 64 columns (fp32) per window
 constexpr int kThreads = 256;        // 8 warps per CTA
 constexpr int kTablePadBytes = kMaxSec * kSectorBytes;  // over-read slack after the last row
 
-// One layer of a kernel launch: the sector window [sec0, sec0 + nsec) of the
-// interleaved row, the per-column terms of that window (columns outside the
-// layer carry deductible +inf so they contribute an exact +0), and the layer
-// terms.  Passed by value in the launch parameters (constant bank).
+// Direct-access table geometry: ELT columns are cut
+// into blocks of `epb` elements (<= 128 B); block b is a dense [C+1][epb]
+// array, so element (event e, ELT j) lives at
+//   (j / epb) * block_elems + e * epb + j % epb.
+// A layer of <= 16 fp64 ELTs therefore reads one contiguous 32..128-B row
+// window per event, and each block spans at most (C+1) * 128 B (256 MB at the
+// paper's 2M-event catalogue), inside the GPU TLB's reach.
+struct TableGeo {
+    uint32_t esz = 8;            // element bytes (8 fp64, 4 fp32-storage)
+    uint32_t epb = 0;            // elements per block row
+    uint32_t n_blocks = 0;
+    uint64_t block_elems = 0;    // (C+1) * epb
+    size_t bytes = 0;            // allocation incl. pad
+};
+inline TableGeo table_geometry(uint32_t n_elts, uint32_t catalog, int fp32) {
+    TableGeo g;
+    g.esz = fp32 ? 4 : 8;
+    uint64_t row = (uint64_t)n_elts * g.esz;
+    row = (row + kSectorBytes - 1) / kSectorBytes * kSectorBytes;
+    if (row > (uint64_t)kBlockBytes) row = kBlockBytes;
+    g.epb = (uint32_t)(row / g.esz);
+    g.n_blocks = (n_elts + g.epb - 1) / g.epb;
+    g.block_elems = ((uint64_t)catalog + 1) * g.epb;
+    g.bytes = (size_t)g.n_blocks * g.block_elems * g.esz + kTablePadBytes;
+    return g;
+}
+
+// Layer terms of one launch (P:373 occurrence, P:375 aggregate).
 struct LayerWin {
-    uint32_t sec0;
-    uint32_t nsec;
     double occ_r, occ_l, agg_r, agg_l;
 };
 
+// All layers of one launch share one sector window: sec_off[s] is the element
+// offset of window sector s for event 0 (event e adds e * row_stride).  Window
+// columns outside a layer carry deductible +inf, so they contribute an exact
+// +0 and need no predicate.  Passed by value (constant bank).
 struct TrialParams {
+    CUtensorMap tmap;           // TMA variant: the window's column block as a 2D [C+1][epb] tensor
+    uint32_t tma_col;           // TMA variant: first window column inside the block
     const uint64_t* off;        // local CSR offsets [n_local + 1]
     const uint32_t* ids;        // events of off[0] ...
     uint64_t t_begin, t_end;    // trial range of this launch (local indices)
     uint32_t catalog;
     uint32_t n_layers;          // layers in this launch (<= kMaxLB)
-    const void* table;          // [C+1][row_elems] (+ pad)
-    uint64_t row_elems;         // elements per row (row stride)
+    const void* table;          // column-blocked direct-access table (+ pad)
+    uint64_t row_stride;        // elements per block row (= epb)
+    uint64_t block_stride;      // elements per column block (= (C+1) * epb)
+    uint64_t sec_off[kMaxSec];  // window sector offsets (elements, event 0)
     double* ylt;                // [.. rows][ld] : row ylt_row0 + l
     uint64_t ld;                // row stride of ylt (= n_local)
     uint32_t ylt_row0;          // first YLT row written by this launch
@@ -54,6 +86,7 @@ struct TrialParams {
     uint32_t portfolio_row;
     uint32_t* lossy;            // [.. rows][ld] or null
     uint32_t* err;              // device error word
+    int pf_sectors;             // sectors per prefetched window (prefetching kernels)
     LayerWin lw[kMaxLB];
     double2 term[kMaxLB][kMaxWin];   // (deductible, limit) per window column
 };
@@ -61,11 +94,10 @@ struct TrialParams {
 // ---- launchers (defined in the .cu files; all enqueue on `s`)
 cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const double* d_loss,
                            uint32_t n_elts, uint64_t n_records, uint32_t catalog, void* d_table,
-                           uint64_t row_elems, int fp32, uint32_t* d_err, cudaStream_t s);
+                           const TableGeo& geo, int fp32, uint32_t* d_err, cudaStream_t s);
 
-cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, bool shared_window,
-                          int grid, cudaStream_t s);
-int trial_kernel_grid(int fp32, uint32_t max_nsec, bool shared_window, int n_layers);
+cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int grid, int variant, cudaStream_t s);
+int trial_kernel_grid(int fp32, uint32_t max_nsec, int n_layers, int variant);
 cudaError_t launch_trials_wide(const TrialParams& p, int fp32, const double2* d_cterm, uint32_t col0,
                                uint32_t ncol, int grid, cudaStream_t s);
 
@@ -104,10 +136,10 @@ struct ara_ctx {
 
     uint32_t catalog = 0;
 
-    // ELT direct-access table tab[e][col], e in [0, C] (row 0 = zeros)
+    // ELT direct-access table (column-blocked, ara::TableGeo), row 0 = zeros
     void* d_table = nullptr;
     size_t table_bytes = 0;
-    uint64_t row_elems = 0;
+    ara::TableGeo geo;
     uint32_t n_elts = 0;
     std::vector<ara_elt_terms> terms;
 
@@ -142,5 +174,9 @@ struct ara_ctx {
     uint64_t* d_small = nullptr;
 
     ara::MetricsScratch ms;
+    // tuning knobs (environment, read at ara_create; not part of the ABI)
+    double grid_mult = 1.0;           // ARA_GRID_MULT
+    int kernel_variant = -1;          // ARA_KERNEL (-1 auto; see pick_kernel in ara_kernel.cu)
+    int pf_sectors = 1;               // ARA_PFN
     cudaEvent_t ev[8] = {};
 };

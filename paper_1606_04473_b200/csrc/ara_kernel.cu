@@ -10,18 +10,22 @@
 //   * one warp per trial (the paper used one thread per trial);
 //   * the trial's event ids stream through coalesced 128-B warp loads with an
 //     L2 evict_first policy (the YET is read exactly once);
-//   * event k of the trial goes to lane k % 32, slot (k / 32) % 4 — a mapping
-//     that depends only on the trial's own event order, so the per-trial
-//     summation order (and therefore the YLT bits) is independent of how the
-//     YET is sharded, chunked or aligned in memory (partition invariance);
-//   * one lane reads one event's whole interleaved row tab[e][*] — the layer's
-//     window of 32-B sectors — with 256-bit non-allocating loads
-//     (LDG.E.NA.ENL2.256), then sums the ELT terms sequentially in ELT order
-//     (bit-identical per-event loss to the sequential oracle);
-//   * the trial sum is a fixed lane-strided + 5-step xor-shuffle tree; lossy
-//     occurrence counts are integers (exact);
+//   * event k of the trial goes to lane k % 32 and each lane visits its events
+//     in increasing k — a mapping that depends only on the trial's own event
+//     order, so the per-trial summation order (and the YLT bits) is
+//     independent of how the YET is sharded, chunked or aligned in memory;
+//   * one lane reads one event's row window of the column-blocked
+//     direct-access table — the layer's 32-B sectors — with 256-bit
+//     non-allocating loads (LDG.E.NA.ENL2.256), then sums the ELT terms
+//     sequentially in ELT order (bit-identical per-event loss to the
+//     sequential oracle, hence exact lossy-occurrence counts);
+//   * software pipeline per warp: ids two steps ahead, rows one step ahead of
+//     the fp64 term arithmetic, so every lane keeps a row in flight;
+//   * the trial sum is a fixed lane-strided + 5-step xor-shuffle tree;
 //   * validation of YET ids / offsets is fused (error bits, no extra pass).
 // This is a gather-and-reduce path: no tensor cores (not a contraction).
+#include <cstring>
+
 #include "ara_internal.cuh"
 
 namespace ara {
@@ -40,31 +44,33 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t po
     return v;
 }
 
-// One 32-B sector of a row, predicated (pred == 0 leaves x untouched).
-__device__ __forceinline__ void ld_sector(const double* p, double (&x)[4], uint32_t pred) {
-    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t"
-        "@q ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%5];\n\t}"
-        : "+d"(x[0]), "+d"(x[1]), "+d"(x[2]), "+d"(x[3]) : "r"(pred), "l"(p));
+// One 32-B sector of a row, unconditional 256-bit non-allocating load.
+// Lanes without an event load row 0 (all zeros, L2-resident), and sectors
+// beyond a layer's window carry deductible +inf, so neither needs a predicate.
+__device__ __forceinline__ void ld_sector(const double* p, double (&x)[4]) {
+    asm("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(x[0]), "=d"(x[1]), "=d"(x[2]), "=d"(x[3]) : "l"(p));
 }
-__device__ __forceinline__ void ld_sector(const float* p, float (&x)[8], uint32_t pred) {
-    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %8, 0;\n\t"
-        "@q ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%9];\n\t}"
-        : "+f"(x[0]), "+f"(x[1]), "+f"(x[2]), "+f"(x[3]),
-          "+f"(x[4]), "+f"(x[5]), "+f"(x[6]), "+f"(x[7])
-        : "r"(pred), "l"(p));
+__device__ __forceinline__ void ld_sector(const float* p, float (&x)[8]) {
+    asm("ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3]), "=f"(x[4]), "=f"(x[5]), "=f"(x[6]), "=f"(x[7])
+        : "l"(p));
 }
 
 // min(max(x - r, 0), lim): P:373/P:375 with reading A1; also I_j (A3).
+// max(v, 0) is the oracle's (v > 0 ? v : 0) done on the sign bit (integer
+// pipe; v is never NaN); min is (v < lim ? v : lim).  Identical results to
+// the oracle for every non-NaN input, signed zeros included.
 __device__ __forceinline__ double terms(double x, double r, double lim) {
-    return fmin(fmax(__dsub_rn(x, r), 0.0), lim);
+    double v = __dsub_rn(x, r);
+    v = (__double2hiint(v) >= 0) ? v : 0.0;
+    return (v < lim) ? v : lim;
 }
 
 template <typename TV> struct SecT;
 template <> struct SecT<double> { static constexpr int N = 4; };
 template <> struct SecT<float> { static constexpr int N = 8; };
 
-// Per-event work for all layers of the launch: a3 lookup, a4 per-ELT terms,
-// a5 sequential ELT sum, a6 occurrence terms, a7 accumulate.
 // Terms of small windows stay in uniform registers (constant bank); larger
 // sets are read from shared memory at the point of use (volatile, so the
 // compiler cannot hoist them into vector registers and spill).
@@ -75,37 +81,43 @@ __device__ __forceinline__ double2 lds_term(const double2* p) {
     return v;
 }
 
-template <typename TV, int NSEC, int NLB, bool SHARE>
+template <typename TV, int NSEC, int NLB>
 struct TermsInSmem {
     static constexpr bool value = NLB * NSEC * SecT<TV>::N > 16;
 };
 
-template <typename TV, int NSEC, int NLB, bool SHARE>
-__device__ __forceinline__ void event_step(const TrialParams& p, const double2 (*s_term)[kMaxWin], uint32_t e,
-                                           double (&G)[NLB], uint32_t (&m)[NLB]) {
-    constexpr int EPS = SecT<TV>::N;
-    constexpr bool SM = TermsInSmem<TV, NSEC, NLB, SHARE>::value;
-    const TV* row = static_cast<const TV*>(p.table) + (uint64_t)e * p.row_elems;
+// One event's window (NSEC sectors) of the column-blocked table (a3 lookup).
+// Layers sharing a launch share their window (tower layers), so one load
+// serves all of them.
+template <typename TV, int NSEC>
+struct Row {
+    static constexpr int EPS = SecT<TV>::N;
     TV x[NSEC][EPS];
+
+    __device__ __forceinline__ void load(const TrialParams& p, uint32_t e) {
+        const TV* tab = static_cast<const TV*>(p.table) + (uint64_t)e * p.row_stride;
+#pragma unroll
+        for (int s = 0; s < NSEC; ++s) ld_sector(tab + p.sec_off[s], x[s]);
+    }
+};
+
+// Per-event work for the layers of the launch: a4 per-ELT terms, a5
+// sequential ELT sum, a6 occurrence terms, a7 accumulate.
+template <typename TV, int NSEC, int NLB>
+__device__ __forceinline__ void event_compute(const TrialParams& p, const double2 (*s_term)[kMaxWin],
+                                              const Row<TV, NSEC>& r, double (&G)[NLB], uint32_t (&m)[NLB]) {
+    constexpr int EPS = SecT<TV>::N;
+    constexpr bool SM = TermsInSmem<TV, NSEC, NLB>::value;
 #pragma unroll
     for (int l = 0; l < NLB; ++l) {
         if (l >= (int)p.n_layers) break;
-        if (!SHARE || l == 0) {
-            const TV* w = row + (uint64_t)p.lw[l].sec0 * EPS;
-#pragma unroll
-            for (int s = 0; s < NSEC; ++s) {
-#pragma unroll
-                for (int c = 0; c < EPS; ++c) x[s][c] = TV(0);
-                ld_sector(w + s * EPS, x[s], e != 0u && (uint32_t)s < p.lw[l].nsec);
-            }
-        }
         double le = 0.0;
 #pragma unroll
         for (int s = 0; s < NSEC; ++s)
 #pragma unroll
             for (int c = 0; c < EPS; ++c) {
                 const double2 tc = SM ? lds_term(&s_term[l][s * EPS + c]) : p.term[l][s * EPS + c];
-                le = __dadd_rn(le, terms((double)x[s][c], tc.x, tc.y));
+                le = __dadd_rn(le, terms((double)r.x[s][c], tc.x, tc.y));
             }
         const double o = terms(le, p.lw[l].occ_r, p.lw[l].occ_l);
         G[l] = __dadd_rn(G[l], o);
@@ -113,32 +125,49 @@ __device__ __forceinline__ void event_step(const TrialParams& p, const double2 (
     }
 }
 
-// Events per lane in flight per iteration: one 32-B sector per fp64 window
-// column group costs 8 registers, so keep ~64 registers of rows in flight.
-template <typename TV, int NSEC, int NLB, bool SHARE>
+// Events per lane per pipeline step (~16-32 row registers per stage); windows
+// wider than 32 registers run without the row double buffer (PIPE = false).
+template <typename TV, int NSEC>
 struct Batch {
-    static constexpr int R = NSEC * SecT<TV>::N * (int)sizeof(TV) / 4 * (SHARE ? 1 : NLB);  // row regs/event
-    static constexpr int QB = R >= 64 ? 1 : (R >= 32 ? 2 : 4);
+    static constexpr int R = NSEC * SecT<TV>::N * (int)sizeof(TV) / 4;   // row registers per event
+    static constexpr int QB = R >= 16 ? 1 : (R >= 8 ? 2 : 4);
+    static constexpr bool PIPE = R <= 32;
 };
 
-template <typename TV, int NSEC, int NLB, bool SHARE>
-__global__ void __launch_bounds__(kThreads, 2) trial_kernel(const __grid_constant__ TrialParams p) {
-    constexpr int QB = Batch<TV, NSEC, NLB, SHARE>::QB;
+// L2 prefetch of one event's window (no register destination: CCTL.E.PF2).
+__device__ __forceinline__ void prefetch_l2(const void* ptr) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+}
+
+// D = id-queue depth: rows of step i+1 are demand-loaded into registers while
+// step i is computed; for D > 1 the rows of step i+D are also prefetched into
+// L2 (no registers held), so the demand loads mostly hit L2.
+template <typename TV, int NSEC, int NLB, int D, int MINB = 2>
+__global__ void __launch_bounds__(kThreads, MINB) trial_kernel(const __grid_constant__ TrialParams p) {
+    constexpr int QB = Batch<TV, NSEC>::QB;
+    constexpr bool PIPE = Batch<TV, NSEC>::PIPE;
     constexpr uint64_t STEP = 32u * QB;
+    constexpr bool SM = TermsInSmem<TV, NSEC, NLB>::value;
+    using R = Row<TV, NSEC>;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t gw = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
     const uint64_t nw = (uint64_t(gridDim.x) * kThreads) >> 5;
     const uint64_t pol = policy_evict_first();
     const uint64_t base = __ldg(p.off);
     uint32_t err = 0;
-    __shared__ double2 s_term[TermsInSmem<TV, NSEC, NLB, SHARE>::value ? NLB : 1][kMaxWin];
-    if (TermsInSmem<TV, NSEC, NLB, SHARE>::value) {
-        for (int i = threadIdx.x; i < NLB * kMaxWin; i += kThreads) s_term[i / kMaxWin][i % kMaxWin] = p.term[i / kMaxWin][i % kMaxWin];
+    __shared__ double2 s_term[SM ? NLB : 1][kMaxWin];
+    if (SM) {
+        for (int i = threadIdx.x; i < NLB * kMaxWin; i += kThreads)
+            s_term[i / kMaxWin][i % kMaxWin] = p.term[i / kMaxWin][i % kMaxWin];
         __syncthreads();
     }
 
-    for (uint64_t t = p.t_begin + gw; t < p.t_end; t += nw) {
-        uint64_t a = __ldg(p.off + t), b = __ldg(p.off + t + 1);
+    uint64_t t = p.t_begin + gw;
+    uint64_t a_nxt = 0, b_nxt = 0;
+    if (t < p.t_end) { a_nxt = __ldg(p.off + t); b_nxt = __ldg(p.off + t + 1); }
+    for (; t < p.t_end; t += nw) {
+        uint64_t a = a_nxt, b = b_nxt;
+        if (t + nw < p.t_end) { a_nxt = __ldg(p.off + t + nw); b_nxt = __ldg(p.off + t + nw + 1); }
         if (b < a) { err |= ERRBIT_OFFSETS; b = a; }
         const uint64_t n = b - a;
         const uint32_t* ids = p.ids + (a - base);
@@ -147,8 +176,8 @@ __global__ void __launch_bounds__(kThreads, 2) trial_kernel(const __grid_constan
 #pragma unroll
         for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
 
-        // Event k of the trial -> lane k % 32; each lane visits its events in
-        // increasing k.  Ids of the next step are prefetched one step ahead.
+        // Event k of the trial -> lane k % 32, visited in increasing k.
+        // Software pipeline: ids two steps ahead, rows one step ahead.
         auto load_ids = [&](uint64_t k0, uint32_t (&e)[QB]) {
 #pragma unroll
             for (int q = 0; q < QB; ++q) {
@@ -161,16 +190,64 @@ __global__ void __launch_bounds__(kThreads, 2) trial_kernel(const __grid_constan
                 e[q] = v;
             }
         };
-        uint32_t e_cur[QB];
-        load_ids(0, e_cur);
+        auto prefetch_rows = [&](const uint32_t (&e)[QB]) {
+#pragma unroll
+            for (int q = 0; q < QB; ++q) {
+                const TV* row = static_cast<const TV*>(p.table) + (uint64_t)e[q] * p.row_stride;
+#pragma unroll
+                for (int sct = 0; sct < NSEC; ++sct)
+                    if (sct < p.pf_sectors) prefetch_l2(row + p.sec_off[sct]);
+            }
+        };
+        if (PIPE) {
+            uint32_t qe[D][QB];   // ids of steps i+1 .. i+D
+            R r0[QB];
+            {
+                uint32_t e0[QB];
+                load_ids(0, e0);
+#pragma unroll
+                for (int d = 0; d < D; ++d) load_ids((d + 1) * STEP, qe[d]);
+#pragma unroll
+                for (int q = 0; q < QB; ++q) r0[q].load(p, e0[q]);
+#pragma unroll
+                for (int d = 1; d < D; ++d)
+                    if ((d + 1) * STEP < n) prefetch_rows(qe[d]);
+            }
 #pragma unroll 1
-        for (uint64_t k0 = 0; k0 < n; k0 += STEP) {
-            uint32_t e_nxt[QB];
-            load_ids(k0 + STEP, e_nxt);
+            for (uint64_t k0 = 0; k0 < n; k0 += STEP) {
+                uint32_t en[QB];
+                load_ids(k0 + (D + 1) * STEP, en);
+                if (D > 1 && k0 + D * STEP < n) prefetch_rows(qe[D - 1]);
+                R r1[QB];
+                if (k0 + STEP < n) {
 #pragma unroll
-            for (int q = 0; q < QB; ++q) event_step<TV, NSEC, NLB, SHARE>(p, s_term, e_cur[q], G, m);
+                    for (int q = 0; q < QB; ++q) r1[q].load(p, qe[0][q]);
+                }
 #pragma unroll
-            for (int q = 0; q < QB; ++q) e_cur[q] = e_nxt[q];
+                for (int q = 0; q < QB; ++q) event_compute<TV, NSEC, NLB>(p, s_term, r0[q], G, m);
+#pragma unroll
+                for (int q = 0; q < QB; ++q) {
+                    r0[q] = r1[q];
+#pragma unroll
+                    for (int d = 0; d + 1 < D; ++d) qe[d][q] = qe[d + 1][q];
+                    qe[D - 1][q] = en[q];
+                }
+            }
+        } else {
+            uint32_t e1[QB];
+            load_ids(0, e1);
+#pragma unroll 1
+            for (uint64_t k0 = 0; k0 < n; k0 += STEP) {
+                uint32_t e2[QB];
+                load_ids(k0 + STEP, e2);
+                R r0[QB];
+#pragma unroll
+                for (int q = 0; q < QB; ++q) r0[q].load(p, e1[q]);
+#pragma unroll
+                for (int q = 0; q < QB; ++q) event_compute<TV, NSEC, NLB>(p, s_term, r0[q], G, m);
+#pragma unroll
+                for (int q = 0; q < QB; ++q) e1[q] = e2[q];
+            }
         }
         // a7: fixed xor-tree over lanes; every lane ends with the same bits.
 #pragma unroll
@@ -199,8 +276,410 @@ __global__ void __launch_bounds__(kThreads, 2) trial_kernel(const __grid_constan
     if (err) atomicOr(p.err, err);
 }
 
+// ---------------------------------------------------------------------------
+// Shared-memory staged variant (default for the paper-shaped path).  The
+// register-pipelined kernel above can keep at most ~2 row windows per lane in
+// flight before the register file (256 KB/SM) is exhausted; with 128-B windows
+// that is too little memory-level parallelism to cover loaded DRAM latency
+// (ncu: long-scoreboard stalls, DRAM ~55 % busy).  Here each lane copies its
+// event's window straight into a per-warp shared-memory ring with cp.async
+// (LDGSTS, no registers held), NS steps deep, so ~(NS-1) x 4 KB per warp is in
+// flight continuously; the fp64 arithmetic reads the window back with swizzled
+// (bank-conflict-free) LDS.128.  The ring runs across trial boundaries: a step
+// iterator two steps ahead loads ids, the producer issues step j, the consumer
+// retires step j-(NS-1) and finishes a trial on its last step.  Same lane
+// mapping, same per-lane order, same arithmetic as trial_kernel: identical
+// YLT bits.
+struct StepMeta {
+    uint64_t t;      // trial (UINT64_MAX: no more steps)
+    uint32_t n, k0;  // trial length, first event index of the step
+};
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename TV, int NSEC>
+struct SmGeo {
+    static constexpr int WARPS = kThreads / 32;
+    static constexpr int CH = NSEC * 2;                // 16-B chunks per lane slot
+    static constexpr int SLOT = CH * 16;               // bytes per lane slot
+    static constexpr int STAGE = 32 * SLOT;            // bytes per warp stage
+    static constexpr int NS0 = (196 * 1024) / (WARPS * STAGE);
+    static constexpr int NS = NS0 > 8 ? 8 : (NS0 < 2 ? 2 : NS0);
+    static constexpr int RING = WARPS * NS * STAGE;
+    static constexpr int BYTES = RING + WARPS * NS * (int)sizeof(StepMeta);
+};
+
+template <typename TV, int NSEC, int NLB>
+__global__ void __launch_bounds__(kThreads, 1) trial_kernel_sm(const __grid_constant__ TrialParams p) {
+    using Geo = SmGeo<TV, NSEC>;
+    constexpr int NS = Geo::NS, CH = Geo::CH;
+    constexpr bool SM = TermsInSmem<TV, NSEC, NLB>::value;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double2 s_term[SM ? NLB : 1][kMaxWin];
+    const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem) + wib * NS * Geo::STAGE + lane * Geo::SLOT;
+    StepMeta* meta = reinterpret_cast<StepMeta*>(smem + Geo::RING) + wib * NS;
+    if (SM) {
+        for (int i = threadIdx.x; i < NLB * kMaxWin; i += kThreads)
+            s_term[i / kMaxWin][i % kMaxWin] = p.term[i / kMaxWin][i % kMaxWin];
+    }
+    __syncthreads();
+
+    const uint64_t nw = (uint64_t)gridDim.x * Geo::WARPS;
+    const uint64_t pol = policy_evict_first();
+    const uint64_t base = __ldg(p.off);
+    const TV* tab = static_cast<const TV*>(p.table);
+    uint32_t err = 0;
+
+    // ---- id iterator (two steps ahead of the producer)
+    uint64_t it_t = p.t_begin + (uint64_t)blockIdx.x * Geo::WARPS + wib;
+    uint64_t it_a = 0, nx_a = 0, nx_b = 0;
+    uint32_t it_n = 0, it_k0 = 0;
+    bool it_valid = it_t < p.t_end;
+    auto fetch_next_offsets = [&](uint64_t tn) {
+        if (tn < p.t_end) { nx_a = __ldg(p.off + tn); nx_b = __ldg(p.off + tn + 1); }
+    };
+    auto enter_trial = [&](uint64_t a, uint64_t b) {
+        if (b < a) { err |= ERRBIT_OFFSETS; b = a; }
+        it_a = a - base;
+        it_n = (uint32_t)(b - a);
+        it_k0 = 0;
+    };
+    if (it_valid) {
+        enter_trial(__ldg(p.off + it_t), __ldg(p.off + it_t + 1));
+        fetch_next_offsets(it_t + nw);
+    }
+    auto it_advance = [&]() {
+        it_k0 += 32u;
+        if (it_k0 >= it_n) {
+            it_t += nw;
+            it_valid = it_t < p.t_end;
+            if (it_valid) {
+                enter_trial(nx_a, nx_b);
+                fetch_next_offsets(it_t + nw);
+            }
+        }
+    };
+    // queue of two steps whose ids are in flight
+    uint64_t q_t[2];
+    uint32_t q_n[2], q_k0[2], q_e[2];
+    uint64_t q_a[2];
+    auto load_step = [&](int slot) {
+        if (it_valid) {
+            q_t[slot] = it_t;
+            q_a[slot] = it_a;
+            q_n[slot] = it_n;
+            q_k0[slot] = it_k0;
+            const uint32_t k = it_k0 + lane;
+            uint32_t v = 0u;
+            if (k < it_n) {
+                v = ld_stream_u32(p.ids + it_a + k, pol);
+                if (v == 0u || v > p.catalog) { err |= ERRBIT_EVENT_RANGE; v = 0u; }
+            }
+            q_e[slot] = v;
+            it_advance();
+        } else {
+            q_t[slot] = ~0ull;
+            q_e[slot] = 0u;
+        }
+    };
+    load_step(0);
+    load_step(1);
+
+    double G[NLB];
+    uint32_t m[NLB];
+#pragma unroll
+    for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
+
+#pragma unroll 1
+    for (uint32_t j = 0;; ++j) {
+        // ---- producer: issue the rows of step j into ring slot j % NS
+        {
+            const uint64_t ct = q_t[0];
+            const uint32_t cn = q_n[0], ck0 = q_k0[0], ce = q_e[0];
+            q_t[0] = q_t[1]; q_n[0] = q_n[1]; q_k0[0] = q_k0[1]; q_e[0] = q_e[1]; q_a[0] = q_a[1];
+            load_step(1);
+            const uint32_t slot = j % NS;
+            if (ct != ~0ull) {
+                const TV* row = tab + (uint64_t)ce * p.row_stride;
+                const uint32_t src_bytes = ce ? 16u : 0u;   // lanes without an event: zero-fill
+                const uint32_t dst = ring + slot * Geo::STAGE;
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    const TV* src = row + p.sec_off[c >> 1] + (c & 1) * (8 / sizeof(TV) * 2);
+                    cp_async16(dst + ((c ^ (lane & (CH - 1))) << 4), src, src_bytes);
+                }
+            }
+            if (lane == 0) meta[slot] = StepMeta{ct, cn, ck0};
+            cp_commit();
+        }
+        // ---- consumer: retire step j - (NS - 1)
+        if (j + 1 >= (uint32_t)NS) {
+            cp_wait<NS - 1>();
+            __syncwarp();
+            const uint32_t slot = (j + 1) % NS;   // == (j - (NS - 1)) % NS
+            const StepMeta md = meta[slot];
+            if (md.t == ~0ull) break;
+            Row<TV, NSEC> r;
+            const uint32_t src = ring + slot * Geo::STAGE;
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                uint4 v;
+                asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                             : "r"(src + ((c ^ (lane & (CH - 1))) << 4)));
+                memcpy(&r.x[c >> 1][(c & 1) * (16 / sizeof(TV))], &v, 16);
+            }
+            event_compute<TV, NSEC, NLB>(p, s_term, r, G, m);
+            if (md.k0 + 32u >= md.n) {   // last step of trial md.t: a7 + a8
+#pragma unroll
+                for (int l = 0; l < NLB; ++l) {
+#pragma unroll
+                    for (int off = 16; off >= 1; off >>= 1) {
+                        G[l] = __dadd_rn(G[l], __shfl_xor_sync(0xffffffffu, G[l], off));
+                        m[l] += __shfl_xor_sync(0xffffffffu, m[l], off);
+                    }
+                }
+                if (lane == 0) {
+                    const uint64_t t = md.t;
+                    double port = 0.0;
+                    if (p.portfolio_mode == 1) port = p.ylt[(uint64_t)p.portfolio_row * p.ld + t];
+#pragma unroll
+                    for (int l = 0; l < NLB; ++l) {
+                        if (l >= (int)p.n_layers) break;
+                        const double y = terms(G[l], p.lw[l].agg_r, p.lw[l].agg_l);
+                        p.ylt[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = y;
+                        if (p.lossy) p.lossy[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = m[l];
+                        port = __dadd_rn(port, y);
+                    }
+                    if (p.portfolio_mode >= 0) p.ylt[(uint64_t)p.portfolio_row * p.ld + t] = port;
+                }
+#pragma unroll
+                for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
+            }
+            __syncwarp();
+        }
+    }
+    cp_wait<0>();
+    if (err) atomicOr(p.err, err);
+}
+
+// ---------------------------------------------------------------------------
+// TMA variant (default for fp64 128-B windows).  The row windows are gathered
+// by the Tensor Memory Accelerator with tile::gather4 (4 rows per instruction,
+// UTMALDG.2D.GATHER4) into a per-warp shared-memory ring NS stages deep; an
+// mbarrier per stage counts the landed bytes (complete_tx).  No registers are
+// held by in-flight rows, so ~(NS-1) x 4 KB per warp stays in flight and the
+// TMA's own address translation keeps the random 128-B gathers off the LSU
+// and TLB paths (measured: 9.5 TB/s vs 8.0 TB/s for LDG gathers of 128-B rows
+// from a 256 MB table, tools/microbench.py).  The TMA box is the layer's
+// window in its column block, swizzled (128/64/32B) so that each lane's read
+// of its own row is bank-conflict free.  Same lane mapping, per-lane order
+// and arithmetic as trial_kernel: identical YLT bits.
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, uint32_t bar, int32_t col,
+                                            uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(col), "r"(r0), "r"(r1),
+        "r"(r2), "r"(r3)
+        : "memory");
+}
+
+template <typename TV, int NSEC>
+struct TmaGeo {
+    static constexpr int WARPS = kThreads / 32;
+    static constexpr int ROWB = NSEC * kSectorBytes;   // bytes per gathered row (= TMA box)
+    static constexpr int CH = ROWB / 16;
+    static constexpr int STAGE = 32 * ROWB;            // one row per lane
+    static constexpr int NS0 = (192 * 1024) / (WARPS * STAGE);
+    static constexpr int NS = NS0 > 8 ? 8 : (NS0 < 2 ? 2 : NS0);
+    static constexpr int BYTES = WARPS * NS * STAGE + 1024;   // + alignment slack
+};
+
+template <typename TV, int NSEC, int NLB>
+__global__ void __launch_bounds__(kThreads, 1) trial_kernel_tma(const __grid_constant__ TrialParams p) {
+    using Geo = TmaGeo<TV, NSEC>;
+    constexpr int NS = Geo::NS, CH = Geo::CH;
+    constexpr int QD = 8;              // id stage runs QD steps ahead of the gathers
+    constexpr int IR = QD + 1;         // id ring slots
+    constexpr int MR = QD + NS;        // step-metadata ring slots
+    constexpr bool SM = TermsInSmem<TV, NSEC, NLB>::value;
+    extern __shared__ unsigned char smem_dyn[];
+    __shared__ __align__(8) uint64_t bars[Geo::WARPS][NS];
+    __shared__ StepMeta meta[Geo::WARPS][MR];
+    __shared__ __align__(16) uint32_t idring[Geo::WARPS][IR][32];
+    __shared__ double2 s_term[SM ? NLB : 1][kMaxWin];
+    const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+    const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(smem_dyn) + 1023u) & ~1023u;
+    const uint32_t ring = sbase + wib * NS * Geo::STAGE;
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&bars[wib][0]);
+    const uint32_t id0 = (uint32_t)__cvta_generic_to_shared(&idring[wib][0][0]);
+    if (lane == 0)
+        for (int s = 0; s < NS; ++s) mbar_init(bar0 + 8u * s, 1u);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (SM) {
+        for (int i = threadIdx.x; i < NLB * kMaxWin; i += kThreads)
+            s_term[i / kMaxWin][i % kMaxWin] = p.term[i / kMaxWin][i % kMaxWin];
+    }
+    __syncthreads();
+
+    const uint64_t nw = (uint64_t)gridDim.x * Geo::WARPS;
+    const uint64_t base = __ldg(p.off);
+    uint32_t err = 0;
+    // lane's conflict-free chunk permutation (matches the map's swizzle mode)
+    const uint32_t swz = (lane * (uint32_t)Geo::ROWB / 128u) & (uint32_t)(CH - 1);
+
+    // ---- id stage: a step iterator QD steps ahead of the gathers.  Each lane
+    // copies its event id of the step straight into the id ring (cp.async,
+    // zero-filled past the trial's end); lane 0 records the step metadata.
+    uint64_t it_t = p.t_begin + (uint64_t)blockIdx.x * Geo::WARPS + wib;
+    uint64_t it_a = 0, nx_a = 0, nx_b = 0;
+    uint32_t it_n = 0, it_k0 = 0;
+    bool it_valid = it_t < p.t_end;
+    auto fetch_next_offsets = [&](uint64_t tn) {
+        if (tn < p.t_end) { nx_a = __ldg(p.off + tn); nx_b = __ldg(p.off + tn + 1); }
+    };
+    auto enter_trial = [&](uint64_t a, uint64_t b) {
+        if (b < a) { err |= ERRBIT_OFFSETS; b = a; }
+        it_a = a - base;
+        it_n = (uint32_t)(b - a);
+        it_k0 = 0;
+    };
+    if (it_valid) {
+        enter_trial(__ldg(p.off + it_t), __ldg(p.off + it_t + 1));
+        fetch_next_offsets(it_t + nw);
+    }
+    auto id_stage = [&](uint32_t step) {
+        StepMeta md{~0ull, 0u, 0u};
+        if (it_valid) {
+            md = StepMeta{it_t, it_n, it_k0};
+            const uint32_t k = it_k0 + lane;
+            const uint32_t* src = p.ids + it_a + (k < it_n ? k : 0u);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(id0 + ((step % IR) * 32u + lane) * 4u),
+                         "l"(src), "r"(k < it_n ? 4u : 0u)
+                         : "memory");
+            it_k0 += 32u;
+            if (it_k0 >= it_n) {
+                it_t += nw;
+                it_valid = it_t < p.t_end;
+                if (it_valid) {
+                    enter_trial(nx_a, nx_b);
+                    fetch_next_offsets(it_t + nw);
+                }
+            }
+        }
+        if (lane == 0) meta[wib][step % MR] = md;
+        cp_commit();
+    };
+    for (uint32_t s = 0; s < (uint32_t)QD; ++s) id_stage(s);
+
+    double G[NLB];
+    uint32_t m[NLB];
+#pragma unroll
+    for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
+    const int32_t col = (int32_t)p.tma_col;
+
+#pragma unroll 1
+    for (uint32_t j = 0;; ++j) {
+        id_stage(j + QD);
+        // ---- producer: ids of step j are in the ring; gather its rows into slot j % NS
+        cp_wait<QD>();
+        __syncwarp();
+        {
+            const StepMeta md = meta[wib][j % MR];
+            const uint32_t slot = j % NS;
+            if (md.t != ~0ull) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the slot
+                if (lane == 0) mbar_expect_tx(bar0 + 8u * slot, (uint32_t)Geo::STAGE);
+                __syncwarp();
+                if (lane < 8u) {
+                    uint4 e4;
+                    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(e4.x), "=r"(e4.y), "=r"(e4.z), "=r"(e4.w)
+                                 : "r"(id0 + ((j % IR) * 32u + lane * 4u) * 4u));
+                    uint32_t e[4] = {e4.x, e4.y, e4.z, e4.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {   // fused YET validation (A14)
+                        const bool live = md.k0 + lane * 4u + i < md.n;
+                        if (live && (e[i] == 0u || e[i] > p.catalog)) err |= ERRBIT_EVENT_RANGE;
+                        if (!live || e[i] > p.catalog) e[i] = 0u;
+                    }
+                    tma_gather4(ring + slot * Geo::STAGE + lane * 4u * Geo::ROWB, &p.tmap, bar0 + 8u * slot, col,
+                                e[0], e[1], e[2], e[3]);
+                }
+            }
+        }
+        // ---- consumer: retire step c = j - (NS - 1)
+        if (j + 1 >= (uint32_t)NS) {
+            const uint32_t c = j + 1 - NS;
+            const uint32_t slot = c % NS;
+            const StepMeta md = meta[wib][c % MR];
+            if (md.t == ~0ull) break;
+            mbar_wait(bar0 + 8u * slot, (c / NS) & 1u);
+            Row<TV, NSEC> r;
+            const uint32_t src = ring + slot * Geo::STAGE + lane * Geo::ROWB;
+#pragma unroll
+            for (int q = 0; q < CH; ++q) {
+                uint4 v;
+                asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                             : "r"(src + (((uint32_t)q ^ swz) << 4)));
+                memcpy(&r.x[q >> 1][(q & 1) * (16 / sizeof(TV))], &v, 16);
+            }
+            event_compute<TV, NSEC, NLB>(p, s_term, r, G, m);
+            if (md.k0 + 32u >= md.n) {   // last step of trial md.t: a7 + a8
+#pragma unroll
+                for (int l = 0; l < NLB; ++l) {
+#pragma unroll
+                    for (int off = 16; off >= 1; off >>= 1) {
+                        G[l] = __dadd_rn(G[l], __shfl_xor_sync(0xffffffffu, G[l], off));
+                        m[l] += __shfl_xor_sync(0xffffffffu, m[l], off);
+                    }
+                }
+                if (lane == 0) {
+                    const uint64_t t = md.t;
+                    double port = 0.0;
+                    if (p.portfolio_mode == 1) port = p.ylt[(uint64_t)p.portfolio_row * p.ld + t];
+#pragma unroll
+                    for (int l = 0; l < NLB; ++l) {
+                        if (l >= (int)p.n_layers) break;
+                        const double y = terms(G[l], p.lw[l].agg_r, p.lw[l].agg_l);
+                        p.ylt[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = y;
+                        if (p.lossy) p.lossy[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = m[l];
+                        port = __dadd_rn(port, y);
+                    }
+                    if (p.portfolio_mode >= 0) p.ylt[(uint64_t)p.portfolio_row * p.ld + t] = port;
+                }
+#pragma unroll
+                for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
+            }
+        }
+        __syncwarp();   // id-ring / slot reads of this iteration precede the next writes
+    }
+    cp_wait<0>();
+    if (err) atomicOr(p.err, err);
+}
+
 // Wide layers (window > kMaxSec sectors): same arithmetic and lane mapping,
-// one layer per launch, scalar loads, runtime column loop.
+// one layer per launch, scalar loads through the column-block address map.
 template <typename TV>
 __global__ void __launch_bounds__(kThreads) trial_kernel_wide(const __grid_constant__ TrialParams p,
                                                               const double2* __restrict__ cterm,
@@ -218,26 +697,24 @@ __global__ void __launch_bounds__(kThreads) trial_kernel_wide(const __grid_const
         const uint32_t* ids = p.ids + (a - base);
         double G = 0.0;
         uint32_t m = 0;
-        for (uint64_t k0 = 0; k0 < n; k0 += 128) {
-            for (int q = 0; q < 4; ++q) {
-                const uint64_t k = k0 + 32u * q + lane;
-                uint32_t v = 0u;
-                if (k < n) {
-                    v = __ldg(ids + k);
-                    if (v == 0u || v > p.catalog) { err |= ERRBIT_EVENT_RANGE; v = 0u; }
-                }
-                double le = 0.0;
-                if (v) {
-                    const TV* row = tab + (uint64_t)v * p.row_elems + col0;
-                    for (uint32_t c = 0; c < ncol; ++c) {
-                        const double2 tc = cterm[c];
-                        le = __dadd_rn(le, terms((double)__ldg(row + c), tc.x, tc.y));
-                    }
-                }
-                const double o = terms(le, p.lw[0].occ_r, p.lw[0].occ_l);
-                G = __dadd_rn(G, o);
-                m += (o > 0.0) ? 1u : 0u;
+        for (uint64_t k0 = 0; k0 < n; k0 += 32) {
+            const uint64_t k = k0 + lane;
+            uint32_t v = 0u;
+            if (k < n) {
+                v = __ldg(ids + k);
+                if (v == 0u || v > p.catalog) { err |= ERRBIT_EVENT_RANGE; v = 0u; }
             }
+            double le = 0.0;
+            for (uint32_t c = 0; c < ncol; ++c) {
+                const uint32_t j = col0 + c;
+                const double2 tc = cterm[c];
+                const double x = (double)__ldg(tab + (uint64_t)(j / p.row_stride) * p.block_stride +
+                                               (uint64_t)v * p.row_stride + j % p.row_stride);
+                le = __dadd_rn(le, terms(x, tc.x, tc.y));
+            }
+            const double o = terms(le, p.lw[0].occ_r, p.lw[0].occ_l);
+            G = __dadd_rn(G, o);
+            m += (o > 0.0) ? 1u : 0u;
         }
         for (int off = 16; off >= 1; off >>= 1) {
             G = __dadd_rn(G, __shfl_xor_sync(0xffffffffu, G, off));
@@ -248,7 +725,7 @@ __global__ void __launch_bounds__(kThreads) trial_kernel_wide(const __grid_const
             p.ylt[(uint64_t)p.ylt_row0 * p.ld + t] = y;
             if (p.lossy) p.lossy[(uint64_t)p.ylt_row0 * p.ld + t] = m;
             if (p.portfolio_mode >= 0) {
-                double port = p.portfolio_mode == 1 ? p.ylt[(uint64_t)p.portfolio_row * p.ld + t] : 0.0;
+                const double port = p.portfolio_mode == 1 ? p.ylt[(uint64_t)p.portfolio_row * p.ld + t] : 0.0;
                 p.ylt[(uint64_t)p.portfolio_row * p.ld + t] = __dadd_rn(port, y);
             }
         }
@@ -256,60 +733,110 @@ __global__ void __launch_bounds__(kThreads) trial_kernel_wide(const __grid_const
     if (err) atomicOr(p.err, err);
 }
 
-template <typename TV, int NSEC, int NLB, bool SHARE>
-struct Inst {
-    static void* fn() { return (void*)trial_kernel<TV, NSEC, NLB, SHARE>; }
-};
-
-template <typename TV, int NLB, bool SHARE>
+template <typename TV, int NLB, int D, int MINB = 2>
 void* pick_nsec(uint32_t nsec) {
-    if (nsec <= 1) return Inst<TV, 1, NLB, SHARE>::fn();
-    if (nsec <= 2) return Inst<TV, 2, NLB, SHARE>::fn();
-    if (nsec <= 4) return Inst<TV, 4, NLB, SHARE>::fn();
-    return Inst<TV, 8, NLB, SHARE>::fn();
+    if (nsec <= 1) return (void*)trial_kernel<TV, 1, NLB, D, MINB>;
+    if (nsec <= 2) return (void*)trial_kernel<TV, 2, NLB, D, MINB>;
+    if (nsec <= 4) return (void*)trial_kernel<TV, 4, NLB, D, MINB>;
+    return (void*)trial_kernel<TV, 8, NLB, D, MINB>;
+}
+
+// variant: 0 = no prefetch (D = 1), 2 = prefetch 2 steps ahead (D = 3),
+// 3 = 4 steps ahead (D = 5), 4 = 7 steps ahead (D = 8).
+template <typename TV>
+void* pick(uint32_t nsec, int nl, int variant) {
+    if (nl <= 1) {
+        if (variant == 2) return pick_nsec<TV, 1, 3>(nsec);
+        if (variant == 3) return pick_nsec<TV, 1, 5>(nsec);
+        if (variant == 4) return pick_nsec<TV, 1, 8>(nsec);
+        if (variant == 5) return pick_nsec<TV, 1, 1, 3>(nsec);
+        if (variant == 6) return pick_nsec<TV, 1, 1, 4>(nsec);
+        if (variant == 7) return pick_nsec<TV, 1, 3, 3>(nsec);
+        return pick_nsec<TV, 1, 1>(nsec);
+    }
+    if (nl <= 2) return pick_nsec<TV, 2, 1>(nsec);
+    return pick_nsec<TV, 4, 1>(nsec);
+}
+
+template <typename TV, int NLB>
+void* pick_nsec_sm(uint32_t nsec, int* smem) {
+    if (nsec <= 1) { *smem = SmGeo<TV, 1>::BYTES; return (void*)trial_kernel_sm<TV, 1, NLB>; }
+    if (nsec <= 2) { *smem = SmGeo<TV, 2>::BYTES; return (void*)trial_kernel_sm<TV, 2, NLB>; }
+    if (nsec <= 4) { *smem = SmGeo<TV, 4>::BYTES; return (void*)trial_kernel_sm<TV, 4, NLB>; }
+    *smem = SmGeo<TV, 8>::BYTES;
+    return (void*)trial_kernel_sm<TV, 8, NLB>;
 }
 
 template <typename TV>
-void* pick(uint32_t nsec, bool share, int nl) {
-    if (nl <= 1) return pick_nsec<TV, 1, false>(nsec);
-    if (nl <= 2) return share ? pick_nsec<TV, 2, true>(nsec) : pick_nsec<TV, 2, false>(nsec);
-    return share ? pick_nsec<TV, 4, true>(nsec) : pick_nsec<TV, 4, false>(nsec);
+void* pick_sm(uint32_t nsec, int nl, int* smem) {
+    if (nl <= 1) return pick_nsec_sm<TV, 1>(nsec, smem);
+    if (nl <= 2) return pick_nsec_sm<TV, 2>(nsec, smem);
+    return pick_nsec_sm<TV, 4>(nsec, smem);
 }
 
-void* pick_kernel(int fp32, uint32_t nsec, bool share, int nl) {
-    return fp32 ? pick<float>(nsec, share, nl) : pick<double>(nsec, share, nl);
+template <typename TV, int NLB>
+void* pick_nsec_tma(uint32_t nsec, int* smem) {
+    if (nsec <= 1) { *smem = TmaGeo<TV, 1>::BYTES; return (void*)trial_kernel_tma<TV, 1, NLB>; }
+    if (nsec <= 2) { *smem = TmaGeo<TV, 2>::BYTES; return (void*)trial_kernel_tma<TV, 2, NLB>; }
+    *smem = TmaGeo<TV, 4>::BYTES;
+    return (void*)trial_kernel_tma<TV, 4, NLB>;
+}
+
+template <typename TV>
+void* pick_tma(uint32_t nsec, int nl, int* smem) {
+    if (nl <= 1) return pick_nsec_tma<TV, 1>(nsec, smem);
+    if (nl <= 2) return pick_nsec_tma<TV, 2>(nsec, smem);
+    return pick_nsec_tma<TV, 4>(nsec, smem);
+}
+
+// variant: 0 = register-pipelined, 1 = shared-memory staged (cp.async ring),
+// 2-4 = register + L2 prefetch, 5-7 = register at higher occupancy,
+// 8 = TMA gather4 ring (needs p.tmap; windows of <= 4 sectors in one block).
+void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
+    *smem = 0;
+    if (variant == 8 && nsec <= 4)
+        return fp32 ? pick_tma<float>(nsec, nl, smem) : pick_tma<double>(nsec, nl, smem);
+    if (nsec > (uint32_t)kMaxSec) return fp32 ? (void*)trial_kernel_wide<float> : (void*)trial_kernel_wide<double>;
+    if (variant == 1) return fp32 ? pick_sm<float>(nsec, nl, smem) : pick_sm<double>(nsec, nl, smem);
+    return fp32 ? pick<float>(nsec, nl, variant) : pick<double>(nsec, nl, variant);
 }
 
 }  // namespace
 
-int trial_kernel_grid(int fp32, uint32_t max_nsec, bool shared_window, int n_layers) {
-    int dev = 0, nsm = 148, per_sm = 1;
+int trial_kernel_grid(int fp32, uint32_t max_nsec, int n_layers, int variant) {
+    static int cache[16][2][kMaxSec + 2][kMaxLB + 1] = {};
+    const uint32_t ns = max_nsec > (uint32_t)kMaxSec ? kMaxSec + 1 : max_nsec;
+    int& c = cache[variant & 15][fp32 ? 1 : 0][ns][n_layers];
+    if (c) return c;
+    int dev = 0, nsm = 148, per_sm = 1, smem = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    void* fn = max_nsec > (uint32_t)kMaxSec
-                   ? (fp32 ? (void*)trial_kernel_wide<float> : (void*)trial_kernel_wide<double>)
-                   : pick_kernel(fp32, max_nsec, shared_window, n_layers);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0) != cudaSuccess ||
-        per_sm < 1) {
+    void* fn = pick_kernel(fp32, max_nsec, n_layers, variant, &smem);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess || per_sm < 1) {
         cudaGetLastError();
         per_sm = 1;
     }
-    return nsm * per_sm;
+    c = nsm * per_sm;
+    return c;
 }
 
-cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, bool shared_window,
-                          int grid, cudaStream_t s) {
+cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int grid, int variant, cudaStream_t s) {
     if (p.t_end <= p.t_begin) return cudaSuccess;
-    const uint64_t warps = p.t_end - p.t_begin;
-    const uint64_t need = (warps * 32 + kThreads - 1) / kThreads;
+    const uint64_t need = ((p.t_end - p.t_begin) * 32 + kThreads - 1) / kThreads;
     const int g = (int)((uint64_t)grid < need ? (uint64_t)grid : need);
-    void* fn = pick_kernel(fp32, max_nsec, shared_window, (int)p.n_layers);
+    int smem = 0;
+    void* fn = pick_kernel(fp32, max_nsec, (int)p.n_layers, variant, &smem);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+    }
     void* args[] = {(void*)&p};
-    return cudaLaunchKernel(fn, dim3(g), dim3(kThreads), args, 0, s);
+    return cudaLaunchKernel(fn, dim3(g), dim3(kThreads), args, (size_t)smem, s);
 }
 
-cudaError_t launch_trials_wide(const TrialParams& p, int fp32, const double2* d_cterm, uint32_t col0,
-                               uint32_t ncol, int grid, cudaStream_t s) {
+cudaError_t launch_trials_wide(const TrialParams& p, int fp32, const double2* d_cterm, uint32_t col0, uint32_t ncol,
+                               int grid, cudaStream_t s) {
     if (p.t_end <= p.t_begin) return cudaSuccess;
     const uint64_t need = ((p.t_end - p.t_begin) * 32 + kThreads - 1) / kThreads;
     const int g = (int)((uint64_t)grid < need ? (uint64_t)grid : need);

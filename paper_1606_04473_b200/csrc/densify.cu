@@ -2,9 +2,10 @@
 //
 // "ELTs corresponding to a Layer were implemented as direct
 // access tables ... Each ELT is implemented as an independent table".  On B200
-// the tables are interleaved instead: tab[e][j] holds ELT j's loss for event
-// e, so the E losses one event needs are one contiguous row (one 128-B line
-// for 16 fp64 ELTs) rather than E scattered sectors.  Row 0 stays zero (event
+// the tables are interleaved instead: within a column block tab[e][j] holds
+// ELT j's loss for event e, so the E losses one event needs are one
+// contiguous row (one 128-B line for 16 fp64 ELTs) rather than E scattered
+// sectors (geometry: ara::TableGeo).  Row 0 stays zero (event
 // ids are 1-based, reading A14); a missing (event, ELT) pair reads 0 (A4).
 //
 // The table was zero-filled by cudaMemsetAsync; this kernel scatters the
@@ -21,7 +22,7 @@ __global__ void __launch_bounds__(256) densify_kernel(const uint64_t* __restrict
                                                       const uint32_t* __restrict__ ev,
                                                       const double* __restrict__ loss,
                                                       uint32_t catalog, TV* __restrict__ tab,
-                                                      uint64_t row_elems, uint32_t* err) {
+                                                      uint32_t epb, uint64_t block_elems, uint32_t* err) {
     const uint32_t j = blockIdx.y;
     const uint64_t lo = eoff[j], hi = eoff[j + 1];
     uint32_t bad = 0;
@@ -35,7 +36,7 @@ __global__ void __launch_bounds__(256) densify_kernel(const uint64_t* __restrict
             bad |= ERRBIT_ELT_LOSS;
             continue;
         }
-        tab[(uint64_t)e * row_elems + j] = (TV)(x + 0.0);   // canonical +0 (A16)
+        tab[(uint64_t)(j / epb) * block_elems + (uint64_t)e * epb + j % epb] = (TV)(x + 0.0);   // canonical +0 (A16)
     }
     if (bad) atomicOr(err, bad);
 }
@@ -44,7 +45,7 @@ __global__ void __launch_bounds__(256) densify_kernel(const uint64_t* __restrict
 
 cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const double* d_loss,
                            uint32_t n_elts, uint64_t n_records, uint32_t catalog, void* d_table,
-                           uint64_t row_elems, int fp32, uint32_t* d_err, cudaStream_t s) {
+                           const TableGeo& geo, int fp32, uint32_t* d_err, cudaStream_t s) {
     if (n_records == 0) return cudaSuccess;
     uint64_t per = (n_records + n_elts - 1) / n_elts;
     uint64_t bx = (per + 255) / 256;
@@ -53,10 +54,10 @@ cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const d
     dim3 grid((unsigned)bx, n_elts);
     if (fp32)
         densify_kernel<float><<<grid, 256, 0, s>>>(d_eoff, d_ev, d_loss, catalog,
-                                                   static_cast<float*>(d_table), row_elems, d_err);
+                                                   static_cast<float*>(d_table), geo.epb, geo.block_elems, d_err);
     else
         densify_kernel<double><<<grid, 256, 0, s>>>(d_eoff, d_ev, d_loss, catalog,
-                                                    static_cast<double*>(d_table), row_elems, d_err);
+                                                    static_cast<double*>(d_table), geo.epb, geo.block_elems, d_err);
     return cudaGetLastError();
 }
 

@@ -112,3 +112,118 @@ extern "C" double mb_gather(uint64_t table_bytes, uint32_t row_bytes, uint64_t n
     cudaFree(out);
     return cudaGetLastError() == cudaSuccess ? ms : -1;
 }
+
+// ---------------------------------------------------------------------------
+// TMA tile::gather4 gather ceiling: each warp owns NSTG smem stages of 32 rows;
+// lanes 0..7 each issue one gather4 (4 hashed rows) per stage; completion via
+// one mbarrier per stage (complete_tx).  Measures rows/s the TMA engine can
+// gather from a `table_bytes` table with `row_bytes` rows.
+#include <cuda.h>
+
+namespace {
+constexpr int MB_WARPS = 8, MB_NSTG = 6;
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(cnt));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity) : "memory");
+}
+
+__global__ void __launch_bounds__(MB_WARPS * 32, 1) tma_gather_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                       uint32_t n_rows, uint32_t row_bytes,
+                                                                       uint64_t steps_per_warp, uint32_t seed,
+                                                                       double* out) {
+    extern __shared__ __align__(1024) unsigned char sm[];
+    __shared__ __align__(8) uint64_t bars[MB_WARPS][MB_NSTG];
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t stage_bytes = 32 * row_bytes;
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(sm) + w * MB_NSTG * stage_bytes;
+    if (lane == 0)
+        for (int s = 0; s < MB_NSTG; ++s) mbar_init((uint32_t)__cvta_generic_to_shared(&bars[w][s]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    double acc = 0;
+    const uint64_t gwarp = (uint64_t)blockIdx.x * MB_WARPS + w;
+    auto issue = [&](uint64_t step, int s) {
+        const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&bars[w][s]);
+        uint32_t r = hash32((gwarp * steps_per_warp + step) * 32 + lane + seed) % n_rows;
+        uint32_t r0 = __shfl_sync(0xffffffffu, r, (lane & 7) * 4 + 0);
+        uint32_t r1 = __shfl_sync(0xffffffffu, r, (lane & 7) * 4 + 1);
+        uint32_t r2 = __shfl_sync(0xffffffffu, r, (lane & 7) * 4 + 2);
+        uint32_t r3 = __shfl_sync(0xffffffffu, r, (lane & 7) * 4 + 3);
+        if (lane == 0) mbar_expect_tx(bar, stage_bytes);
+        __syncwarp();
+        if (lane < 8) {
+            const uint32_t dst = base + s * stage_bytes + lane * 4 * row_bytes;
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(dst), "l"(&tmap), "r"(bar), "r"(0), "r"(r0),
+                "r"(r1), "r"(r2), "r"(r3)
+                : "memory");
+        }
+    };
+    for (int s = 0; s < MB_NSTG - 1 && s < (int)steps_per_warp; ++s) issue(s, s);
+    for (uint64_t step = 0; step < steps_per_warp; ++step) {
+        const int s = (int)(step % MB_NSTG);
+        if (step + MB_NSTG - 1 < steps_per_warp) issue(step + MB_NSTG - 1, (int)((step + MB_NSTG - 1) % MB_NSTG));
+        mbar_wait((uint32_t)__cvta_generic_to_shared(&bars[w][s]), (uint32_t)((step / MB_NSTG) & 1));
+        double v;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(base + s * stage_bytes + lane * row_bytes));
+        acc += v;
+        __syncwarp();
+    }
+    if (acc == 123.456) out[0] = acc;
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+struct TArg { CUtensorMap tm; uint32_t n_rows, row_bytes; uint64_t spw; uint32_t seed; double* out; int grid; int smem; };
+void launch_tma(void* v) {
+    TArg* a = (TArg*)v;
+    a->seed += 0x9e3779;
+    tma_gather_kernel<<<a->grid, MB_WARPS * 32, a->smem>>>(a->tm, a->n_rows, a->row_bytes, a->spw, a->seed, a->out);
+}
+}  // namespace
+
+extern "C" double mb_tma_gather(uint64_t table_bytes, uint32_t row_bytes, uint64_t n_gathers, int iters) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return -2;
+    double *tab = nullptr, *out = nullptr;
+    if (cudaMalloc(&tab, table_bytes + 4096) != cudaSuccess || cudaMalloc(&out, 64) != cudaSuccess) return -1;
+    cudaMemset(tab, 0, table_bytes);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    TArg a{};
+    a.n_rows = (uint32_t)(table_bytes / row_bytes);
+    a.row_bytes = row_bytes;
+    cuuint64_t gdim[2] = {row_bytes / 8, a.n_rows};
+    cuuint64_t gstr[1] = {row_bytes};
+    cuuint32_t box[2] = {row_bytes / 8, 1};
+    cuuint32_t est[2] = {1, 1};
+    CUresult r = ((EncodeTiledFn)fn)(&a.tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, tab, gdim, gstr, box, est,
+                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                     CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return -3 - (double)r;
+    a.grid = nsm;
+    a.spw = n_gathers / 32 / ((uint64_t)nsm * MB_WARPS);
+    a.smem = MB_WARPS * MB_NSTG * 32 * row_bytes;
+    a.seed = 7;
+    a.out = out;
+    cudaFuncSetAttribute(tma_gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem);
+    float ms = time_it(launch_tma, &a, iters);
+    cudaError_t e = cudaGetLastError();
+    cudaFree(tab);
+    cudaFree(out);
+    if (e != cudaSuccess) return -100 - (double)e;
+    // report ms scaled to n_gathers rows
+    return ms * (double)n_gathers / (double)(a.spw * 32 * (uint64_t)nsm * MB_WARPS);
+}

@@ -30,12 +30,27 @@ def run_oracle(off, ids, elts, w, layers, fp32=False, terms=None):
                       oracle.layers_from_specs(layers), lookup="dense", fp32_storage=fp32)
 
 
+KERNEL_VARIANTS = (-1, 0, 1, 5, 8)   # ARA_KERNEL: auto, register, cp.async ring, register/3 CTAs, TMA gather4
+
+
 def run_gpu(off, ids, elts, w, layers, precision="f64", terms=None, load_mode="all", chunk_trials=0,
-            device_inputs=False, return_periods=None):
+            device_inputs=False, return_periods=None, variant=None):
+    import os
     import torch
     from paper_1606_04473_b200 import ara
     d, li = (w.elt_terms() if terms is None else terms)
-    with ara.Context(w.catalog, precision=precision, load_mode=load_mode, chunk_trials=chunk_trials) as ctx:
+    old = os.environ.get("ARA_KERNEL")
+    if variant is not None:
+        os.environ["ARA_KERNEL"] = str(variant)
+    try:
+        ctx = ara.Context(w.catalog, precision=precision, load_mode=load_mode, chunk_trials=chunk_trials)
+    finally:
+        if variant is not None:
+            if old is None:
+                os.environ.pop("ARA_KERNEL", None)
+            else:
+                os.environ["ARA_KERNEL"] = old
+    with ctx:
         eo, ev, ls = elts
         if device_inputs:
             t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()

@@ -7,8 +7,8 @@ import pytest
 
 import oracle
 import synth
-from parity_util import (RTOL, assert_metrics_close, assert_ylt_close, make_inputs, oracle_rows,
-                         run_gpu, run_oracle)
+from parity_util import (KERNEL_VARIANTS, RTOL, assert_metrics_close, assert_ylt_close, make_inputs,
+                         oracle_rows, run_gpu, run_oracle)
 
 pytestmark = pytest.mark.gpu
 INF = math.inf
@@ -20,21 +20,23 @@ def _ara():
 
 
 # ------------------------------------------------------------------ tiny configs
+@pytest.mark.parametrize("variant", KERNEL_VARIANTS)
 @pytest.mark.parametrize("precision", ["f64", "f32"])
-def test_tiny(cuda, precision):
+def test_tiny(cuda, precision, variant):
     w = synth.get_config("tiny").with_(return_periods=(1, 2, 3.5, 10, 100, 1000))
     off, ids, elts = make_inputs(w)
     orc = run_oracle(off, ids, elts, w, w.layers, fp32=precision == "f32")
     ylt, lossy, st, met = run_gpu(off, ids, elts, w, w.layers, precision=precision,
-                                  return_periods=w.return_periods)
+                                  return_periods=w.return_periods, variant=variant)
     assert_ylt_close(ylt, orc)
     assert np.array_equal(lossy, orc["lossy"])
     assert_metrics_close(met, oracle_rows(orc), orc["scale"], w.return_periods)
     assert st["n_events_local"] == len(ids) and st["n_lookups_local"] == len(ids) * w.n_elts
 
 
+@pytest.mark.parametrize("variant", KERNEL_VARIANTS)
 @pytest.mark.parametrize("precision,cap", [("f64", 2.0 ** 31), ("f32", 2.0 ** 24)])
-def test_tiny_integer_valued_is_bitwise(cuda, precision, cap):
+def test_tiny_integer_valued_is_bitwise(cuda, precision, cap, variant):
     """P10: integer-valued losses and terms make every sum exact, so the GPU
     must match the oracle bit for bit in any summation order (YLT, portfolio,
     lossy counts, PML, TVaR)."""
@@ -42,7 +44,7 @@ def test_tiny_integer_valued_is_bitwise(cuda, precision, cap):
     off, ids, elts = make_inputs(w)
     orc = run_oracle(off, ids, elts, w, w.layers, fp32=precision == "f32")
     ylt, lossy, _, met = run_gpu(off, ids, elts, w, w.layers, precision=precision,
-                                 return_periods=w.return_periods)
+                                 return_periods=w.return_periods, variant=variant)
     assert np.array_equal(ylt[:-1], orc["ylt"]) and np.array_equal(ylt[-1], orc["portfolio"])
     assert np.array_equal(lossy, orc["lossy"])
     assert_metrics_close(met, oracle_rows(orc), orc["scale"], w.return_periods, exact=True)
@@ -67,7 +69,8 @@ def _edge_yet(C, rng):
     return off, ids
 
 
-def test_edge_trials_and_unaligned_layers(cuda):
+@pytest.mark.parametrize("variant", KERNEL_VARIANTS)
+def test_edge_trials_and_unaligned_layers(cuda, variant):
     rng = np.random.default_rng(9)
     w = synth.get_config("tiny").with_(n_elts=5, catalog=777, rho=0.5, n_trials=16)
     _, _, elts = make_inputs(w)
@@ -76,13 +79,14 @@ def test_edge_trials_and_unaligned_layers(cuda):
               synth.LayerSpec(3, 5, 1e5, 2e5, 1e6, 3e6), synth.LayerSpec(2, 3, 0.0, 1e4, 1e4, INF))
     for precision in ("f64", "f32"):
         orc = run_oracle(off, ids, elts, w, layers, fp32=precision == "f32")
-        ylt, lossy, _, _ = run_gpu(off, ids, elts, w, layers, precision=precision)
+        ylt, lossy, _, _ = run_gpu(off, ids, elts, w, layers, precision=precision, variant=variant)
         assert_ylt_close(ylt, orc)
         assert np.array_equal(lossy, orc["lossy"])
         assert (ylt[:, [0, 6, 15]] == 0).all()
 
 
-def test_wide_windows_tower_and_many_layers(cuda):
+@pytest.mark.parametrize("variant", KERNEL_VARIANTS)
+def test_wide_windows_tower_and_many_layers(cuda, variant):
     """40 ELTs: aligned, unaligned, 8-sector, >8-sector (generic kernel) and
     single-ELT layers; 4 identical windows (shared-load path); 9 layers ->
     three launches with the portfolio accumulated across them."""
@@ -98,7 +102,7 @@ def test_wide_windows_tower_and_many_layers(cuda):
               synth.LayerSpec(8, 24, 1e5, 1e5, 3e5, INF), synth.LayerSpec(8, 24, 0.0, 7e4, 0.0, 9e5))
     for precision in ("f64", "f32"):
         orc = run_oracle(off, ids, elts, w, layers, fp32=precision == "f32", terms=(d, li))
-        ylt, lossy, st, _ = run_gpu(off, ids, elts, w, layers, precision=precision, terms=(d, li))
+        ylt, lossy, st, _ = run_gpu(off, ids, elts, w, layers, precision=precision, terms=(d, li), variant=variant)
         assert_ylt_close(ylt, orc)
         assert np.array_equal(lossy, orc["lossy"])
         assert st["n_kernel_launches"] >= 3
@@ -115,12 +119,16 @@ def test_single_elt_single_event_lookup(cuda):
 
 
 # ------------------------------------------------------------------ invariants
-def test_partition_and_alignment_invariance(cuda):
+@pytest.mark.parametrize("variant", KERNEL_VARIANTS)
+def test_partition_and_alignment_invariance(cuda, variant):
     """P11 on the GPU: shards loaded as independent YETs (different base
     alignment of every trial) reproduce the unsharded YLT bit for bit."""
     w = synth.get_config("tiny").with_(n_trials=1001)
     off, ids, elts = make_inputs(w)
-    full, _, _, _ = run_gpu(off, ids, elts, w, w.layers)
+    full, _, _, _ = run_gpu(off, ids, elts, w, w.layers, variant=variant)
+    for v2 in KERNEL_VARIANTS:                  # every kernel: same summation order, same bits
+        other, _, _, _ = run_gpu(off, ids, elts, w, w.layers, variant=v2)
+        assert np.array_equal(full, other)
     ara = _ara()
     for N in (2, 3, 8, 16):
         parts = []
@@ -130,7 +138,7 @@ def test_partition_and_alignment_invariance(cuda):
             si = ids[int(off[f]):int(off[f + c])]
             if r % 2:                      # misalign the shard by one element
                 si = np.concatenate([np.zeros(1, np.uint32), si])[1:]
-            y, _, _, _ = run_gpu(so, si, elts, w, w.layers)
+            y, _, _, _ = run_gpu(so, si, elts, w, w.layers, variant=variant)
             parts.append(y[:, :c])
         assert np.array_equal(np.concatenate(parts, axis=1), full)
 

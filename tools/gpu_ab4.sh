@@ -1,0 +1,20 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+P="python tools/prof_ara.py --steps 3"
+: > gpurun_out/ab.jsonl
+for k in 0 2 3 4; do
+  for pfn in 1 4; do
+    ARA_KERNEL=$k ARA_PFN=$pfn timeout 300 $P >> gpurun_out/ab.jsonl 2>> gpurun_out/ab.err
+  done
+done
+for k in 0 3 4; do
+  ARA_KERNEL=$k ARA_PFN=2 timeout 300 $P --precision f32 >> gpurun_out/ab.jsonl 2>> gpurun_out/ab.err
+  ARA_KERNEL=$k ARA_PFN=1 timeout 300 $P --precision f32 >> gpurun_out/ab.jsonl 2>> gpurun_out/ab.err
+done
+ARA_KERNEL=3 timeout 300 $P --config multilayer >> gpurun_out/ab.jsonl 2>> gpurun_out/ab.err
+tail -3 gpurun_out/pytest_gpu.log
+python -c "
+import json
+for l in open('gpurun_out/ab.jsonl'):
+    d=json.loads(l); print(d['config'], d['precision'], d['env'], [round(x,3) for x in d['kernel_ms']])
+"
