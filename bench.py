@@ -282,10 +282,10 @@ def main():
             launches.append(st["n_kernel_launches"])
         return st, pml, tvar
 
+    clocks = ClockSampler(local)
+    clocks.start()                       # sampling runs from warm-up through the timed region
     for _ in range(a.warmup):
         st0, pml, tvar = step(False)
-    clocks = ClockSampler(local)
-    clocks.start()
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -297,7 +297,6 @@ def main():
     barrier()
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1)) / a.steps
-    n_events_global = int(max_over_ranks(0) if False else 0)
     ev_local = st["n_events_local"]
     if world > 1:
         t = torch.tensor([ev_local], dtype=torch.int64, device=dev)
@@ -324,17 +323,26 @@ def main():
     e2e = None
     if not a.no_e2e:
         ylt_pin = torch.empty((L + 1) * T, dtype=torch.float64, pin_memory=True)
+        ids_view = ids_pin[:n_ev]
         ectx = ara.Context(w.catalog, device=local, precision=a.precision, stream=stream, rank=rank, world=world,
                            nccl_id=nccl_id, load_mode=a.e2e_mode, chunk_trials=a.chunk_trials,
                            l2_persist=a.l2_persist)
         h2d_ms = []
 
+        wall = []
+
         def estep():
+            t0 = time.perf_counter()
             ectx.load_elts(eo_pin, ev_pin, ls_pin, terms, n_elts=w.n_elts)
-            ectx.load_yet(T, first, off_pin, ids_pin[:n_ev])
+            t1 = time.perf_counter()
+            ectx.load_yet(T, first, off_pin, ids_view)
+            t2 = time.perf_counter()
             s2 = ectx.run(w.layers, ylt_pin)
+            t3 = time.perf_counter()
             ectx.metrics(R)
+            t4 = time.perf_counter()
             h2d_ms.append(s2["h2d_ms"])
+            wall.append((t1 - t0, t2 - t1, t3 - t2, t4 - t3))
             return s2
 
         for _ in range(max(1, a.warmup)):
@@ -353,7 +361,9 @@ def main():
         e2e = {"value": T / (ems / 1e3), "unit": "trials/s", "ms_per_step": ems, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "mode": a.e2e_mode, "chunk_trials": a.chunk_trials,
                "h2d_gbs": (n_ev * 4 + n_off * 8) / (float(np.mean(h2d_ms[-a.steps:])) / 1e3) / 1e9
-               if a.e2e_mode == "chunked" and np.mean(h2d_ms) > 0 else None}
+               if a.e2e_mode == "chunked" and np.mean(h2d_ms) > 0 else None,
+               "wall_ms": {k: 1e3 * float(np.median([x[i] for x in wall[-a.steps:]]))
+                           for i, k in enumerate(("load_elts", "load_yet", "run", "metrics"))}}
         ectx.close()
 
     # ---- CPU baseline (oracle) on rank 0 at N = 1 only

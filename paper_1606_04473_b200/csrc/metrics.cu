@@ -55,6 +55,7 @@ __global__ void __launch_bounds__(256) radix_pass_kernel(const __grid_constant__
     __shared__ uint32_t s_rep[ARA_MAX_RP];
     __shared__ uint32_t s_last;
     const uint32_t row = blockIdx.y, n_rp = P.n_rp;
+    const uint32_t lane = threadIdx.x & 31u;
     const int shift = 56 - 8 * pass;
     for (uint32_t i = threadIdx.x; i < n_rp; i += blockDim.x) {
         s_prefix[i] = P.prefix[row * n_rp + i];
@@ -63,14 +64,21 @@ __global__ void __launch_bounds__(256) radix_pass_kernel(const __grid_constant__
     for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) sh[i] = 0;
     __syncthreads();
 
+    // Warp-uniform sweep; lanes holding the same digit are merged with
+    // match_any so each (return period, digit) costs one shared atomic per
+    // warp (YLT keys concentrate in a few top-byte bins).
     const double* y = P.ylt + (uint64_t)row * P.ld;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.T;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t key = key_of(y[i]);
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < P.T;
+         i0 += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = i0 + lane;
+        const bool valid = i < P.T;
+        const uint64_t key = valid ? key_of(y[i]) : 0ull;
         const uint32_t d = (uint32_t)(key >> shift) & 255u;
         for (uint32_t r = 0; r < n_rp; ++r) {
             if (s_rep[r] != r) continue;
-            if (pass == 0 || ((key ^ s_prefix[r]) >> (shift + 8)) == 0) atomicAdd(&sh[r * 256 + d], 1u);
+            const bool mt = valid && (pass == 0 || ((key ^ s_prefix[r]) >> (shift + 8)) == 0);
+            const unsigned peers = __match_any_sync(0xffffffffu, mt ? d : 256u);
+            if (mt && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&sh[r * 256 + d], (uint32_t)__popc(peers));
         }
     }
     __syncthreads();
@@ -84,23 +92,42 @@ __global__ void __launch_bounds__(256) radix_pass_kernel(const __grid_constant__
     if (!s_last) return;
     __threadfence();
 
-    // Last block of this row: choose the digit for every return period.
-    for (uint32_t r = threadIdx.x; r < n_rp; r += blockDim.x) {
-        const uint32_t* h = gh + s_rep[r] * 256;
-        uint64_t kr = P.krem[row * n_rp + r], cum = 0;
-        uint64_t pre = s_prefix[r];
-        for (int d = 255; d >= 0; --d) {
-            const uint64_t c = __ldcg(h + d);
-            if (kr <= cum + c) {
-                pre |= (uint64_t)d << shift;
-                kr -= cum;
-                break;
-            }
-            cum += c;
+    // Last block of this row: stage the row's histograms in shared memory
+    // (coalesced), then one warp per return period finds the digit with a
+    // warp-wide scan from the top digit down.
+    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) sh[i] = (s_rep[i >> 8] == (i >> 8)) ? __ldcg(gh + i) : 0u;
+    __syncthreads();
+    const uint32_t wid = threadIdx.x >> 5;
+    for (uint32_t r = wid; r < n_rp; r += blockDim.x >> 5) {
+        const uint32_t* h = sh + s_rep[r] * 256;
+        const uint64_t kr = P.krem[row * n_rp + r];
+        // lane l owns digits 255-8l .. 248-8l (descending)
+        uint32_t c[8];
+        uint64_t tot = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { c[q] = h[255 - 8 * lane - q]; tot += c[q]; }
+        uint64_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += v;
         }
-        P.prefix[row * n_rp + r] = pre;
-        P.krem[row * n_rp + r] = kr;
-        s_prefix[r] = pre;
+        const uint64_t excl = incl - tot;
+        const unsigned hit = __ballot_sync(0xffffffffu, excl < kr && kr <= incl);
+        const uint32_t src = (uint32_t)(__ffs(hit) - 1);
+        if (lane == src) {
+            uint64_t cum = excl;
+            uint32_t d = 255 - 8 * lane;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (kr <= cum + c[q]) { d = 255 - 8 * lane - q; break; }
+                cum += c[q];
+            }
+            const uint64_t pre = s_prefix[r] | ((uint64_t)d << shift);
+            P.prefix[row * n_rp + r] = pre;
+            P.krem[row * n_rp + r] = kr - cum;
+            s_prefix[r] = pre;
+        }
     }
     __syncthreads();
     for (uint32_t r = threadIdx.x; r < n_rp; r += blockDim.x) {
@@ -150,18 +177,30 @@ __global__ void __launch_bounds__(256) tail_kernel(const __grid_constant__ MPara
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    for (uint32_t r = threadIdx.x; r < n_rp; r += blockDim.x) {
+    // Combine the per-block partials in block order (deterministic): one warp
+    // per return period, partials staged through registers in fixed chunks.
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    for (uint32_t r = wid; r < n_rp; r += blockDim.x >> 5) {
         const double v = __longlong_as_double((long long)P.prefix[row * n_rp + r]);
+        const double* ps = P.part_sum + ((uint64_t)row * n_rp + r) * P.nblk;
+        const uint64_t* pc = P.part_cnt + ((uint64_t)row * n_rp + r) * P.nblk;
         double s = 0.0;
         uint64_t c = 0;
-        for (uint32_t b = 0; b < P.nblk; ++b) {
-            s = __dadd_rn(s, __ldcg(P.part_sum + ((uint64_t)row * n_rp + r) * P.nblk + b));
-            c += __ldcg(P.part_cnt + ((uint64_t)row * n_rp + r) * P.nblk + b);
+        for (uint32_t b0 = 0; b0 < P.nblk; b0 += 32) {
+            const uint32_t b = b0 + lane;
+            const double x = b < P.nblk ? __ldcg(ps + b) : 0.0;
+            const uint64_t y = b < P.nblk ? __ldcg(pc + b) : 0ull;
+            for (uint32_t q = 0; q < 32 && b0 + q < P.nblk; ++q) {   // sequential, block order
+                s = __dadd_rn(s, __shfl_sync(0xffffffffu, x, q));
+                c += __shfl_sync(0xffffffffu, y, q);
+            }
         }
-        const uint64_t k = P.k[r];
-        const double tail = __dadd_rn(s, __dmul_rn((double)(k - c), v));
-        P.out[((uint64_t)row * n_rp + r) * 2 + 0] = v;
-        P.out[((uint64_t)row * n_rp + r) * 2 + 1] = __ddiv_rn(tail, (double)k);
+        if (lane == 0) {
+            const uint64_t k = P.k[r];
+            const double tail = __dadd_rn(s, __dmul_rn((double)(k - c), v));
+            P.out[((uint64_t)row * n_rp + r) * 2 + 0] = v;
+            P.out[((uint64_t)row * n_rp + r) * 2 + 1] = __ddiv_rn(tail, (double)k);
+        }
     }
     if (threadIdx.x == 0) P.done[row] = 0;
 }

@@ -1,0 +1,52 @@
+"""Multi-GPU path on real GPUs (gpurun --gpus 2/4): the sharded, all-gathered
+YLT is bit-identical to the 1-GPU YLT (P11) and every rank derives the same
+PML/TVaR.  Skipped when fewer than 2 GPUs are visible."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import synth
+from parity_util import make_inputs, run_gpu
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _ngpu():
+    import torch
+    return torch.cuda.device_count()
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("name,n_trials", [("tiny", 1000), ("tiny", 997), ("mini", 20_000)])
+def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials):
+    n = _ngpu()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    out = str(tmp_path / "r0.npz")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(HERE, "mgpu_worker.py"),
+           name, str(n_trials), out]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    got = np.load(out)
+    assert bool(got["same"])
+    w = synth.get_config(name).with_(n_trials=n_trials)
+    off, ids, elts = make_inputs(w)
+    R = [x for x in w.return_periods if x <= w.n_trials]
+    ylt, _, _, met = run_gpu(off, ids, elts, w, w.layers, return_periods=R)
+    assert np.array_equal(got["ylt"], ylt)
+    assert np.array_equal(got["pml"], met[1]) and np.array_equal(got["k"], met[0])
+    assert np.allclose(got["tvar"], met[2], rtol=1e-12, atol=0)
