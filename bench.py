@@ -34,6 +34,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ["NCCL_DEBUG"] = os.environ.get("ARA_NCCL_DEBUG", "WARN")   # stdout: the one JSON line only
 
 import synth  # noqa: E402
 
@@ -224,11 +225,13 @@ def main():
     first, count = ara.ara_partition(T, world, rank)
     stream = torch.cuda.current_stream()
 
-    nccl_id = None
-    if world > 1:
+    def new_nccl_id():
+        """A fresh NCCL unique id per communicator (an id initialises one communicator)."""
+        if world == 1:
+            return None
         obj = [ara.ara_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
 
     def barrier():
         if world > 1:
@@ -267,7 +270,7 @@ def main():
 
     # ---- device-resident arm (value)
     ctx = ara.Context(w.catalog, device=local, precision=a.precision, stream=stream, rank=rank, world=world,
-                      nccl_id=nccl_id, l2_persist=a.l2_persist)
+                      nccl_id=new_nccl_id(), l2_persist=a.l2_persist)
     kern_ms, ag_ms, met_ms, launches = [], [], [], []
 
     def step(record):
@@ -325,7 +328,7 @@ def main():
         ylt_pin = torch.empty((L + 1) * T, dtype=torch.float64, pin_memory=True)
         ids_view = ids_pin[:n_ev]
         ectx = ara.Context(w.catalog, device=local, precision=a.precision, stream=stream, rank=rank, world=world,
-                           nccl_id=nccl_id, load_mode=a.e2e_mode, chunk_trials=a.chunk_trials,
+                           nccl_id=new_nccl_id(), load_mode=a.e2e_mode, chunk_trials=a.chunk_trials,
                            l2_persist=a.l2_persist)
         h2d_ms = []
 

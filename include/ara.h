@@ -137,14 +137,16 @@ const char* ara_last_error(const ara_ctx* ctx);
  * contiguous).
  *   elt_offsets [n_elts+1] u64, elt_offsets[0] == 0; ELT j owns records
  *   [elt_offsets[j], elt_offsets[j+1]) of event_ids (u32, in [1, catalog]) and
- *   losses (f64, finite, >= 0).  Order within an ELT is free; an event id may
- *   appear at most once per ELT.
+ *   losses (f64, finite, >= 0), event ids strictly ascending within each ELT
+ *   (an ELT is a map: no duplicates).
  *   terms [n_elts] or NULL (identity: deductible 0, limit +inf).
  * Arrays may be host or device memory; they are not referenced after return.
- * COLLECTIVE when world > 1: rank 0's arrays are authoritative and its table is
- * broadcast over NVLink (ncclBroadcast); other ranks may pass NULL arrays but
- * must pass the same n_elts.
- * Errors: INVALID_ARG (n_elts == 0, NULL arrays, bad offsets, duplicate id),
+ * COLLECTIVE when world > 1: rank 0's arrays are authoritative; rank 0
+ * validates them and broadcasts the sparse records over NVLink (ncclBroadcast),
+ * then every rank densifies its own copy of the table.  Other ranks may pass
+ * NULL arrays but must pass the same n_elts (and their own terms).
+ * Errors: INVALID_ARG (n_elts == 0 or > 65535, NULL arrays, bad offsets, ids
+ * not strictly ascending within an ELT),
  * OUT_OF_RANGE (event id outside [1, catalog]), DOMAIN (negative / non-finite
  * loss, negative deductible, non-positive limit), OOM, CUDA, NCCL. */
 ara_status ara_load_elts(ara_ctx* ctx, uint32_t n_elts, const uint64_t* elt_offsets,

@@ -277,6 +277,9 @@ extern "C" void ara_destroy(ara_ctx* ctx) {
     cudaFree(ctx->d_ylt_gather);
     cudaFree(ctx->d_ylt_global);
     cudaFree(ctx->d_lossy);
+    cudaFree(ctx->d_sp_off);
+    cudaFree(ctx->d_sp_ev);
+    cudaFree(ctx->d_sp_ls);
     cudaFree(ctx->d_err);
     cudaFree(ctx->d_small);
     cudaFreeHost(ctx->h_small);
@@ -317,77 +320,67 @@ ara_status alloc_table(ara_ctx* ctx, uint32_t n_elts) {
     return ARA_OK;
 }
 
-// Rank-0 (or single-rank) part: validate, upload, densify.  Returns status.
-ara_status build_table(ara_ctx* ctx, uint32_t n_elts, const uint64_t* elt_offsets, const uint32_t* event_ids,
-                       const double* losses) {
+// Validate the ELT offsets on the host and return them (rank 0 / single rank).
+ara_status read_elt_offsets(ara_ctx* ctx, uint32_t n_elts, const uint64_t* elt_offsets, const uint32_t* event_ids,
+                            const double* losses, std::vector<uint64_t>& hoff) {
     if (!elt_offsets) return fail(ctx, ARA_ERR_INVALID_ARG, "elt_offsets is NULL");
-    std::vector<uint64_t> hoff(n_elts + 1);
-    const Mem mo = classify(elt_offsets);
-    if (mo == Mem::Device)
+    hoff.resize(n_elts + 1);
+    if (classify(elt_offsets) == Mem::Device)
         CK(cudaMemcpy(hoff.data(), elt_offsets, (n_elts + 1) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
     else
         std::memcpy(hoff.data(), elt_offsets, (n_elts + 1) * sizeof(uint64_t));
     if (hoff[0] != 0) return fail(ctx, ARA_ERR_INVALID_ARG, "elt_offsets[0] must be 0");
     for (uint32_t j = 0; j < n_elts; ++j)
         if (hoff[j + 1] < hoff[j]) return fail(ctx, ARA_ERR_INVALID_ARG, "elt_offsets decrease at ELT %u", j);
-    const uint64_t nrec = hoff[n_elts];
-    if (nrec && (!event_ids || !losses)) return fail(ctx, ARA_ERR_INVALID_ARG, "event_ids/losses NULL");
+    if (hoff[n_elts] && (!event_ids || !losses)) return fail(ctx, ARA_ERR_INVALID_ARG, "event_ids/losses NULL");
+    return ARA_OK;
+}
 
+// Device view of the sparse ELT records: the caller's device arrays, or the
+// context's staging buffers (filled by H2D copies or an NVLink broadcast).
+struct SparseDev {
+    const uint64_t* off = nullptr;
+    const uint32_t* ev = nullptr;
+    const double* ls = nullptr;
+};
+
+ara_status stage_sparse(ara_ctx* ctx, uint32_t n_elts, uint64_t nrec, const uint64_t* hoff,
+                        const uint64_t* elt_offsets, const uint32_t* event_ids, const double* losses,
+                        bool to_staging, SparseDev* out) {
+    ara_status st;
+    if ((st = ensure(ctx, ctx->d_sp_off, ctx->sp_off_cap, (size_t)n_elts + 1)) != ARA_OK) return st;
+    if ((st = ensure(ctx, ctx->d_sp_ev, ctx->sp_ev_cap, (size_t)nrec)) != ARA_OK) return st;
+    if ((st = ensure(ctx, ctx->d_sp_ls, ctx->sp_ls_cap, (size_t)nrec)) != ARA_OK) return st;
+    *out = SparseDev{ctx->d_sp_off, ctx->d_sp_ev, ctx->d_sp_ls};
+    if (hoff) {   // this rank holds the arrays
+        if (classify(elt_offsets) == Mem::Device && !to_staging) out->off = elt_offsets;
+        else CK(cudaMemcpyAsync(ctx->d_sp_off, hoff, (n_elts + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        if (nrec) {
+            const bool dev_ev = classify(event_ids) == Mem::Device, dev_ls = classify(losses) == Mem::Device;
+            if (dev_ev && !to_staging) out->ev = event_ids;
+            else CK(cudaMemcpyAsync(ctx->d_sp_ev, event_ids, nrec * sizeof(uint32_t),
+                                    dev_ev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+            if (dev_ls && !to_staging) out->ls = losses;
+            else CK(cudaMemcpyAsync(ctx->d_sp_ls, losses, nrec * sizeof(double),
+                                    dev_ls ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+        }
+    }
+    return ARA_OK;
+}
+
+// (Re)build this rank's table from device-resident sparse records: zero-fill,
+// scatter + validate (densify kernel), read back the error bits.
+ara_status densify_local(ara_ctx* ctx, uint32_t n_elts, uint64_t nrec, const SparseDev& sp) {
     const int fp32 = ctx->precision == ARA_F32_STORAGE;
     ara_status ast = alloc_table(ctx, n_elts);
     if (ast != ARA_OK) return ast;
     CK(cudaMemsetAsync(ctx->d_table, 0, ctx->table_bytes, ctx->stream));
-
-    // sparse arrays -> device (temporary copies only for host inputs)
-    uint64_t* d_eoff = nullptr;
-    uint32_t* d_ev = nullptr;
-    double* d_ls = nullptr;
-    bool own_off = false, own_ev = false, own_ls = false;
-    auto cleanup = [&]() {
-        if (own_off) cudaFree(d_eoff);
-        if (own_ev) cudaFree(d_ev);
-        if (own_ls) cudaFree(d_ls);
-    };
-    ara_status st = ARA_OK;
-    do {
-        if (mo == Mem::Device) {
-            d_eoff = const_cast<uint64_t*>(elt_offsets);
-        } else {
-            if (cudaMalloc(&d_eoff, (n_elts + 1) * sizeof(uint64_t)) != cudaSuccess) { st = ARA_ERR_OOM; break; }
-            own_off = true;
-            if (cudaMemcpyAsync(d_eoff, hoff.data(), (n_elts + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                                ctx->stream) != cudaSuccess) { st = ARA_ERR_CUDA; break; }
-        }
-        if (nrec) {
-            if (classify(event_ids) == Mem::Device) {
-                d_ev = const_cast<uint32_t*>(event_ids);
-            } else {
-                if (cudaMalloc(&d_ev, nrec * sizeof(uint32_t)) != cudaSuccess) { st = ARA_ERR_OOM; break; }
-                own_ev = true;
-                if (cudaMemcpyAsync(d_ev, event_ids, nrec * sizeof(uint32_t), cudaMemcpyHostToDevice, ctx->stream) !=
-                    cudaSuccess) { st = ARA_ERR_CUDA; break; }
-            }
-            if (classify(losses) == Mem::Device) {
-                d_ls = const_cast<double*>(losses);
-            } else {
-                if (cudaMalloc(&d_ls, nrec * sizeof(double)) != cudaSuccess) { st = ARA_ERR_OOM; break; }
-                own_ls = true;
-                if (cudaMemcpyAsync(d_ls, losses, nrec * sizeof(double), cudaMemcpyHostToDevice, ctx->stream) !=
-                    cudaSuccess) { st = ARA_ERR_CUDA; break; }
-            }
-        }
-        if (cudaMemsetAsync(ctx->d_err, 0, sizeof(uint32_t), ctx->stream) != cudaSuccess) { st = ARA_ERR_CUDA; break; }
-        if (launch_densify(d_eoff, d_ev, d_ls, n_elts, nrec, ctx->catalog, ctx->d_table, ctx->geo, fp32,
-                           ctx->d_err, ctx->stream) != cudaSuccess) { st = ARA_ERR_CUDA; break; }
-        if (cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream) !=
-            cudaSuccess) { st = ARA_ERR_CUDA; break; }
-        if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) { st = ARA_ERR_CUDA; break; }
-    } while (0);
-    cleanup();
-    if (st != ARA_OK) {
-        cudaError_t e = cudaGetLastError();
-        return fail(ctx, st, "ELT upload/densify failed: %s", cudaGetErrorString(e));
-    }
+    CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(uint32_t), ctx->stream));
+    CK(launch_densify(sp.off, sp.ev, sp.ls, n_elts, nrec, ctx->catalog, ctx->d_table, ctx->geo, fp32, ctx->d_err,
+                      ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return device_errors(ctx, (uint32_t)(ctx->h_small[0] & 0xffffffffu));
 }
 
@@ -417,34 +410,47 @@ extern "C" ara_status ara_load_elts(ara_ctx* ctx, uint32_t n_elts, const uint64_
     CK(cudaSetDevice(ctx->device));
     if (n_elts == 0 || n_elts > 65535) return fail(ctx, ARA_ERR_INVALID_ARG, "n_elts must be in [1, 65535]");
     const bool root = ctx->rank == 0;
-    ara_status st = ARA_OK;
-    if (root) {
-        st = check_terms(ctx, n_elts, terms);
-        if (st == ARA_OK) st = build_table(ctx, n_elts, elt_offsets, event_ids, losses);
-    }
+    ara_status st = check_terms(ctx, n_elts, terms);
+    std::vector<uint64_t> hoff;
+    if (st == ARA_OK && root) st = read_elt_offsets(ctx, n_elts, elt_offsets, event_ids, losses, hoff);
+    uint64_t nrec = (st == ARA_OK && root) ? hoff[n_elts] : 0;
+    SparseDev sp;
     if (ctx->world > 1) {
-        // Agree on (status, n_elts) first so a failing root cannot strand the others.
+        // Agree on (status, n_elts, records) first so a failing root cannot
+        // strand the others; then rank 0's sparse records (a few MB) go over
+        // NVLink and every rank densifies locally — instead of N host copies
+        // of the replicated data or a broadcast of the
+        // whole table.
         ctx->h_small[0] = (uint64_t)st;
         ctx->h_small[1] = n_elts;
-        CK(cudaMemcpyAsync(ctx->d_small, ctx->h_small, 2 * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
-        NK(ncclBroadcast(ctx->d_small, ctx->d_small, 2, ncclUint64, 0, ctx->comm, ctx->stream));
-        CK(cudaMemcpyAsync(ctx->h_small, ctx->d_small, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->h_small[2] = nrec;
+        CK(cudaMemcpyAsync(ctx->d_small, ctx->h_small, 3 * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+        NK(ncclBroadcast(ctx->d_small, ctx->d_small, 3, ncclUint64, 0, ctx->comm, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_small + 8, ctx->d_small, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
-        const ara_status rst = (ara_status)ctx->h_small[0];
+        const ara_status rst = (ara_status)ctx->h_small[8];
         if (rst != ARA_OK) return root ? st : fail(ctx, rst, "rank 0 rejected the ELTs");
-        if (ctx->h_small[1] != n_elts) return fail(ctx, ARA_ERR_INVALID_ARG, "n_elts differs from rank 0");
-        if (!root) {
-            st = check_terms(ctx, n_elts, terms);
-            ara_status ast = alloc_table(ctx, n_elts);
-            if (ast != ARA_OK) return ast;
+        if (ctx->h_small[9] != n_elts) return fail(ctx, ARA_ERR_INVALID_ARG, "n_elts differs from rank 0");
+        if (st != ARA_OK) return st;   // non-root terms invalid (checked locally)
+        nrec = ctx->h_small[10];
+        ara_status s2 = stage_sparse(ctx, n_elts, nrec, root ? hoff.data() : nullptr, elt_offsets, event_ids, losses,
+                                     /*to_staging=*/true, &sp);
+        if (s2 != ARA_OK) return s2;
+        NK(ncclGroupStart());
+        NK(ncclBroadcast(ctx->d_sp_off, ctx->d_sp_off, n_elts + 1, ncclUint64, 0, ctx->comm, ctx->stream));
+        if (nrec) {
+            NK(ncclBroadcast(ctx->d_sp_ev, ctx->d_sp_ev, nrec, ncclUint32, 0, ctx->comm, ctx->stream));
+            NK(ncclBroadcast(ctx->d_sp_ls, ctx->d_sp_ls, nrec, ncclDouble, 0, ctx->comm, ctx->stream));
         }
-        // The table goes over NVLink once instead of N host copies.
-        NK(ncclBroadcast(ctx->d_table, ctx->d_table, ctx->table_bytes, ncclUint8, 0, ctx->comm, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
+        NK(ncclGroupEnd());
+    } else {
         if (st != ARA_OK) return st;
-    } else if (st != ARA_OK) {
-        return st;
+        ara_status s2 = stage_sparse(ctx, n_elts, nrec, hoff.data(), elt_offsets, event_ids, losses,
+                                     /*to_staging=*/false, &sp);
+        if (s2 != ARA_OK) return s2;
     }
+    st = densify_local(ctx, n_elts, nrec, sp);   // every rank sees the same records: same verdict
+    if (st != ARA_OK) return st;
     ctx->n_elts = n_elts;
     ctx->terms.assign(n_elts, ara_elt_terms{0.0, INFINITY});
     if (terms)

@@ -141,6 +141,10 @@ struct ara_ctx {
     size_t table_bytes = 0;
     ara::TableGeo geo;
     uint32_t n_elts = 0;
+    uint64_t* d_sp_off = nullptr;      // sparse ELT staging (host uploads / NVLink broadcast)
+    uint32_t* d_sp_ev = nullptr;
+    double* d_sp_ls = nullptr;
+    size_t sp_off_cap = 0, sp_ev_cap = 0, sp_ls_cap = 0;
     std::vector<ara_elt_terms> terms;
 
     // YET (local shard)

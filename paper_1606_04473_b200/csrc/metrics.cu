@@ -64,9 +64,21 @@ __global__ void __launch_bounds__(256) radix_pass_kernel(const __grid_constant__
     for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) sh[i] = 0;
     __syncthreads();
 
-    // Warp-uniform sweep; lanes holding the same digit are merged with
-    // match_any so each (return period, digit) costs one shared atomic per
-    // warp (YLT keys concentrate in a few top-byte bins).
+    // Warp-uniform sweep.  Distinct current prefixes ("reps") are disjoint, so
+    // a key belongs to at most one rep; lanes with the same (rep, digit) are
+    // merged with match_any so each pair costs one shared atomic per warp
+    // (YLT keys concentrate in a few top-byte bins).
+    __shared__ uint32_t s_ulist[ARA_MAX_RP];
+    __shared__ uint64_t s_upre[ARA_MAX_RP];
+    __shared__ uint32_t s_nu;
+    if (threadIdx.x == 0) {
+        uint32_t nu = 0;
+        for (uint32_t r = 0; r < n_rp; ++r)
+            if (s_rep[r] == r) { s_ulist[nu] = r; s_upre[nu] = s_prefix[r]; ++nu; }
+        s_nu = nu;
+    }
+    __syncthreads();
+    const uint32_t nu = s_nu;
     const double* y = P.ylt + (uint64_t)row * P.ld;
     for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < P.T;
          i0 += (uint64_t)gridDim.x * blockDim.x) {
@@ -74,12 +86,17 @@ __global__ void __launch_bounds__(256) radix_pass_kernel(const __grid_constant__
         const bool valid = i < P.T;
         const uint64_t key = valid ? key_of(y[i]) : 0ull;
         const uint32_t d = (uint32_t)(key >> shift) & 255u;
-        for (uint32_t r = 0; r < n_rp; ++r) {
-            if (s_rep[r] != r) continue;
-            const bool mt = valid && (pass == 0 || ((key ^ s_prefix[r]) >> (shift + 8)) == 0);
-            const unsigned peers = __match_any_sync(0xffffffffu, mt ? d : 256u);
-            if (mt && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&sh[r * 256 + d], (uint32_t)__popc(peers));
+        uint32_t which = 0xffffffffu;
+        if (valid) {
+            if (pass == 0) which = 0;
+            else
+                for (uint32_t u = 0; u < nu; ++u)
+                    if (((key ^ s_upre[u]) >> (shift + 8)) == 0) which = u;
         }
+        const uint32_t tag = which == 0xffffffffu ? 0xffffffffu : (which << 8) | d;
+        const unsigned peers = __match_any_sync(0xffffffffu, tag);
+        if (tag != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
+            atomicAdd(&sh[s_ulist[which] * 256 + d], (uint32_t)__popc(peers));
     }
     __syncthreads();
     uint32_t* gh = P.hist + (uint64_t)row * n_rp * 256;

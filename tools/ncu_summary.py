@@ -11,10 +11,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "l1tex__m_xbar2l1tex_read_bytes.sum", "lts__t_sectors_srcunit_tex_op_read.sum"]
 
 
-def load(path):
+def load(path, idx=0):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units, vals = rows[0], rows[1], rows[2 + idx]
     name = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
     d = {"kernel": name}
     for h, u, v in zip(hdr, units, vals):
@@ -29,7 +29,20 @@ def load(path):
     return d
 
 
+def count(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    return len(list(csv.reader(io.StringIO(out)))) - 2
+
+
 if __name__ == "__main__":
+    if "--all" in sys.argv:
+        for i in range(count(sys.argv[1])):
+            d = load(sys.argv[1], i)
+            print(f"[{i}] {d['kernel'][:80]}  time={d.get('gpu__time_duration.sum', ('?',))[0]} "
+                  f"{d.get('gpu__time_duration.sum', ('', ''))[1]}  inst={d.get('smsp__inst_executed.sum', ('?',))[0]}  "
+                  f"issue%={d.get('smsp__issue_active.avg.pct_of_peak_sustained_active', ('?',))[0]}  "
+                  f"stalls={ {k.split('stalled_')[1].split('_per')[0]: round(v[0], 2) for k, v in d.items() if 'stalled' in k and v[0] > 0.5} }")
+        sys.exit(0)
     d = load(sys.argv[1])
     if "--json" in sys.argv:
         print(json.dumps({k: (v[0] if isinstance(v, tuple) else v) for k, v in d.items()}, indent=1))
