@@ -224,6 +224,7 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
     if (const char* v = getenv("ARA_GRID_MULT")) ctx->grid_mult = atof(v);
     if (const char* v = getenv("ARA_KERNEL")) ctx->kernel_variant = atoi(v);
     if (const char* v = getenv("ARA_PFN")) ctx->pf_sectors = atoi(v);
+    if (const char* v = getenv("ARA_BATCH")) ctx->batch = (uint32_t)atoi(v) ? (uint32_t)atoi(v) : 4u;
     auto bail = [&](ara_status st) {
         ara_destroy(ctx);
         return st;
@@ -240,6 +241,11 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
         ctx->own_stream = true;
     }
     if (cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return bail(ARA_ERR_CUDA);
+    if (cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking) != cudaSuccess) return bail(ARA_ERR_CUDA);
+    if (cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return bail(ARA_ERR_CUDA);
+    if (cudaMalloc(&ctx->d_work, sizeof(unsigned long long)) != cudaSuccess) return bail(ARA_ERR_OOM);
     for (auto& e : ctx->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return bail(ARA_ERR_CUDA);
     if (cudaMalloc(&ctx->d_err, 64) != cudaSuccess) return bail(ARA_ERR_OOM);
@@ -287,6 +293,10 @@ extern "C" void ara_destroy(ara_ctx* ctx) {
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    cudaFree(ctx->d_work);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     cudaGetLastError();
     delete ctx;
@@ -757,14 +767,36 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
                 const uint32_t box_sec = g.nsec <= 1 ? 1 : (g.nsec <= 2 ? 2 : 4);
                 const bool tma_ok = g.nsec <= 4 && (g.q0 % spb) + g.nsec <= spb && encode_tiled() != nullptr;
                 if (variant < 0) variant = g.nl == 1 ? 5 : 0;
-                if (variant == 8 && !tma_ok) variant = g.nl == 1 ? 5 : 0;
-                if (variant == 8) {
+                if ((variant == 8 || variant == 9) && !tma_ok) variant = g.nl == 1 ? 5 : 0;
+                if (variant == 8 || variant == 9) {
                     if (!make_block_map(ctx, g.q0 / spb, box_sec, &p.tmap))
                         return fail(ctx, ARA_ERR_CUDA, "cuTensorMapEncodeTiled failed");
                     p.tma_col = (g.q0 % spb) * eps;
                 }
-                const int grid = (int)(trial_kernel_grid(fp32, g.nsec, (int)g.nl, variant) * ctx->grid_mult);
-                CK(launch_trials(p, fp32, g.nsec, grid > 0 ? grid : 1, variant, s));
+                if (variant == 9) {
+                    // Hybrid: the register-pipelined LDG kernel (2 CTAs/SM) and the TMA
+                    // gather4 kernel (1 CTA/SM, shared-memory ring) run side by side on two
+                    // streams, co-resident on every SM (registers + shared memory both hold
+                    // rows in flight), claiming trial batches from one counter.
+                    p.work_ctr = ctx->d_work;
+                    p.batch = ctx->batch;
+                    CK(cudaMemsetAsync(ctx->d_work, 0, sizeof(unsigned long long), s));
+                    CK(cudaEventRecord(ctx->ev_fork, s));
+                    CK(cudaStreamWaitEvent(ctx->aux_stream, ctx->ev_fork, 0));
+                    // TMA kernel first (1 CTA/SM, ~213 KB smem); the LDG kernel asks for the
+                    // max-shared carveout so its CTAs do not force the SM into an L1-heavy
+                    // split that would keep the TMA CTA out.
+                    CK(launch_trials(p, fp32, g.nsec, ctx->n_sm, 8, ctx->aux_stream));
+                    set_ldg_carveout(fp32, g.nsec, (int)g.nl, 100);
+                    CK(launch_trials(p, fp32, g.nsec, 2 * ctx->n_sm, 5, s));
+                    set_ldg_carveout(fp32, g.nsec, (int)g.nl, -1);
+                    CK(cudaEventRecord(ctx->ev_join, ctx->aux_stream));
+                    CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
+                    p.work_ctr = nullptr;
+                } else {
+                    const int grid = (int)(trial_kernel_grid(fp32, g.nsec, (int)g.nl, variant) * ctx->grid_mult);
+                    CK(launch_trials(p, fp32, g.nsec, grid > 0 ? grid : 1, variant, s));
+                }
             }
             ++launches;
         }

@@ -87,6 +87,8 @@ struct TrialParams {
     uint32_t* lossy;            // [.. rows][ld] or null
     uint32_t* err;              // device error word
     int pf_sectors;             // sectors per prefetched window (prefetching kernels)
+    unsigned long long* work_ctr;   // dynamic trial batches (hybrid launches), or null = static stride
+    uint32_t batch;             // trials per dynamic claim
     LayerWin lw[kMaxLB];
     double2 term[kMaxLB][kMaxWin];   // (deductible, limit) per window column
 };
@@ -98,6 +100,7 @@ cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const d
 
 cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int grid, int variant, cudaStream_t s);
 int trial_kernel_grid(int fp32, uint32_t max_nsec, int n_layers, int variant);
+void set_ldg_carveout(int fp32, uint32_t nsec, int nl, int pct);
 cudaError_t launch_trials_wide(const TrialParams& p, int fp32, const double2* d_cterm, uint32_t col0,
                                uint32_t ncol, int grid, cudaStream_t s);
 
@@ -128,7 +131,10 @@ struct ara_ctx {
     ara_load_mode load_mode = ARA_LOAD_ALL_AT_ONCE;
     uint64_t chunk_trials = 65536;
     int l2_persist = 0;
-    cudaStream_t stream = nullptr, copy_stream = nullptr;
+    cudaStream_t stream = nullptr, copy_stream = nullptr, aux_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    unsigned long long* d_work = nullptr;   // dynamic trial counter (hybrid launches)
+    uint32_t batch = 4;                     // ARA_BATCH
     bool own_stream = false;
     ncclComm_t comm = nullptr;
     int n_sm = 148;

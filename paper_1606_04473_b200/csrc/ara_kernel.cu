@@ -142,6 +142,39 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr) {
 // D = id-queue depth: rows of step i+1 are demand-loaded into registers while
 // step i is computed; for D > 1 the rows of step i+D are also prefetched into
 // L2 (no registers held), so the demand loads mostly hit L2.
+// Warp-level trial scheduler.  Static: trials gw, gw+nw, ... (work_ctr ==
+// null).  Dynamic: batches of p.batch consecutive trials claimed from a
+// global counter shared by every warp of every kernel of the launch group —
+// this is what lets the LDG and TMA kernels run side by side (hybrid) and
+// balance themselves.  Per-trial arithmetic does not depend on which warp
+// takes a trial, so the YLT bits do not either.
+struct TrialSched {
+    uint64_t cur, end, stride;
+    bool dyn;
+    __device__ __forceinline__ void init(const TrialParams& p, uint64_t gw, uint64_t nw) {
+        dyn = p.work_ctr != nullptr;
+        if (dyn) { cur = end = 0; stride = 0; }
+        else { cur = p.t_begin + gw; end = ~0ull; stride = nw; }
+    }
+    // next trial index for this warp, or ~0 when the range is exhausted
+    __device__ __forceinline__ uint64_t next(const TrialParams& p) {
+        if (!dyn) {
+            const uint64_t t = cur;
+            cur += stride;
+            return t < p.t_end ? t : ~0ull;
+        }
+        if (cur >= end) {
+            unsigned long long b = 0;
+            if ((threadIdx.x & 31u) == 0) b = atomicAdd(p.work_ctr, (unsigned long long)p.batch);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            cur = p.t_begin + b;
+            end = cur + p.batch < p.t_end ? cur + p.batch : p.t_end;
+            if (cur >= p.t_end) { end = cur; return ~0ull; }
+        }
+        return cur++;
+    }
+};
+
 template <typename TV, int NSEC, int NLB, int D, int MINB = 2>
 __global__ void __launch_bounds__(kThreads, MINB) trial_kernel(const __grid_constant__ TrialParams p) {
     constexpr int QB = Batch<TV, NSEC>::QB;
@@ -162,12 +195,14 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel(const __grid_cons
         __syncthreads();
     }
 
-    uint64_t t = p.t_begin + gw;
+    TrialSched sched;
+    sched.init(p, gw, nw);
+    uint64_t t = sched.next(p), tn = sched.next(p);
     uint64_t a_nxt = 0, b_nxt = 0;
-    if (t < p.t_end) { a_nxt = __ldg(p.off + t); b_nxt = __ldg(p.off + t + 1); }
-    for (; t < p.t_end; t += nw) {
+    if (t != ~0ull) { a_nxt = __ldg(p.off + t); b_nxt = __ldg(p.off + t + 1); }
+    for (; t != ~0ull; t = tn, tn = sched.next(p)) {
         uint64_t a = a_nxt, b = b_nxt;
-        if (t + nw < p.t_end) { a_nxt = __ldg(p.off + t + nw); b_nxt = __ldg(p.off + t + nw + 1); }
+        if (tn != ~0ull) { a_nxt = __ldg(p.off + tn); b_nxt = __ldg(p.off + tn + 1); }
         if (b < a) { err |= ERRBIT_OFFSETS; b = a; }
         const uint64_t n = b - a;
         const uint32_t* ids = p.ids + (a - base);
@@ -550,12 +585,14 @@ __global__ void __launch_bounds__(kThreads, 1) trial_kernel_tma(const __grid_con
     // ---- id stage: a step iterator QD steps ahead of the gathers.  Each lane
     // copies its event id of the step straight into the id ring (cp.async,
     // zero-filled past the trial's end); lane 0 records the step metadata.
-    uint64_t it_t = p.t_begin + (uint64_t)blockIdx.x * Geo::WARPS + wib;
+    TrialSched sched;
+    sched.init(p, (uint64_t)blockIdx.x * Geo::WARPS + wib, nw);
+    uint64_t it_t = sched.next(p), it_tn = sched.next(p);
     uint64_t it_a = 0, nx_a = 0, nx_b = 0;
     uint32_t it_n = 0, it_k0 = 0;
-    bool it_valid = it_t < p.t_end;
+    bool it_valid = it_t != ~0ull;
     auto fetch_next_offsets = [&](uint64_t tn) {
-        if (tn < p.t_end) { nx_a = __ldg(p.off + tn); nx_b = __ldg(p.off + tn + 1); }
+        if (tn != ~0ull) { nx_a = __ldg(p.off + tn); nx_b = __ldg(p.off + tn + 1); }
     };
     auto enter_trial = [&](uint64_t a, uint64_t b) {
         if (b < a) { err |= ERRBIT_OFFSETS; b = a; }
@@ -565,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1) trial_kernel_tma(const __grid_con
     };
     if (it_valid) {
         enter_trial(__ldg(p.off + it_t), __ldg(p.off + it_t + 1));
-        fetch_next_offsets(it_t + nw);
+        fetch_next_offsets(it_tn);
     }
     auto id_stage = [&](uint32_t step) {
         StepMeta md{~0ull, 0u, 0u};
@@ -578,11 +615,12 @@ __global__ void __launch_bounds__(kThreads, 1) trial_kernel_tma(const __grid_con
                          : "memory");
             it_k0 += 32u;
             if (it_k0 >= it_n) {
-                it_t += nw;
-                it_valid = it_t < p.t_end;
+                it_t = it_tn;
+                it_valid = it_t != ~0ull;
                 if (it_valid) {
                     enter_trial(nx_a, nx_b);
-                    fetch_next_offsets(it_t + nw);
+                    it_tn = sched.next(p);
+                    fetch_next_offsets(it_tn);
                 }
             }
         }
@@ -819,6 +857,12 @@ int trial_kernel_grid(int fp32, uint32_t max_nsec, int n_layers, int variant) {
     }
     c = nsm * per_sm;
     return c;
+}
+
+void set_ldg_carveout(int fp32, uint32_t nsec, int nl, int pct) {
+    int smem = 0;
+    cudaFuncSetAttribute(pick_kernel(fp32, nsec, nl, 5, &smem), cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaGetLastError();
 }
 
 cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int grid, int variant, cudaStream_t s) {

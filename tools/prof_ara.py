@@ -11,12 +11,15 @@ ap.add_argument("--precision", default="f64")
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--l2-persist", action="store_true")
 ap.add_argument("--rho", type=float, default=None)
+ap.add_argument("--catalog", type=int, default=None)
 a = ap.parse_args()
 import torch
 from paper_1606_04473_b200 import ara
 w = synth.get_config(a.config)
 if a.rho is not None:
     w = w.with_(rho=a.rho)
+if a.catalog is not None:
+    w = w.with_(catalog=a.catalog)
 off, ids = synth.gen_yet(w)
 eo, ev, ls = synth.gen_elts(w)
 d_off = torch.from_numpy(off.view(np.int64)).cuda()
@@ -32,6 +35,6 @@ for s in range(a.steps):
     res.append((st["kernel_ms"], mms))
 torch.cuda.synchronize()
 ctx.close()
-print(json.dumps({"config": w.name, "precision": a.precision, "env": {k: v for k, v in os.environ.items() if k.startswith("ARA_")},
+print(json.dumps({"config": w.name, "catalog": w.catalog, "precision": a.precision, "env": {k: v for k, v in os.environ.items() if k.startswith("ARA_")},
                   "l2_persist": a.l2_persist, "kernel_ms": [r[0] for r in res], "metrics_ms": [r[1] for r in res],
                   "events": len(ids), "pml0": pml[0].tolist()}))
