@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--l2-persist", action="store_true")
+    ap.add_argument("--mode", default="direct", choices=["direct", "fold"],
+                    help="direct = Alg. 3 per occurrence (headline); fold = catalogue-fold mode (SURVEY 8f F2)")
     return ap.parse_args()
 
 
@@ -128,14 +130,24 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str) -> int:
-    """per event 4 B of id + the 32-B sectors of every
-    layer window; per trial 8 B of offsets + 8 B per YLT row written."""
+def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str = "direct") -> int:
+    """direct mode — per event 4 B of id + the 32-B
+    sectors of every layer window; per trial 8 B of offsets + 8 B per YLT row.
+    Fold mode — the fold pass reads every catalogue row window once and writes
+    8 B per (event id, layer); the trial pass reads 4 B of id + one fold row
+    (8 B x layers, padded to a power of two) per event."""
     eps = 4 if precision == "f64" else 8
     sec = 0
     for L in w.layers:
         sec += (L.elt_end + eps - 1) // eps - L.elt_begin // eps
-    return n_events * (4 + 32 * sec) + n_trials * (8 + 8 * (len(w.layers) + 1))
+    per_trial = n_trials * (8 + 8 * (len(w.layers) + 1))
+    if mode == "fold":
+        nl = len(w.layers)
+        nlc = 1
+        while nlc < nl and nlc < 8:
+            nlc *= 2
+        return (w.catalog + 1) * (32 * sec + 8 * nl) + n_events * (4 + 8 * nlc) * ((nl + nlc - 1) // nlc) + per_trial
+    return n_events * (4 + 32 * sec) + per_trial
 
 
 def load_peaks():
@@ -270,7 +282,7 @@ def main():
 
     # ---- device-resident arm (value)
     ctx = ara.Context(w.catalog, device=local, precision=a.precision, stream=stream, rank=rank, world=world,
-                      nccl_id=new_nccl_id(), l2_persist=a.l2_persist)
+                      nccl_id=new_nccl_id(), l2_persist=a.l2_persist, run_mode=a.mode)
     kern_ms, ag_ms, met_ms, launches = [], [], [], []
 
     def step(record):
@@ -312,7 +324,7 @@ def main():
 
     # roofline of the dominant kernel (the ARA trial kernel) on this rank
     k_ms = float(np.mean(kern_ms))
-    alg = algorithmic_bytes(w, ev_local, count, a.precision)
+    alg = algorithmic_bytes(w, ev_local, count, a.precision, a.mode)
     peaks = load_peaks()
     peak = peaks.get("hbm_gbs")
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
@@ -329,7 +341,7 @@ def main():
         ids_view = ids_pin[:n_ev]
         ectx = ara.Context(w.catalog, device=local, precision=a.precision, stream=stream, rank=rank, world=world,
                            nccl_id=new_nccl_id(), load_mode=a.e2e_mode, chunk_trials=a.chunk_trials,
-                           l2_persist=a.l2_persist)
+                           l2_persist=a.l2_persist, run_mode=a.mode)
         h2d_ms = []
 
         wall = []
@@ -387,10 +399,11 @@ def main():
                        "n_events": n_events_global, "elts_per_layer": [Lr.elt_end - Lr.elt_begin for Lr in w.layers],
                        "catalog": w.catalog, "layers": L, "return_periods": len(R), "parallelism": f"trials/{world}",
                        "l2": "inputs larger than L2 (4 GB YET streamed once per step; 256 MB table)",
-                       "l2_persist": a.l2_persist},
+                       "l2_persist": a.l2_persist, "mode": a.mode},
             "lookups_per_sec": lookups / (ms / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "ara::trial_kernel",
+                         "frac": achieved / peak, "traffic": traffic if a.mode == "direct" else None,
+                         "kernel": "ara::trial_kernel" if a.mode == "direct" else "ara::fold_kernel+trial_fold_kernel",
                          "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
             "breakdown_ms": {"ara_kernel": k_ms, "allgather": float(np.mean(ag_ms)), "metrics": float(np.mean(met_ms)),
                              "step": ms},

@@ -71,6 +71,12 @@ typedef enum {
                                   (paper's "sequential" transfer mode analogue) */
 } ara_load_mode;
 
+typedef enum {
+    ARA_RUN_DIRECT = 0,   /* per occurrence: gather the layer's row window and apply every term (Alg. 3 as written) */
+    ARA_RUN_FOLD = 1      /* per run: fold the catalogue once (o(e) for every event id, P:373 per-occurrence
+                             independence), then gather one value per occurrence; bit-identical YLT */
+} ara_run_mode;
+
 typedef struct {
     int device;               /* CUDA device ordinal */
     ara_precision precision;
@@ -81,6 +87,7 @@ typedef struct {
     ara_load_mode load_mode;
     uint64_t chunk_trials;    /* CHUNKED: trials per H2D chunk; 0 = 65536 */
     int l2_persist;           /* nonzero: put the ELT table under an L2 persisting access-policy window */
+    ara_run_mode run_mode;    /* ARA_RUN_DIRECT (default) or ARA_RUN_FOLD */
 } ara_config;
 
 /* Per-ELT financial terms I_j (Eq. 2; applied per lookup):

@@ -28,6 +28,7 @@ ARA_OK, ARA_ERR_INVALID_ARG, ARA_ERR_OUT_OF_RANGE, ARA_ERR_DOMAIN = 0, 1, 2, 3
 ARA_ERR_STATE, ARA_ERR_OOM, ARA_ERR_CUDA, ARA_ERR_NCCL = 4, 5, 6, 7
 ARA_F64, ARA_F32_STORAGE = 0, 1
 ARA_LOAD_ALL_AT_ONCE, ARA_LOAD_CHUNKED = 0, 1
+ARA_RUN_DIRECT, ARA_RUN_FOLD = 0, 1
 ARA_NCCL_ID_BYTES = 128
 ARA_MAX_LAYERS = 64
 ARA_MAX_RP = 64
@@ -37,7 +38,7 @@ class ara_config(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("precision", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("rank", ctypes.c_int), ("world", ctypes.c_int), ("nccl_unique_id", ctypes.c_void_p),
                 ("load_mode", ctypes.c_int), ("chunk_trials", ctypes.c_uint64),
-                ("l2_persist", ctypes.c_int)]
+                ("l2_persist", ctypes.c_int), ("run_mode", ctypes.c_int)]
 
 
 class ara_elt_terms(ctypes.Structure):
@@ -143,11 +144,11 @@ def ara_nccl_unique_id() -> bytes:
 
 def ara_create(catalog_size: int, device: int = 0, precision: int = ARA_F64, stream=None, rank: int = 0,
                world: int = 1, nccl_id: Optional[bytes] = None, load_mode: int = ARA_LOAD_ALL_AT_ONCE,
-               chunk_trials: int = 0, l2_persist: bool = False):
+               chunk_trials: int = 0, l2_persist: bool = False, run_mode: int = ARA_RUN_DIRECT):
     idbuf = ctypes.create_string_buffer(nccl_id, ARA_NCCL_ID_BYTES) if nccl_id else None
     cfg = ara_config(device, precision, _stream_ptr(stream), rank, world,
                      ctypes.cast(idbuf, _vp) if idbuf is not None else None, load_mode, chunk_trials,
-                     1 if l2_persist else 0)
+                     1 if l2_persist else 0, run_mode)
     h = _vp()
     st = _lib.ara_create(catalog_size, ctypes.byref(cfg), ctypes.byref(h))
     _check(st, what="ara_create (no CUDA device, bad config, or NCCL init failure)")
@@ -227,11 +228,12 @@ class Context:
 
     def __init__(self, catalog_size: int, device: int = 0, precision: str = "f64", stream=None,
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, load_mode: str = "all",
-                 chunk_trials: int = 0, l2_persist: bool = False):
+                 chunk_trials: int = 0, l2_persist: bool = False, run_mode: str = "direct"):
         prec = {"f64": ARA_F64, "f32": ARA_F32_STORAGE}[precision]
         mode = {"all": ARA_LOAD_ALL_AT_ONCE, "chunked": ARA_LOAD_CHUNKED}[load_mode]
+        rmode = {"direct": ARA_RUN_DIRECT, "fold": ARA_RUN_FOLD}[run_mode]
         self.h = ara_create(catalog_size, device, prec, stream, rank, world, nccl_id, mode, chunk_trials,
-                            l2_persist)
+                            l2_persist, rmode)
         self.n_layers = 0
         self.n_trials = 0
 

@@ -211,6 +211,7 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
     if (cfg->world > 1 && !cfg->nccl_unique_id) return ARA_ERR_INVALID_ARG;
     if (cfg->precision != ARA_F64 && cfg->precision != ARA_F32_STORAGE) return ARA_ERR_INVALID_ARG;
     if (cfg->load_mode != ARA_LOAD_ALL_AT_ONCE && cfg->load_mode != ARA_LOAD_CHUNKED) return ARA_ERR_INVALID_ARG;
+    if (cfg->run_mode != ARA_RUN_DIRECT && cfg->run_mode != ARA_RUN_FOLD) return ARA_ERR_INVALID_ARG;
     ara_ctx* ctx = new (std::nothrow) ara_ctx();
     if (!ctx) return ARA_ERR_OOM;
     ctx->device = cfg->device;
@@ -220,6 +221,7 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
     ctx->load_mode = cfg->load_mode;
     ctx->chunk_trials = cfg->chunk_trials ? cfg->chunk_trials : 65536;
     ctx->l2_persist = cfg->l2_persist;
+    ctx->run_mode = cfg->run_mode;
     ctx->catalog = catalog_size;
     if (const char* v = getenv("ARA_GRID_MULT")) ctx->grid_mult = atof(v);
     if (const char* v = getenv("ARA_KERNEL")) ctx->kernel_variant = atoi(v);
@@ -283,6 +285,7 @@ extern "C" void ara_destroy(ara_ctx* ctx) {
     cudaFree(ctx->d_ylt_gather);
     cudaFree(ctx->d_ylt_global);
     cudaFree(ctx->d_lossy);
+    cudaFree(ctx->d_fold);
     cudaFree(ctx->d_sp_off);
     cudaFree(ctx->d_sp_ev);
     cudaFree(ctx->d_sp_ls);
@@ -629,11 +632,18 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
     // Layer groups: consecutive layers on the same sector window share one
     // launch (one row load serves up to kMaxLB tower layers); a layer wider
     // than kMaxSec sectors runs alone in the generic kernel.
+    // Fold mode: layers are folded in chunks of nlc (power of two <= 8) per
+    // folded trial launch; groups never straddle a chunk.
+    bool fold = ctx->run_mode == ARA_RUN_FOLD;
+    for (uint32_t l = 0; l < n_layers && fold; ++l)
+        if ((layers[l].elt_end + eps - 1) / eps - layers[l].elt_begin / eps > (uint32_t)kMaxSec) fold = false;
+    uint32_t nlc = 1;
+    while (nlc < n_layers && nlc < (uint32_t)kMaxFoldL) nlc <<= 1;
     std::vector<Group> groups;
     for (uint32_t l = 0; l < n_layers; ++l) {
         const uint32_t q0 = layers[l].elt_begin / eps, q1 = (layers[l].elt_end + eps - 1) / eps;
         const bool wide = q1 - q0 > (uint32_t)kMaxSec;
-        if (!wide && !groups.empty()) {
+        if (!wide && !groups.empty() && !(fold && l % nlc == 0)) {
             Group& g = groups.back();
             if (!g.wide && g.q0 == q0 && g.nsec == q1 - q0 && g.nl < (uint32_t)kMaxLB) {
                 ++g.nl;
@@ -716,9 +726,66 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
     uint32_t launches = 0;
     double2* d_cterm = nullptr;
     std::vector<double2> wide_terms;
+    // per-group window setup shared by the direct and fold launches
+    auto setup_window = [&](const Group& g, TrialParams& p) {
+        for (uint32_t q = 0; q < g.nl; ++q) {
+            const ara_layer& L = layers[g.l0 + q];
+            p.lw[q] = {L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit};
+        }
+        for (uint32_t sct = 0; sct < (uint32_t)kMaxSec; ++sct) {
+            const uint32_t qq = g.q0 + (sct < g.nsec ? sct : 0);
+            p.sec_off[sct] = (uint64_t)(qq / spb) * geo.block_elems + (uint64_t)(qq % spb) * eps;
+        }
+        for (uint32_t q = 0; q < g.nl; ++q) {
+            const ara_layer& L = layers[g.l0 + q];
+            for (uint32_t w = 0; w < (uint32_t)kMaxWin; ++w) {
+                const uint32_t col = g.q0 * eps + w;
+                if (w / eps < g.nsec && col >= L.elt_begin && col < L.elt_end)
+                    p.term[q][w] = make_double2(ctx->terms[col].deductible, ctx->terms[col].limit);
+                else
+                    p.term[q][w] = make_double2(INFINITY, INFINITY);   // contributes exactly +0
+            }
+        }
+    };
+    const uint32_t n_chunks_fold = (n_layers + nlc - 1) / nlc;
+    const uint64_t fold_rows = (uint64_t)ctx->catalog + 1;
     CK(cudaEventRecord(ctx->ev[1], s));
+    if (fold) {
+        // a0': fold the catalogue once per run (all layers), bit-identical per-event values
+        st = ensure(ctx, ctx->d_fold, ctx->fold_cap, (size_t)n_chunks_fold * fold_rows * nlc);
+        if (st != ARA_OK) return st;
+        for (const Group& g : groups) {
+            TrialParams p = base;
+            p.n_layers = g.nl;
+            setup_window(g, p);
+            p.fold = ctx->d_fold + (uint64_t)(g.l0 / nlc) * fold_rows * nlc;
+            p.fold_stride = nlc;
+            p.fold_col0 = g.l0 % nlc;
+            CK(launch_fold(p, fp32, g.nsec, s));
+            ++launches;
+        }
+    }
     for (size_t c = 0; c < chunks.size(); ++c) {
         if (stream_in) CK(cudaStreamWaitEvent(s, chunk_ev[c], 0));
+        if (fold) {
+            for (uint32_t fc = 0; fc < n_chunks_fold; ++fc) {
+                TrialParams p = base;
+                p.t_begin = chunks[c].first;
+                p.t_end = chunks[c].second;
+                p.n_layers = (n_layers - fc * nlc) < nlc ? (n_layers - fc * nlc) : nlc;
+                p.ylt_row0 = fc * nlc;
+                p.portfolio_mode = fc == 0 ? 0 : 1;
+                for (uint32_t q = 0; q < p.n_layers; ++q) {
+                    const ara_layer& L = layers[fc * nlc + q];
+                    p.lw[q] = {L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit};
+                }
+                p.fold = ctx->d_fold + (uint64_t)fc * fold_rows * nlc;
+                p.fold_stride = nlc;
+                CK(launch_trials_folded(p, (int)(100 * ctx->grid_mult), s));
+                ++launches;
+            }
+            continue;
+        }
         for (size_t gi = 0; gi < groups.size(); ++gi) {
             const Group& g = groups[gi];
             TrialParams p = base;

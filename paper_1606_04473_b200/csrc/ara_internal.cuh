@@ -27,6 +27,7 @@ constexpr int kSectorBytes = 32;     // one L2 sector; windows are sector-granul
 constexpr int kBlockBytes = 128;     // column-block width of the direct-access table
 constexpr int kMaxSec = 8;           // widest per-layer window handled by the fast kernel (256 B)
 constexpr int kMaxLB = 4;            // layers sharing one window per launch
+constexpr int kMaxFoldL = 8;         // layers per folded trial launch (fold mode)
 constexpr int kMaxWin = kMaxSec * kSectorBytes / 4;   // 64 columns (fp32) per window
 constexpr int kThreads = 256;        // 8 warps per CTA
 constexpr int kTablePadBytes = kMaxSec * kSectorBytes;  // over-read slack after the last row
@@ -89,7 +90,10 @@ struct TrialParams {
     int pf_sectors;             // sectors per prefetched window (prefetching kernels)
     unsigned long long* work_ctr;   // dynamic trial batches (hybrid launches), or null = static stride
     uint32_t batch;             // trials per dynamic claim
-    LayerWin lw[kMaxLB];
+    double* fold;               // fold mode: per-event occurrence-net losses, [C+1][fold_stride] per chunk
+    uint32_t fold_stride;       // doubles per fold row (layers of one chunk, power of two <= 8)
+    uint32_t fold_col0;         // fold column of the launch's first layer
+    LayerWin lw[kMaxFoldL];
     double2 term[kMaxLB][kMaxWin];   // (deductible, limit) per window column
 };
 
@@ -101,6 +105,8 @@ cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const d
 cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int grid, int variant, cudaStream_t s);
 int trial_kernel_grid(int fp32, uint32_t max_nsec, int n_layers, int variant);
 void set_ldg_carveout(int fp32, uint32_t nsec, int nl, int pct);
+cudaError_t launch_fold(const TrialParams& p, int fp32, uint32_t nsec, cudaStream_t s);
+cudaError_t launch_trials_folded(const TrialParams& p, int grid_mult_x100, cudaStream_t s);
 cudaError_t launch_trials_wide(const TrialParams& p, int fp32, const double2* d_cterm, uint32_t col0,
                                uint32_t ncol, int grid, cudaStream_t s);
 
@@ -184,6 +190,9 @@ struct ara_ctx {
     uint64_t* d_small = nullptr;
 
     ara::MetricsScratch ms;
+    int run_mode = 0;                  // ARA_RUN_DIRECT / ARA_RUN_FOLD
+    double* d_fold = nullptr;          // fold mode: per-event occurrence-net losses
+    size_t fold_cap = 0;
     // tuning knobs (environment, read at ara_create; not part of the ABI)
     double grid_mult = 1.0;           // ARA_GRID_MULT
     int kernel_variant = -1;          // ARA_KERNEL (-1 auto; see pick_kernel in ara_kernel.cu)

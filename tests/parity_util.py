@@ -34,7 +34,7 @@ KERNEL_VARIANTS = (-1, 0, 1, 5, 8, 9)   # ARA_KERNEL: auto, register, cp.async r
 
 
 def run_gpu(off, ids, elts, w, layers, precision="f64", terms=None, load_mode="all", chunk_trials=0,
-            device_inputs=False, return_periods=None, variant=None):
+            device_inputs=False, return_periods=None, variant=None, run_mode="direct"):
     import os
     import torch
     from paper_1606_04473_b200 import ara
@@ -43,7 +43,8 @@ def run_gpu(off, ids, elts, w, layers, precision="f64", terms=None, load_mode="a
     if variant is not None:
         os.environ["ARA_KERNEL"] = str(variant)
     try:
-        ctx = ara.Context(w.catalog, precision=precision, load_mode=load_mode, chunk_trials=chunk_trials)
+        ctx = ara.Context(w.catalog, precision=precision, load_mode=load_mode, chunk_trials=chunk_trials,
+                          run_mode=run_mode)
     finally:
         if variant is not None:
             if old is None:

@@ -1,0 +1,76 @@
+"""Catalogue-fold mode: o(e) evaluated once per catalogue
+event, one gather per occurrence.  It must reproduce the direct path bit for
+bit (same per-event arithmetic, same per-trial order) and hence match the
+oracle within the same tolerance."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from parity_util import assert_ylt_close, make_inputs, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_fold_equals_direct_tiny(cuda, precision):
+    w = synth.get_config("tiny")
+    off, ids, elts = make_inputs(w)
+    a = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100))
+    b = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100), run_mode="fold")
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.array_equal(a[3][1], b[3][1]) and np.array_equal(a[3][2], b[3][2])
+    assert_ylt_close(b[0], run_oracle(off, ids, elts, w, w.layers, fp32=precision == "f32"))
+
+
+@pytest.mark.parametrize("n_layers", [1, 3, 5, 9, 17])
+def test_fold_many_layers_and_chunks(cuda, n_layers):
+    """Layer counts that exercise fold chunks of 1, 4, 8 layers and several
+    folded launches; windows unaligned and shared."""
+    w = synth.get_config("tiny").with_(n_elts=24, catalog=2000, rho=0.3, n_trials=600, nmin=0, nmax=260)
+    off, ids, elts = make_inputs(w)
+    rng = np.random.default_rng(n_layers)
+    layers = []
+    for l in range(n_layers):
+        b = int(rng.integers(0, 20))
+        e = int(rng.integers(b + 1, min(24, b + 16) + 1))
+        layers.append(synth.LayerSpec(b, e, float(rng.uniform(0, 5e4)), float(rng.choice([INF, rng.uniform(1e5, 1e6)])),
+                                      float(rng.uniform(0, 2e6)), float(rng.choice([INF, rng.uniform(1e6, 5e6)]))))
+    a = run_gpu(off, ids, elts, w, layers)
+    b = run_gpu(off, ids, elts, w, layers, run_mode="fold")
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    orc = run_oracle(off, ids, elts, w, layers)
+    assert_ylt_close(b[0], orc)
+    assert np.array_equal(b[1], orc["lossy"])
+
+
+def test_fold_chunked_h2d(cuda):
+    w = synth.get_config("tiny").with_(n_trials=2000)
+    off, ids, elts = make_inputs(w)
+    a = run_gpu(off, ids, elts, w, w.layers)
+    b = run_gpu(off, ids, elts, w, w.layers, run_mode="fold", load_mode="chunked", chunk_trials=77)
+    assert np.array_equal(a[0], b[0])
+
+
+def test_fold_fullsize_equals_direct(cuda):
+    """Paper-shaped (1M trials, 1e9 events): fold == direct, bit for bit."""
+    import torch
+    from paper_1606_04473_b200 import ara
+    w = synth.get_config("paper")
+    off, ids = synth.gen_yet(w)
+    eo, ev, ls = synth.gen_elts(w)
+    d_off = torch.from_numpy(off.view(np.int64)).cuda()
+    d_ids = torch.from_numpy(ids.view(np.int32)).cuda()
+    out = []
+    for mode in ("direct", "fold"):
+        y = torch.empty((2, w.n_trials), dtype=torch.float64, device="cuda")
+        with ara.Context(w.catalog, run_mode=mode, stream=torch.cuda.current_stream()) as ctx:
+            ctx.load_elts(eo, ev, ls, w.elt_terms())
+            ctx.load_yet(w.n_trials, 0, d_off, d_ids)
+            st = ctx.run(w.layers, y)
+        torch.cuda.synchronize()
+        out.append((y.cpu().numpy(), st))
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[1][1]["kernel_ms"] < out[0][1]["kernel_ms"]

@@ -12,6 +12,7 @@ ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--l2-persist", action="store_true")
 ap.add_argument("--rho", type=float, default=None)
 ap.add_argument("--catalog", type=int, default=None)
+ap.add_argument("--mode", default="direct")
 a = ap.parse_args()
 import torch
 from paper_1606_04473_b200 import ara
@@ -25,7 +26,8 @@ eo, ev, ls = synth.gen_elts(w)
 d_off = torch.from_numpy(off.view(np.int64)).cuda()
 d_ids = torch.from_numpy(ids.view(np.int32)).cuda()
 d_eo, d_ev, d_ls = (torch.from_numpy(x).cuda() for x in (eo.view(np.int64), ev.view(np.int32), ls))
-ctx = ara.Context(w.catalog, precision=a.precision, stream=torch.cuda.current_stream(), l2_persist=a.l2_persist)
+ctx = ara.Context(w.catalog, precision=a.precision, stream=torch.cuda.current_stream(), l2_persist=a.l2_persist,
+                  run_mode=a.mode)
 res = []
 for s in range(a.steps):
     ctx.load_elts(d_eo, d_ev, d_ls, w.elt_terms())
@@ -35,6 +37,6 @@ for s in range(a.steps):
     res.append((st["kernel_ms"], mms))
 torch.cuda.synchronize()
 ctx.close()
-print(json.dumps({"config": w.name, "catalog": w.catalog, "precision": a.precision, "env": {k: v for k, v in os.environ.items() if k.startswith("ARA_")},
+print(json.dumps({"config": w.name, "catalog": w.catalog, "mode": a.mode, "precision": a.precision, "env": {k: v for k, v in os.environ.items() if k.startswith("ARA_")},
                   "l2_persist": a.l2_persist, "kernel_ms": [r[0] for r in res], "metrics_ms": [r[1] for r in res],
                   "events": len(ids), "pml0": pml[0].tolist()}))
