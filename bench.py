@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
     ap.add_argument("--e2e-mode", default="chunked", choices=["chunked", "all"])
     ap.add_argument("--chunk-trials", type=int, default=65536)
+    ap.add_argument("--e2e-format", default="packed", choices=["packed", "u32"],
+                    help="host YET format for the e2e leg: bit-packed ids (F3, the library's transfer format) or u32")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -339,6 +341,13 @@ def main():
     if not a.no_e2e:
         ylt_pin = torch.empty((L + 1) * T, dtype=torch.float64, pin_memory=True)
         ids_view = ids_pin[:n_ev]
+        bits = ara.bits_for_catalog(w.catalog)
+        if a.e2e_format == "packed":   # host YET stored in the packed transfer format (setup, untimed)
+            packed_pin = torch.empty(ara.ara_packed_words(n_ev, bits), dtype=torch.int32, pin_memory=True)
+            ara.ara_pack_ids(ids_pin.numpy().view(np.uint32)[:n_ev], bits, packed_pin)
+            ids_bytes = packed_pin.numel() * 4
+        else:
+            ids_bytes = n_ev * 4
         ectx = ara.Context(w.catalog, device=local, precision=a.precision, stream=stream, rank=rank, world=world,
                            nccl_id=new_nccl_id(), load_mode=a.e2e_mode, chunk_trials=a.chunk_trials,
                            l2_persist=a.l2_persist, run_mode=a.mode)
@@ -350,7 +359,10 @@ def main():
             t0 = time.perf_counter()
             ectx.load_elts(eo_pin, ev_pin, ls_pin, terms, n_elts=w.n_elts)
             t1 = time.perf_counter()
-            ectx.load_yet(T, first, off_pin, ids_view)
+            if a.e2e_format == "packed":
+                ectx.load_yet_packed(T, first, off_pin, packed_pin, bits)
+            else:
+                ectx.load_yet(T, first, off_pin, ids_view)
             t2 = time.perf_counter()
             s2 = ectx.run(w.layers, ylt_pin)
             t3 = time.perf_counter()
@@ -371,11 +383,12 @@ def main():
         torch.cuda.synchronize()
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1)) / a.steps
-        h2d = n_off * 8 + n_ev * 4 + (eo_pin.numel() * 8 + ev_pin.numel() * 4 + ls_pin.numel() * 8 if rank == 0 else 0)
+        h2d = n_off * 8 + ids_bytes + (eo_pin.numel() * 8 + ev_pin.numel() * 4 + ls_pin.numel() * 8 if rank == 0 else 0)
         d2h = (L + 1) * T * 8 + 2 * (L + 1) * len(R) * 8 + 8
         e2e = {"value": T / (ems / 1e3), "unit": "trials/s", "ms_per_step": ems, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "mode": a.e2e_mode, "chunk_trials": a.chunk_trials,
-               "h2d_gbs": (n_ev * 4 + n_off * 8) / (float(np.mean(h2d_ms[-a.steps:])) / 1e3) / 1e9
+               "yet_format": a.e2e_format + (str(bits) if a.e2e_format == "packed" else ""),
+               "h2d_gbs": (ids_bytes + n_off * 8) / (float(np.mean(h2d_ms[-a.steps:])) / 1e3) / 1e9
                if a.e2e_mode == "chunked" and np.mean(h2d_ms) > 0 else None,
                "wall_ms": {k: 1e3 * float(np.median([x[i] for x in wall[-a.steps:]]))
                            for i, k in enumerate(("load_elts", "load_yet", "run", "metrics"))}}

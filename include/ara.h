@@ -180,6 +180,26 @@ ara_status ara_load_yet(ara_ctx* ctx, uint64_t n_trials_global, uint64_t first_t
                         uint64_t n_trials_local, const uint64_t* trial_offsets,
                         const uint32_t* event_ids);
 
+/* Packed YET transfer: the same as ara_load_yet, but the
+ * event ids arrive bit-packed, `bits` per id (1..32), id i of this shard at
+ * bit offset i*bits of the little-endian u32 word stream `packed_ids`
+ * (ara_pack_ids produces it; ara_packed_words gives its length, which
+ * includes one padding word).  Only the packed words cross PCIe; a device
+ * kernel unpacks them (per chunk in CHUNKED mode, overlapped with the copies).
+ * With C <= 2^21 (the paper's 2M-event catalogue) 21-bit ids move 34 % fewer
+ * bytes than u32.  Ids >= 2^bits cannot be represented (caller's choice of
+ * bits); ids outside [1, C] are reported by ara_run as usual.
+ * Errors: as ara_load_yet, plus INVALID_ARG for bits outside [1, 32]. */
+ara_status ara_load_yet_packed(ara_ctx* ctx, uint64_t n_trials_global, uint64_t first_trial,
+                               uint64_t n_trials_local, const uint64_t* trial_offsets,
+                               const uint32_t* packed_ids, uint32_t bits);
+
+/* Host helpers for the packed format (no GPU needed). */
+uint64_t ara_packed_words(uint64_t n_ids, uint32_t bits);
+/* Pack n_ids ids into out[ara_packed_words(n_ids, bits)] (host memory);
+ * INVALID_ARG if an id does not fit in `bits` bits or bits is outside [1, 32]. */
+ara_status ara_pack_ids(const uint32_t* ids, uint64_t n_ids, uint32_t bits, uint32_t* out);
+
 /* Aggregate Risk Analysis (Alg. 1 lines 1-8 per layer; Alg. 3 per trial).
  * For each layer l and each trial t (readings A1-A8):
  *   l_e   = sum_{j in layer, in order} min(max(tab[e][j] - D_j, 0), Lim_j)

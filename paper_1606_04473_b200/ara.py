@@ -75,6 +75,9 @@ _sig = {
     "ara_load_elts": (_i, [_vp, _u32, _vp, _vp, _vp, _vp]),
     "ara_set_elt_terms": (_i, [_vp, _u32, _vp]),
     "ara_load_yet": (_i, [_vp, _u64, _u64, _u64, _vp, _vp]),
+    "ara_load_yet_packed": (_i, [_vp, _u64, _u64, _u64, _vp, _vp, _u32]),
+    "ara_packed_words": (_u64, [_u64, _u32]),
+    "ara_pack_ids": (_i, [_vp, _u64, _u32, _vp]),
     "ara_run": (_i, [_vp, _u32, _vp, _vp, _vp, ctypes.POINTER(ara_run_stats)]),
     "ara_metrics": (_i, [_vp, _u32, _vp, _vp, _vp, _vp, ctypes.POINTER(_d)]),
 }
@@ -193,6 +196,30 @@ def ara_load_yet(h, n_trials_global: int, first_trial: int, trial_offsets, event
     _check(_lib.ara_load_yet(h, n_trials_global, first_trial, n_local, _ptr(trial_offsets), _ptr(event_ids)), h)
 
 
+def ara_load_yet_packed(h, n_trials_global: int, first_trial: int, trial_offsets, packed_ids, bits: int) -> None:
+    n_local = len(trial_offsets) - 1
+    _check(_lib.ara_load_yet_packed(h, n_trials_global, first_trial, n_local, _ptr(trial_offsets),
+                                    _ptr(packed_ids), bits), h)
+
+
+def ara_packed_words(n_ids: int, bits: int) -> int:
+    return int(_lib.ara_packed_words(n_ids, bits))
+
+
+def ara_pack_ids(ids, bits: int, out=None):
+    """Bit-pack u32 ids (host) into the ara_load_yet_packed word stream."""
+    ids = np.ascontiguousarray(ids, dtype=np.uint32)
+    words = ara_packed_words(len(ids), bits)
+    if out is None:
+        out = np.empty(words, dtype=np.uint32)
+    _check(_lib.ara_pack_ids(ids.ctypes.data, len(ids), bits, _ptr(out)), what="id does not fit in bits")
+    return out
+
+
+def bits_for_catalog(catalog_size: int) -> int:
+    return max(1, int(catalog_size).bit_length())
+
+
 def _layers_array(layers):
     arr = (ara_layer * len(layers))()
     for i, L in enumerate(layers):
@@ -265,6 +292,10 @@ class Context:
         ara_load_yet(self.h, n_trials_global, first_trial, trial_offsets, event_ids)
         self.n_trials = n_trials_global
 
+    def load_yet_packed(self, n_trials_global: int, first_trial: int, trial_offsets, packed_ids, bits: int):
+        ara_load_yet_packed(self.h, n_trials_global, first_trial, trial_offsets, packed_ids, bits)
+        self.n_trials = n_trials_global
+
     def run(self, layers, ylt=None, lossy=None) -> dict:
         st = ara_run(self.h, layers, ylt, lossy)
         self.n_layers = len(layers)
@@ -285,4 +316,5 @@ class Context:
 
 __all__ = ["Context", "AraError", "ara_create", "ara_destroy", "ara_load_elts", "ara_set_elt_terms",
            "ara_load_yet", "ara_run", "ara_metrics", "ara_partition", "ara_return_period_rank",
-           "ara_nccl_unique_id", "status_string", "version", "EXPORTED"]
+           "ara_nccl_unique_id", "ara_load_yet_packed", "ara_pack_ids", "ara_packed_words", "bits_for_catalog",
+           "status_string", "version", "EXPORTED"]

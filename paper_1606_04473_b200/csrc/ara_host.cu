@@ -10,6 +10,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <new>
+#include <thread>
 
 #include "ara_internal.cuh"
 
@@ -134,6 +135,8 @@ void release_yet(ara_ctx* ctx) {
     ctx->d_ids = nullptr;
     ctx->h_off = nullptr;
     ctx->h_ids = nullptr;
+    ctx->h_packed = nullptr;
+    ctx->pack_bits = 0;
     ctx->chunked_pending = false;
     ctx->yet_loaded = false;
     ctx->tiling_checked = false;
@@ -281,6 +284,7 @@ extern "C" void ara_destroy(ara_ctx* ctx) {
     cudaFree(ctx->d_table);
     cudaFree(ctx->d_off_own);
     cudaFree(ctx->d_ids_own);
+    cudaFree(ctx->d_packed_own);
     cudaFree(ctx->d_ylt_local);
     cudaFree(ctx->d_ylt_gather);
     cudaFree(ctx->d_ylt_global);
@@ -483,9 +487,12 @@ extern "C" ara_status ara_set_elt_terms(ara_ctx* ctx, uint32_t n_elts, const ara
 }
 
 // ============================================================ YET
-extern "C" ara_status ara_load_yet(ara_ctx* ctx, uint64_t n_trials_global, uint64_t first_trial,
-                                   uint64_t n_trials_local, const uint64_t* trial_offsets,
-                                   const uint32_t* event_ids) {
+namespace {
+
+// YET ingest shared by ara_load_yet (bits == 0: u32 ids) and
+// ara_load_yet_packed (bits > 0: bit-packed ids, unpacked on the device).
+ara_status load_yet_impl(ara_ctx* ctx, uint64_t n_trials_global, uint64_t first_trial, uint64_t n_trials_local,
+                         const uint64_t* trial_offsets, const uint32_t* event_ids, uint32_t bits) {
     if (!ctx) return ARA_ERR_INVALID_ARG;
     CK(cudaSetDevice(ctx->device));
     if (n_trials_global == 0) return fail(ctx, ARA_ERR_INVALID_ARG, "n_trials_global must be >= 1");
@@ -494,6 +501,7 @@ extern "C" ara_status ara_load_yet(ara_ctx* ctx, uint64_t n_trials_global, uint6
                     (unsigned long long)first_trial, (unsigned long long)n_trials_local,
                     (unsigned long long)n_trials_global);
     if (!trial_offsets) return fail(ctx, ARA_ERR_INVALID_ARG, "trial_offsets is NULL");
+    if (bits > 32) return fail(ctx, ARA_ERR_INVALID_ARG, "bits must be in [1, 32]");
     CK(cudaStreamSynchronize(ctx->stream));   // a previous run may still read the old YET
     release_yet(ctx);
 
@@ -508,7 +516,7 @@ extern "C" ara_status ara_load_yet(ara_ctx* ctx, uint64_t n_trials_global, uint6
         n_ev_known = true;
     }
     if (!event_ids && !(n_ev_known && n_ev == 0)) return fail(ctx, ARA_ERR_INVALID_ARG, "event_ids is NULL");
-    if (mi != Mem::Device && !n_ev_known) {
+    if ((mi != Mem::Device || bits) && !n_ev_known) {
         CK(cudaMemcpy(ctx->h_small, trial_offsets, sizeof(uint64_t), cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(ctx->h_small + 1, trial_offsets + n_trials_local, sizeof(uint64_t), cudaMemcpyDeviceToHost));
         if (ctx->h_small[1] < ctx->h_small[0]) return fail(ctx, ARA_ERR_OUT_OF_RANGE, "YET trial offsets decrease");
@@ -517,6 +525,7 @@ extern "C" ara_status ara_load_yet(ara_ctx* ctx, uint64_t n_trials_global, uint6
     }
     ctx->n_events_host = n_ev_known ? n_ev : 0;
     const bool chunked = ctx->load_mode == ARA_LOAD_CHUNKED;
+    const uint64_t words = bits ? ara_packed_words(n_ev, bits) : 0;
 
     // offsets
     if (mo == Mem::Device) {
@@ -530,26 +539,43 @@ extern "C" ara_status ara_load_yet(ara_ctx* ctx, uint64_t n_trials_global, uint6
                                 cudaMemcpyHostToDevice, ctx->stream));
     }
     // event ids
-    if (mi == Mem::Device) {
+    if (mi == Mem::Device && !bits) {
         ctx->d_ids = event_ids;
     } else {
         ara_status st = ensure(ctx, ctx->d_ids_own, ctx->own_ids_cap, n_ev);
         if (st != ARA_OK) return st;
         ctx->d_ids = ctx->d_ids_own;
-        if (chunked) {
-            ctx->h_ids = event_ids;
+        if (bits && mi == Mem::Device) {            // packed, already on the device: unpack now
+            CK(launch_unpack(event_ids, bits, 0, n_ev, ctx->d_ids_own, ctx->stream));
+        } else if (chunked) {
+            const size_t host_bytes = bits ? words * sizeof(uint32_t) : n_ev * sizeof(uint32_t);
+            if (bits) {
+                ctx->h_packed = event_ids;
+                st = ensure(ctx, ctx->d_packed_own, ctx->packed_cap, words);
+                if (st != ARA_OK) return st;
+            } else {
+                ctx->h_ids = event_ids;
+            }
             if (mi == Mem::Host && n_ev) {   // pageable: pin for async DMA (once per load)
-                if (cudaHostRegister((void*)event_ids, n_ev * sizeof(uint32_t), cudaHostRegisterReadOnly) ==
-                    cudaSuccess)
+                if (cudaHostRegister((void*)event_ids, host_bytes, cudaHostRegisterReadOnly) == cudaSuccess)
                     ctx->h_registered = (void*)event_ids;
                 cudaGetLastError();
             }
         } else if (n_ev) {
-            CK(cudaMemcpyAsync(ctx->d_ids_own, event_ids, n_ev * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                               ctx->stream));
+            if (bits) {
+                st = ensure(ctx, ctx->d_packed_own, ctx->packed_cap, words);
+                if (st != ARA_OK) return st;
+                CK(cudaMemcpyAsync(ctx->d_packed_own, event_ids, words * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                   ctx->stream));
+                CK(launch_unpack(ctx->d_packed_own, bits, 0, n_ev, ctx->d_ids_own, ctx->stream));
+            } else {
+                CK(cudaMemcpyAsync(ctx->d_ids_own, event_ids, n_ev * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                                   ctx->stream));
+            }
         }
     }
-    ctx->chunked_pending = chunked && (ctx->h_off || ctx->h_ids);
+    ctx->pack_bits = bits;
+    ctx->chunked_pending = chunked && (ctx->h_off || ctx->h_ids || ctx->h_packed);
     if (!ctx->chunked_pending) CK(cudaStreamSynchronize(ctx->stream));
     ctx->T_global = n_trials_global;
     ctx->first = first_trial;
@@ -557,6 +583,61 @@ extern "C" ara_status ara_load_yet(ara_ctx* ctx, uint64_t n_trials_global, uint6
     ctx->yet_loaded = true;
     ctx->tiling_checked = false;
     return ARA_OK;
+}
+
+}  // namespace
+
+extern "C" uint64_t ara_packed_words(uint64_t n_ids, uint32_t bits) {
+    if (bits == 0 || bits > 32) return 0;
+    return (n_ids * bits + 31) / 32 + 1;   // + one padding word (two-word reads)
+}
+
+extern "C" ara_status ara_pack_ids(const uint32_t* ids, uint64_t n, uint32_t bits, uint32_t* out) {
+    if (bits == 0 || bits > 32 || (!ids && n) || !out) return ARA_ERR_INVALID_ARG;
+    const uint64_t words = ara_packed_words(n, bits);
+    const uint64_t lim = bits == 32 ? 0x100000000ull : (1ull << bits);
+    // 32 consecutive ids fill exactly `bits` whole words, so groups of 32 ids
+    // pack independently (threads over groups).
+    const uint64_t groups = (n + 31) / 32;
+    unsigned nt = std::thread::hardware_concurrency();
+    if (nt < 1) nt = 1;
+    if (nt > 64) nt = 64;
+    if (n < (1u << 20)) nt = 1;
+    std::vector<int> bad(nt, 0);
+    auto work = [&](unsigned k) {
+        const uint64_t g0 = groups * k / nt, g1 = groups * (k + 1) / nt;
+        for (uint64_t w = g0 * bits; w < g1 * bits && w < words; ++w) out[w] = 0u;
+        for (uint64_t i = g0 * 32; i < g1 * 32 && i < n; ++i) {
+            const uint64_t v = ids[i];
+            if (v >= lim) { bad[k] = 1; continue; }
+            const uint64_t b = i * bits;
+            const uint64_t w = b >> 5;
+            const uint64_t x = v << (b & 31);
+            out[w] |= (uint32_t)x;
+            if ((x >> 32) != 0) out[w + 1] |= (uint32_t)(x >> 32);
+        }
+    };
+    std::vector<std::thread> th;
+    for (unsigned k = 1; k < nt; ++k) th.emplace_back(work, k);
+    work(0);
+    for (auto& t : th) t.join();
+    for (uint64_t w = groups * bits; w < words; ++w) out[w] = 0u;
+    for (int b : bad)
+        if (b) return ARA_ERR_INVALID_ARG;
+    return ARA_OK;
+}
+
+extern "C" ara_status ara_load_yet(ara_ctx* ctx, uint64_t n_trials_global, uint64_t first_trial,
+                                   uint64_t n_trials_local, const uint64_t* trial_offsets,
+                                   const uint32_t* event_ids) {
+    return load_yet_impl(ctx, n_trials_global, first_trial, n_trials_local, trial_offsets, event_ids, 0);
+}
+
+extern "C" ara_status ara_load_yet_packed(ara_ctx* ctx, uint64_t n_trials_global, uint64_t first_trial,
+                                          uint64_t n_trials_local, const uint64_t* trial_offsets,
+                                          const uint32_t* packed_ids, uint32_t bits) {
+    if (ctx && (bits == 0 || bits > 32)) return fail(ctx, ARA_ERR_INVALID_ARG, "bits must be in [1, 32]");
+    return load_yet_impl(ctx, n_trials_global, first_trial, n_trials_local, trial_offsets, packed_ids, bits);
 }
 
 // ============================================================ run
@@ -667,6 +748,7 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
         chunks.push_back({0, T_local});
     }
     std::vector<cudaEvent_t> chunk_ev;
+    std::vector<uint64_t> ho_chunk;   // event index (relative) of each chunk boundary
     uint64_t h2d_bytes = 0;
     if (stream_in) {
         CK(cudaEventRecord(ctx->ev[5], s));
@@ -693,14 +775,26 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
                 return fail(ctx, ARA_ERR_CUDA, "cudaEventCreate failed");
             }
         }
+        ho_chunk.resize(chunks.size() + 1);
+        for (size_t c = 0; c < chunks.size(); ++c) ho_chunk[c] = ho[chunks[c].first] - ho[0];
+        ho_chunk[chunks.size()] = ho[T_local] - ho[0];
+        const uint64_t nev_all = ho[T_local] - ho[0];
+        const uint32_t pb = ctx->pack_bits;
+        const uint64_t words_all = pb ? ara_packed_words(nev_all, pb) : 0;
         for (size_t c = 0; c < chunks.size(); ++c) {
-            if (ctx->h_ids) {
-                const uint64_t e0 = ho[chunks[c].first] - ho[0], e1 = ho[chunks[c].second] - ho[0];
-                if (e1 > e0) {
-                    CK(cudaMemcpyAsync(ctx->d_ids_own + e0, ctx->h_ids + e0, (e1 - e0) * sizeof(uint32_t),
-                                       cudaMemcpyHostToDevice, ctx->copy_stream));
-                    h2d_bytes += (e1 - e0) * sizeof(uint32_t);
-                }
+            const uint64_t e0 = ho[chunks[c].first] - ho[0], e1 = ho[chunks[c].second] - ho[0];
+            if (ctx->h_ids && e1 > e0) {
+                CK(cudaMemcpyAsync(ctx->d_ids_own + e0, ctx->h_ids + e0, (e1 - e0) * sizeof(uint32_t),
+                                   cudaMemcpyHostToDevice, ctx->copy_stream));
+                h2d_bytes += (e1 - e0) * sizeof(uint32_t);
+            }
+            if (ctx->h_packed && e1 > e0) {   // the chunk's packed words (+ the word its last id spills into)
+                const uint64_t w0 = (e0 * pb) >> 5;
+                uint64_t w1 = ((e1 * pb + 31) >> 5) + 1;
+                if (w1 > words_all) w1 = words_all;
+                CK(cudaMemcpyAsync(ctx->d_packed_own + w0, ctx->h_packed + w0, (w1 - w0) * sizeof(uint32_t),
+                                   cudaMemcpyHostToDevice, ctx->copy_stream));
+                h2d_bytes += (w1 - w0) * sizeof(uint32_t);
             }
             CK(cudaEventRecord(chunk_ev[c], ctx->copy_stream));
         }
@@ -767,6 +861,10 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
     }
     for (size_t c = 0; c < chunks.size(); ++c) {
         if (stream_in) CK(cudaStreamWaitEvent(s, chunk_ev[c], 0));
+        if (stream_in && ctx->h_packed) {   // F3: unpack this chunk's ids on the device
+            const uint64_t e0 = ho_chunk[c], e1 = ho_chunk[c + 1];
+            CK(launch_unpack(ctx->d_packed_own, ctx->pack_bits, e0, e1, ctx->d_ids_own, s));
+        }
         if (fold) {
             for (uint32_t fc = 0; fc < n_chunks_fold; ++fc) {
                 TrialParams p = base;

@@ -106,6 +106,8 @@ cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int
 int trial_kernel_grid(int fp32, uint32_t max_nsec, int n_layers, int variant);
 void set_ldg_carveout(int fp32, uint32_t nsec, int nl, int pct);
 cudaError_t launch_fold(const TrialParams& p, int fp32, uint32_t nsec, cudaStream_t s);
+cudaError_t launch_unpack(const uint32_t* packed, uint32_t bits, uint64_t e0, uint64_t e1, uint32_t* ids,
+                          cudaStream_t s);
 cudaError_t launch_trials_folded(const TrialParams& p, int grid_mult_x100, cudaStream_t s);
 cudaError_t launch_trials_wide(const TrialParams& p, int fp32, const double2* d_cterm, uint32_t col0,
                                uint32_t ncol, int grid, cudaStream_t s);
@@ -171,6 +173,10 @@ struct ara_ctx {
     const uint32_t* h_ids = nullptr;
     void* h_registered = nullptr;      // host range we cudaHostRegister'ed
     bool chunked_pending = false;
+    uint32_t pack_bits = 0;            // > 0: the YET ids arrive bit-packed (ara_load_yet_packed)
+    const uint32_t* h_packed = nullptr;
+    uint32_t* d_packed_own = nullptr;
+    size_t packed_cap = 0;
     uint64_t n_events_host = 0;        // known when offsets were host memory
     bool tiling_checked = false;
 

@@ -41,7 +41,29 @@ __global__ void __launch_bounds__(256) densify_kernel(const uint64_t* __restrict
     if (bad) atomicOr(err, bad);
 }
 
+// Packed YET ids (F3): id i at bit offset i*bits of a u32 word stream.
+__global__ void __launch_bounds__(256) unpack_kernel(const uint32_t* __restrict__ packed, uint32_t bits,
+                                                     uint64_t e0, uint64_t e1, uint32_t* __restrict__ ids) {
+    const uint64_t mask = bits >= 32 ? 0xffffffffull : ((1ull << bits) - 1);
+    for (uint64_t i = e0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < e1;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t b = i * bits;
+        const uint64_t w = b >> 5;
+        const uint64_t v = (uint64_t)__ldg(packed + w) | ((uint64_t)__ldg(packed + w + 1) << 32);
+        ids[i] = (uint32_t)((v >> (b & 31)) & mask);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_unpack(const uint32_t* packed, uint32_t bits, uint64_t e0, uint64_t e1, uint32_t* ids,
+                          cudaStream_t s) {
+    if (e1 <= e0) return cudaSuccess;
+    uint64_t blocks = (e1 - e0 + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    unpack_kernel<<<(unsigned)blocks, 256, 0, s>>>(packed, bits, e0, e1, ids);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const double* d_loss,
                            uint32_t n_elts, uint64_t n_records, uint32_t catalog, void* d_table,

@@ -17,7 +17,7 @@ LIB = os.path.join(ROOT, "paper_1606_04473_b200", "libara.so")
 def declared_symbols():
     src = open(HDR).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:const\s+)?(?:ara_status|void|const char\*|char\*)\s*\**\s*(ara_\w+)\s*\(",
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?(?:ara_status|void|uint64_t|const char\*|char\*)\s*\**\s*(ara_\w+)\s*\(",
                                  src, flags=re.M)))
 
 
@@ -97,3 +97,21 @@ def test_product_path_never_touches_the_oracle():
                     assert bad not in txt, (f, bad)
     out = subprocess.run(["ldd", LIB], capture_output=True, text=True).stdout
     assert "oracle" not in out
+
+
+def test_pack_ids_matches_bit_layout():
+    """F3 packed transfer format: id i at bit offset i*bits, little-endian words."""
+    from paper_1606_04473_b200 import ara
+    rng = np.random.default_rng(5)
+    for bits in (1, 7, 21, 31, 32):
+        for n in (0, 1, 31, 32, 33, 1000, (1 << 20) + 77):
+            ids = rng.integers(0, 1 << bits, size=n, dtype=np.uint64).astype(np.uint32)
+            packed = ara.ara_pack_ids(ids, bits)
+            assert len(packed) == (n * bits + 31) // 32 + 1
+            # decode with python big ints on a sample (exhaustive for small n)
+            as_int = int.from_bytes(packed.astype("<u4").tobytes(), "little")
+            idx = range(n) if n <= 2000 else rng.integers(0, n, 2000)
+            for i in idx:
+                assert (as_int >> (int(i) * bits)) & ((1 << bits) - 1) == ids[i]
+    with pytest.raises(ara.AraError):
+        ara.ara_pack_ids(np.array([1 << 21], np.uint32), 21)

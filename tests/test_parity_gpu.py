@@ -255,3 +255,39 @@ def test_errors_are_reported_and_context_survives(cuda):
         with pytest.raises(ara.AraError) as e:
             ctx.metrics([w.n_trials + 1.0])
         assert e.value.status == ara.ARA_ERR_DOMAIN
+
+
+@pytest.mark.parametrize("load_mode,chunk", [("all", 0), ("chunked", 1), ("chunked", 37), ("chunked", 10 ** 6)])
+def test_packed_yet_transfer_equals_u32(cuda, load_mode, chunk):
+    """F3: bit-packed ids (14/21/32 bits) through host or device memory give the
+    same YLT bits as u32 ids; chunk boundaries split words."""
+    import torch
+    from paper_1606_04473_b200 import ara
+    w = synth.get_config("tiny").with_(n_trials=1500)
+    off, ids, elts = make_inputs(w)
+    ref, ref_lossy, _, _ = run_gpu(off, ids, elts, w, w.layers)
+    for bits in (ara.bits_for_catalog(w.catalog), 21, 32):
+        packed = ara.ara_pack_ids(ids, bits)
+        for device in (False, True):
+            src = torch.from_numpy(packed.view(np.int32)).cuda() if device else packed
+            with ara.Context(w.catalog, load_mode=load_mode, chunk_trials=chunk) as ctx:
+                ctx.load_elts(*elts, terms=w.elt_terms())
+                ctx.load_yet_packed(w.n_trials, 0, off, src, bits)
+                ylt, lossy, st = ctx.run_host(w.layers)
+            assert np.array_equal(ylt, ref) and np.array_equal(lossy, ref_lossy), (bits, device)
+            if load_mode == "chunked" and not device:
+                assert st["h2d_bytes"] < ids.nbytes + off.nbytes or bits == 32
+
+
+def test_packed_out_of_range_id_reported(cuda):
+    from paper_1606_04473_b200 import ara
+    w = synth.get_config("tiny")
+    off, ids, elts = make_inputs(w)
+    bad = ids.copy()
+    bad[777] = w.catalog + 5
+    with ara.Context(w.catalog, load_mode="chunked", chunk_trials=100) as ctx:
+        ctx.load_elts(*elts)
+        ctx.load_yet_packed(w.n_trials, 0, off, ara.ara_pack_ids(bad, 14), 14)
+        with pytest.raises(ara.AraError) as e:
+            ctx.run(w.layers)
+        assert e.value.status == ara.ARA_ERR_OUT_OF_RANGE
