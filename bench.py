@@ -44,7 +44,7 @@ METRIC = "trials/sec and ELT lookups/sec at 1/2/4/8 B200; % of HBM roofline"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=40)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="paper")
@@ -76,9 +76,12 @@ def host_info():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons, sampled every 100 ms from before the
+    warm-up to after the timed region; mark() brackets the timed window and
+    stop() summarises the samples inside it (all samples if the window was
+    shorter than two sampling periods)."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -87,11 +90,12 @@ class ClockSampler:
         self.proc = None
         self.lines = []
         self.t = None
+        self.win = [None, None]
 
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "200", "-i", str(self.gpu)],
+                                          "-lms", "100", "-i", str(self.gpu)],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -100,36 +104,41 @@ class ClockSampler:
 
     def _read(self):
         for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+            self.lines.append((time.time(), ln.strip()))
+
+    def mark(self, i):
+        self.win[i] = time.time()
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.t.join(timeout=2)
-        sm, smax, reasons = [], [], set()
+        rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ts, ln in self.lines:
             p = [x.strip() for x in ln.split(",")]
-            if len(p) < 9:
+            if len(p) < 10:
                 continue
             try:
-                sm.append(float(p[1]))
-                smax.append(float(p[2]))
+                rows.append((ts, float(p[2]), float(p[3]), [nm for nm, v in zip(names, p[6:10]) if v.lower() == "active"]))
             except ValueError:
                 continue
-            for nm, v in zip(names, p[5:9]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
-        load = [s for s in sm if s > 0.5 * max(sm)] or sm
-        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": float(max(smax)), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        a, b = self.win
+        inside = [r for r in rows if a is not None and b is not None and a - 0.15 <= r[0] <= b + 0.15]
+        sel = inside if len(inside) >= 2 else rows
+        sm = [r[1] for r in sel]
+        load = [x for x in sm if x > 0.5 * max(sm)] or sm
+        reasons = sorted({x for r in sel for x in r[3]})
+        return {"sm_mhz": float(np.median(load)), "sm_max_mhz": float(max(r[2] for r in sel)), "reasons": reasons,
+                "samples": len(sel), "window": "timed region" if sel is inside else "whole run"}
 
 
 def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str = "direct") -> int:
@@ -306,11 +315,13 @@ def main():
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks.mark(0)
     e0.record(stream)
     for _ in range(a.steps):
         st, pml, tvar = step(True)
     e1.record(stream)
     torch.cuda.synchronize()
+    clocks.mark(1)
     barrier()
     clk = clocks.stop()
     ms = max_over_ranks(e0.elapsed_time(e1)) / a.steps

@@ -291,10 +291,12 @@ class Context:
     def load_yet(self, n_trials_global: int, first_trial: int, trial_offsets, event_ids):
         ara_load_yet(self.h, n_trials_global, first_trial, trial_offsets, event_ids)
         self.n_trials = n_trials_global
+        self._yet_refs = (trial_offsets, event_ids)   # CHUNKED mode reads them during ara_run
 
     def load_yet_packed(self, n_trials_global: int, first_trial: int, trial_offsets, packed_ids, bits: int):
         ara_load_yet_packed(self.h, n_trials_global, first_trial, trial_offsets, packed_ids, bits)
         self.n_trials = n_trials_global
+        self._yet_refs = (trial_offsets, packed_ids)   # CHUNKED mode reads them during ara_run
 
     def run(self, layers, ylt=None, lossy=None) -> dict:
         st = ara_run(self.h, layers, ylt, lossy)
