@@ -46,6 +46,7 @@ extern "C" {
 #define ARA_NCCL_ID_BYTES 128   /* sizeof(ncclUniqueId) */
 #define ARA_MAX_LAYERS 64       /* layers per ara_run call */
 #define ARA_MAX_RP 64           /* return periods per ara_metrics call */
+#define ARA_MAX_PROGRAMS 64     /* programs per ara_run_portfolio call */
 
 typedef struct ara_ctx ara_ctx;
 
@@ -101,6 +102,15 @@ typedef struct {
     uint32_t elt_begin, elt_end;
     double occ_retention, occ_limit, agg_retention, agg_limit;
 } ara_layer;
+
+/* A layer with an explicit ELT list (ara_run_portfolio): `elts` (host) holds
+ * n_elts strictly ascending indices into the loaded ELT set; the layer's ELT
+ * losses are summed in that order.  Terms as in ara_layer. */
+typedef struct {
+    const uint32_t* elts;
+    uint32_t n_elts;
+    double occ_retention, occ_limit, agg_retention, agg_limit;
+} ara_layer_list;
 
 typedef struct {
     uint64_t n_trials_local, n_events_local, n_lookups_local;
@@ -220,10 +230,26 @@ ara_status ara_pack_ids(const uint32_t* ids, uint64_t n_ids, uint32_t bits, uint
 ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* layers,
                    double* ylt, uint32_t* lossy, ara_run_stats* stats);
 
+/* A portfolio of programs (Alg. 1 lines 1-2 "for each Program, for
+ * each Layer"): n_layers layers with explicit ELT lists, grouped into
+ * n_programs programs — program q owns layers [program_layers[q],
+ * program_layers[q+1]) (program_layers [n_programs+1], host, from 0 to
+ * n_layers, every program non-empty; n_programs may be 0).
+ *   ylt [(n_layers + n_programs + 1)][n_trials_global]: the layer rows, then
+ *       one row per program (sum of its layers, in layer order), then the
+ *       portfolio (sum of all layers, in layer order).
+ *   lossy, stats, collective semantics and errors: as ara_run.
+ * ara_metrics then reports every one of those rows. */
+ara_status ara_run_portfolio(ara_ctx* ctx, uint32_t n_programs, const uint32_t* program_layers,
+                             uint32_t n_layers, const ara_layer_list* layers, double* ylt, uint32_t* lossy,
+                             ara_run_stats* stats);
+
 /* PML / TVaR of the last ara_run's YLT, for every layer and the portfolio:
  *   k[r]   = ceil(T / R_r)                                          (A10)
- *   pml [(n_layers+1)][n_rp]  = k-th largest Y                      (A9)
- *   tvar[(n_layers+1)][n_rp]  = mean of the k largest Y             (A9)
+ *   pml [rows][n_rp]  = k-th largest Y                              (A9)
+ *   tvar[rows][n_rp]  = mean of the k largest Y                     (A9)
+ *   rows = n_layers + 1 after ara_run, n_layers + n_programs + 1 after
+ *   ara_run_portfolio (the YLT rows, in the same order)
  * computed on the device by radix select over the fp64 bit patterns plus a
  * masked tail sum.  Outputs are HOST pointers (k may be NULL).  device_ms
  * (nullable) receives the metrics kernels' event time.  Every rank computes

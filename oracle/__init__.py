@@ -51,6 +51,8 @@ def lib():
         L.oracle_ara.restype = i32
         L.oracle_ara.argtypes = [vp, vp, u64, ctypes.POINTER(_Elts), u32, vp, vp, u32,
                                  ctypes.POINTER(_Layer), i32, vp, i32, vp, vp, vp, vp]
+        L.oracle_programs.restype = i32
+        L.oracle_programs.argtypes = [vp, u64, u32, u32, vp, vp]
         L.oracle_rank.restype = u64
         L.oracle_rank.argtypes = [u64, d]
         L.oracle_metrics.restype = i32
@@ -136,6 +138,17 @@ def ara(trial_off, event_ids, elts: Elts, catalog: int, elt_deductible, elt_limi
     if rc != 0:
         raise ValueError("oracle_ara: event id outside [1, catalog] or unresolved ELT")
     return {"ylt": ylt, "scale": scale, "lossy": lossy, "portfolio": port}
+
+
+def programs(ylt, program_layers):
+    """Program year losses: sums of each program's layer rows in layer order."""
+    y = _c(ylt, np.float64)
+    pl = _c(program_layers, np.uint32)
+    P = len(pl) - 1
+    out = np.zeros((P, y.shape[1]), dtype=np.float64)
+    if lib().oracle_programs(y.ctypes.data, y.shape[1], y.shape[0], P, pl.ctypes.data, out.ctypes.data) != 0:
+        raise ValueError("malformed program_layers")
+    return out
 
 
 def rank(n_trials: int, return_period: float) -> int:

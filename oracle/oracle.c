@@ -102,6 +102,21 @@ int oracle_ara(const uint64_t* trial_off, const uint32_t* event_ids, uint64_t n_
     return 0;
 }
 
+/* P:248-252 "PF = {P1, P2, ...}" with Alg. 1's loops over programs and layers. */
+int oracle_programs(const double* ylt, uint64_t n_trials, uint32_t n_layers, uint32_t n_programs,
+                    const uint32_t* program_layers, double* out) {
+    if (n_programs && (program_layers[0] != 0 || program_layers[n_programs] != n_layers)) return -1;
+    for (uint32_t q = 0; q < n_programs; ++q) {
+        if (program_layers[q + 1] <= program_layers[q]) return -1;
+        for (uint64_t t = 0; t < n_trials; ++t) {
+            double s = 0.0;
+            for (uint32_t l = program_layers[q]; l < program_layers[q + 1]; ++l) s = s + ylt[(uint64_t)l * n_trials + t];
+            out[(uint64_t)q * n_trials + t] = s;
+        }
+    }
+    return 0;
+}
+
 /* Reading A10: integer R -> (T + R - 1) / R in u64; otherwise ceil in long double. */
 uint64_t oracle_rank(uint64_t n_trials, double R) {
     if (!(R >= 1.0) || R > (double)n_trials) return 0;

@@ -80,6 +80,13 @@ int oracle_ara(const uint64_t* trial_off, const uint32_t* event_ids, uint64_t n_
                int lookup_mode, const double* dense, int fp32_storage,
                double* ylt, double* scale, uint32_t* lossy, double* portfolio);
 
+/* Programs (Alg. 1 l.1): program q's year loss = the sum of its
+ * layers' year losses [program_layers[q], program_layers[q+1]) in layer
+ * order, from 0.  ylt [n_layers][T] -> out [n_programs][T].  Returns 0 or -1
+ * on a malformed program_layers. */
+int oracle_programs(const double* ylt, uint64_t n_trials, uint32_t n_layers, uint32_t n_programs,
+                    const uint32_t* program_layers, double* out);
+
 /* k = ceil(T / R) for return period R, 1 <= R <= T (A10).  0 on domain error. */
 uint64_t oracle_rank(uint64_t n_trials, double return_period);
 

@@ -51,6 +51,12 @@ class ara_layer(ctypes.Structure):
                 ("agg_retention", ctypes.c_double), ("agg_limit", ctypes.c_double)]
 
 
+class ara_layer_list(ctypes.Structure):
+    _fields_ = [("elts", ctypes.c_void_p), ("n_elts", ctypes.c_uint32),
+                ("occ_retention", ctypes.c_double), ("occ_limit", ctypes.c_double),
+                ("agg_retention", ctypes.c_double), ("agg_limit", ctypes.c_double)]
+
+
 class ara_run_stats(ctypes.Structure):
     _fields_ = [("n_trials_local", ctypes.c_uint64), ("n_events_local", ctypes.c_uint64),
                 ("n_lookups_local", ctypes.c_uint64), ("kernel_ms", ctypes.c_double),
@@ -79,6 +85,7 @@ _sig = {
     "ara_packed_words": (_u64, [_u64, _u32]),
     "ara_pack_ids": (_i, [_vp, _u64, _u32, _vp]),
     "ara_run": (_i, [_vp, _u32, _vp, _vp, _vp, ctypes.POINTER(ara_run_stats)]),
+    "ara_run_portfolio": (_i, [_vp, _u32, _vp, _u32, _vp, _vp, _vp, ctypes.POINTER(ara_run_stats)]),
     "ara_metrics": (_i, [_vp, _u32, _vp, _vp, _vp, _vp, ctypes.POINTER(_d)]),
 }
 for _name, (_res, _args) in _sig.items():
@@ -239,11 +246,30 @@ def ara_run(h, layers, ylt=None, lossy=None) -> dict:
     return stats.as_dict()
 
 
-def ara_metrics(h, n_layers: int, return_periods: Sequence[float]):
+def ara_run_portfolio(h, programs, ylt=None, lossy=None) -> dict:
+    """programs: list of programs, each a list of layers (elts, OccR, OccL, AggR, AggL)
+    with `elts` strictly ascending ELT indices."""
+    flat = [L for prog in programs for L in prog]
+    pl = np.zeros(len(programs) + 1, dtype=np.uint32)
+    pl[1:] = np.cumsum([len(p) for p in programs])
+    keep = []
+    arr = (ara_layer_list * len(flat))()
+    for i, L in enumerate(flat):
+        e = np.ascontiguousarray(L[0], dtype=np.uint32)
+        keep.append(e)
+        arr[i] = ara_layer_list(e.ctypes.data, len(e), float(L[1]), float(L[2]), float(L[3]), float(L[4]))
+    stats = ara_run_stats()
+    _check(_lib.ara_run_portfolio(h, len(programs), pl.ctypes.data, len(flat), ctypes.cast(arr, _vp), _ptr(ylt),
+                                  _ptr(lossy), ctypes.byref(stats)), h)
+    return stats.as_dict()
+
+
+def ara_metrics(h, n_rows: int, return_periods: Sequence[float]):
+    """n_rows: YLT rows of the last run (n_layers + 1, or n_layers + n_programs + 1)."""
     R = np.ascontiguousarray(return_periods, dtype=np.float64)
     k = np.zeros(len(R), dtype=np.uint64)
-    pml = np.zeros((n_layers + 1, len(R)), dtype=np.float64)
-    tvar = np.zeros((n_layers + 1, len(R)), dtype=np.float64)
+    pml = np.zeros((n_rows, len(R)), dtype=np.float64)
+    tvar = np.zeros((n_rows, len(R)), dtype=np.float64)
     ms = _d()
     _check(_lib.ara_metrics(h, len(R), R.ctypes.data, k.ctypes.data, pml.ctypes.data, tvar.ctypes.data,
                             ctypes.byref(ms)), h)
@@ -262,6 +288,7 @@ class Context:
         self.h = ara_create(catalog_size, device, prec, stream, rank, world, nccl_id, mode, chunk_trials,
                             l2_persist, rmode)
         self.n_layers = 0
+        self.n_rows = 0
         self.n_trials = 0
 
     def close(self):
@@ -301,7 +328,21 @@ class Context:
     def run(self, layers, ylt=None, lossy=None) -> dict:
         st = ara_run(self.h, layers, ylt, lossy)
         self.n_layers = len(layers)
+        self.n_rows = len(layers) + 1
         return st
+
+    def run_portfolio(self, programs, ylt=None, lossy=None) -> dict:
+        st = ara_run_portfolio(self.h, programs, ylt, lossy)
+        self.n_layers = sum(len(p) for p in programs)
+        self.n_rows = self.n_layers + len(programs) + 1
+        return st
+
+    def run_portfolio_host(self, programs, with_lossy: bool = True):
+        L = sum(len(p) for p in programs)
+        ylt = np.empty((L + len(programs) + 1, self.n_trials), dtype=np.float64)
+        lossy = np.empty((L, self.n_trials), dtype=np.uint32) if with_lossy else None
+        st = self.run_portfolio(programs, ylt, lossy)
+        return ylt, lossy, st
 
     def run_host(self, layers, with_lossy: bool = True, n_local: Optional[int] = None):
         """Convenience: YLT [(L+1)][T] and lossy [L][T_local] into new host arrays."""
@@ -313,10 +354,10 @@ class Context:
         return ylt, lossy, st
 
     def metrics(self, return_periods):
-        return ara_metrics(self.h, self.n_layers, return_periods)
+        return ara_metrics(self.h, self.n_rows, return_periods)
 
 
 __all__ = ["Context", "AraError", "ara_create", "ara_destroy", "ara_load_elts", "ara_set_elt_terms",
            "ara_load_yet", "ara_run", "ara_metrics", "ara_partition", "ara_return_period_rank",
-           "ara_nccl_unique_id", "ara_load_yet_packed", "ara_pack_ids", "ara_packed_words", "bits_for_catalog",
+           "ara_nccl_unique_id", "ara_load_yet_packed", "ara_run_portfolio", "ara_pack_ids", "ara_packed_words", "bits_for_catalog",
            "status_string", "version", "EXPORTED"]

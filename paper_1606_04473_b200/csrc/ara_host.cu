@@ -651,6 +651,40 @@ struct Group {
 
 }  // namespace
 
+namespace {
+
+// A layer as the run sees it: its ELT span [elt_begin, elt_end) and, for
+// ara_run_portfolio, the explicit ascending member list (null = the whole span).
+struct LayerI {
+    uint32_t elt_begin, elt_end;
+    double occ_retention, occ_limit, agg_retention, agg_limit;
+    const uint32_t* list;
+    uint32_t n_list;
+    bool member(uint32_t col) const {
+        if (col < elt_begin || col >= elt_end) return false;
+        if (!list) return true;
+        uint32_t lo = 0, hi = n_list;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (list[mid] == col) return true;
+            if (list[mid] < col) lo = mid + 1; else hi = mid;
+        }
+        return false;
+    }
+    uint32_t n_members() const { return list ? n_list : elt_end - elt_begin; }
+};
+
+ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint32_t n_programs,
+                    const uint32_t* program_layers, double* ylt, uint32_t* lossy, ara_run_stats* stats);
+
+ara_status check_layer_terms(ara_ctx* ctx, uint32_t l, double occr, double occl, double aggr, double aggl) {
+    if (!valid_retention(occr) || !valid_retention(aggr) || !valid_limit(occl) || !valid_limit(aggl))
+        return fail(ctx, ARA_ERR_DOMAIN, "layer %u terms: retentions >= 0 finite, limits > 0", l);
+    return ARA_OK;
+}
+
+}  // namespace
+
 extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* layers, double* ylt,
                               uint32_t* lossy, ara_run_stats* stats) {
     if (!ctx) return ARA_ERR_INVALID_ARG;
@@ -660,15 +694,59 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
     if (n_layers == 0 || n_layers > ARA_MAX_LAYERS || !layers)
         return fail(ctx, ARA_ERR_INVALID_ARG, "n_layers must be in [1, %d]", ARA_MAX_LAYERS);
     if (classify(layers) == Mem::Device) return fail(ctx, ARA_ERR_INVALID_ARG, "layers must be host memory");
+    std::vector<LayerI> li(n_layers);
     for (uint32_t l = 0; l < n_layers; ++l) {
         const ara_layer& L = layers[l];
         if (L.elt_begin >= L.elt_end || L.elt_end > ctx->n_elts)
             return fail(ctx, ARA_ERR_INVALID_ARG, "layer %u ELT range [%u,%u) invalid for %u ELTs", l, L.elt_begin,
                         L.elt_end, ctx->n_elts);
-        if (!valid_retention(L.occ_retention) || !valid_retention(L.agg_retention) || !valid_limit(L.occ_limit) ||
-            !valid_limit(L.agg_limit))
-            return fail(ctx, ARA_ERR_DOMAIN, "layer %u terms: retentions >= 0 finite, limits > 0", l);
+        ara_status st = check_layer_terms(ctx, l, L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit);
+        if (st != ARA_OK) return st;
+        li[l] = LayerI{L.elt_begin, L.elt_end, L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit, nullptr, 0};
     }
+    return run_impl(ctx, n_layers, li.data(), 0, nullptr, ylt, lossy, stats);
+}
+
+extern "C" ara_status ara_run_portfolio(ara_ctx* ctx, uint32_t n_programs, const uint32_t* program_layers,
+                                        uint32_t n_layers, const ara_layer_list* layers, double* ylt,
+                                        uint32_t* lossy, ara_run_stats* stats) {
+    if (!ctx) return ARA_ERR_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->d_table || ctx->n_elts == 0) return fail(ctx, ARA_ERR_STATE, "ara_load_elts has not succeeded");
+    if (!ctx->yet_loaded) return fail(ctx, ARA_ERR_STATE, "ara_load_yet has not succeeded");
+    if (n_layers == 0 || n_layers > ARA_MAX_LAYERS || !layers)
+        return fail(ctx, ARA_ERR_INVALID_ARG, "n_layers must be in [1, %d]", ARA_MAX_LAYERS);
+    if (n_programs > ARA_MAX_PROGRAMS || (n_programs && !program_layers))
+        return fail(ctx, ARA_ERR_INVALID_ARG, "n_programs must be in [0, %d] with program_layers", ARA_MAX_PROGRAMS);
+    if (n_programs) {
+        if (program_layers[0] != 0 || program_layers[n_programs] != n_layers)
+            return fail(ctx, ARA_ERR_INVALID_ARG, "program_layers must run from 0 to n_layers");
+        for (uint32_t q = 0; q < n_programs; ++q)
+            if (program_layers[q + 1] <= program_layers[q])
+                return fail(ctx, ARA_ERR_INVALID_ARG, "program %u has no layers", q);
+    }
+    std::vector<LayerI> li(n_layers);
+    for (uint32_t l = 0; l < n_layers; ++l) {
+        const ara_layer_list& L = layers[l];
+        if (L.n_elts == 0 || !L.elts) return fail(ctx, ARA_ERR_INVALID_ARG, "layer %u has no ELTs", l);
+        for (uint32_t q = 0; q < L.n_elts; ++q) {
+            if (L.elts[q] >= ctx->n_elts)
+                return fail(ctx, ARA_ERR_INVALID_ARG, "layer %u ELT %u not loaded", l, L.elts[q]);
+            if (q && L.elts[q] <= L.elts[q - 1])
+                return fail(ctx, ARA_ERR_INVALID_ARG, "layer %u ELT list not strictly ascending", l);
+        }
+        ara_status st = check_layer_terms(ctx, l, L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit);
+        if (st != ARA_OK) return st;
+        li[l] = LayerI{L.elts[0], L.elts[L.n_elts - 1] + 1, L.occ_retention, L.occ_limit, L.agg_retention,
+                       L.agg_limit, L.elts, L.n_elts};
+    }
+    return run_impl(ctx, n_layers, li.data(), n_programs, program_layers, ylt, lossy, stats);
+}
+
+namespace {
+
+ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint32_t n_programs,
+                    const uint32_t* program_layers, double* ylt, uint32_t* lossy, ara_run_stats* stats) {
     const uint32_t world = (uint32_t)ctx->world;
     const uint64_t T_local = ctx->T_local, T_global = ctx->T_global;
 
@@ -694,7 +772,7 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
     const uint32_t eps = fp32 ? 8 : 4;   // elements per 32-B sector
     const uint64_t Tpad = world > 1 ? (T_global + world - 1) / world : T_local;
     const uint64_t ld = world > 1 ? Tpad : (T_local ? T_local : 1);
-    const uint32_t rows = n_layers + 1;
+    const uint32_t rows = n_layers + n_programs + 1;   // layers, programs, portfolio
 
     ara_status st = ensure(ctx, ctx->d_ylt_local, ctx->ylt_local_cap, (size_t)rows * ld);
     if (st != ARA_OK) return st;
@@ -816,14 +894,13 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
     base.lossy = d_lossy;
     base.err = ctx->d_err;
     base.pf_sectors = ctx->pf_sectors;
-    base.portfolio_row = n_layers;
+    base.portfolio_row = n_layers + n_programs;
     uint32_t launches = 0;
-    double2* d_cterm = nullptr;
-    std::vector<double2> wide_terms;
+    std::vector<void*> wide_free;   // per-run column lists / terms of wide layers
     // per-group window setup shared by the direct and fold launches
     auto setup_window = [&](const Group& g, TrialParams& p) {
         for (uint32_t q = 0; q < g.nl; ++q) {
-            const ara_layer& L = layers[g.l0 + q];
+            const LayerI& L = layers[g.l0 + q];
             p.lw[q] = {L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit};
         }
         for (uint32_t sct = 0; sct < (uint32_t)kMaxSec; ++sct) {
@@ -831,10 +908,10 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
             p.sec_off[sct] = (uint64_t)(qq / spb) * geo.block_elems + (uint64_t)(qq % spb) * eps;
         }
         for (uint32_t q = 0; q < g.nl; ++q) {
-            const ara_layer& L = layers[g.l0 + q];
+            const LayerI& L = layers[g.l0 + q];
             for (uint32_t w = 0; w < (uint32_t)kMaxWin; ++w) {
                 const uint32_t col = g.q0 * eps + w;
-                if (w / eps < g.nsec && col >= L.elt_begin && col < L.elt_end)
+                if (w / eps < g.nsec && L.member(col))
                     p.term[q][w] = make_double2(ctx->terms[col].deductible, ctx->terms[col].limit);
                 else
                     p.term[q][w] = make_double2(INFINITY, INFINITY);   // contributes exactly +0
@@ -874,7 +951,7 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
                 p.ylt_row0 = fc * nlc;
                 p.portfolio_mode = fc == 0 ? 0 : 1;
                 for (uint32_t q = 0; q < p.n_layers; ++q) {
-                    const ara_layer& L = layers[fc * nlc + q];
+                    const LayerI& L = layers[fc * nlc + q];
                     p.lw[q] = {L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit};
                 }
                 p.fold = ctx->d_fold + (uint64_t)fc * fold_rows * nlc;
@@ -893,32 +970,38 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
             p.ylt_row0 = g.l0;
             p.portfolio_mode = gi == 0 ? 0 : 1;
             for (uint32_t q = 0; q < g.nl; ++q) {
-                const ara_layer& L = layers[g.l0 + q];
+                const LayerI& L = layers[g.l0 + q];
                 p.lw[q] = {L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit};
             }
             if (g.wide) {
-                const ara_layer& L = layers[g.l0];
-                if (!d_cterm) {
-                    wide_terms.resize(ctx->n_elts);
-                    for (uint32_t j = 0; j < ctx->n_elts; ++j)
-                        wide_terms[j] = make_double2(ctx->terms[j].deductible, ctx->terms[j].limit);
-                    CK(cudaMallocAsync(&d_cterm, ctx->n_elts * sizeof(double2), s));
-                    CK(cudaMemcpyAsync(d_cterm, wide_terms.data(), ctx->n_elts * sizeof(double2),
-                                       cudaMemcpyHostToDevice, s));
-                }
+                const LayerI& L = layers[g.l0];
+                std::vector<uint32_t> wcols;
+                std::vector<double2> wterms;
+                for (uint32_t col = L.elt_begin; col < L.elt_end; ++col)
+                    if (L.member(col)) {
+                        wcols.push_back(col);
+                        wterms.push_back(make_double2(ctx->terms[col].deductible, ctx->terms[col].limit));
+                    }
+                uint32_t* d_wc = nullptr;
+                double2* d_wt = nullptr;
+                CK(cudaMallocAsync(&d_wc, wcols.size() * sizeof(uint32_t), s));
+                CK(cudaMallocAsync(&d_wt, wterms.size() * sizeof(double2), s));
+                CK(cudaMemcpyAsync(d_wc, wcols.data(), wcols.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+                CK(cudaMemcpyAsync(d_wt, wterms.data(), wterms.size() * sizeof(double2), cudaMemcpyHostToDevice, s));
+                wide_free.push_back(d_wc);
+                wide_free.push_back(d_wt);
                 const int grid = trial_kernel_grid(fp32, g.nsec, 1, 0);
-                CK(launch_trials_wide(p, fp32, d_cterm + L.elt_begin, L.elt_begin, L.elt_end - L.elt_begin, grid,
-                                      s));
+                CK(launch_trials_wide(p, fp32, d_wc, d_wt, (uint32_t)wcols.size(), grid, s));
             } else {
                 for (uint32_t sct = 0; sct < (uint32_t)kMaxSec; ++sct) {
                     const uint32_t qq = g.q0 + (sct < g.nsec ? sct : 0);
                     p.sec_off[sct] = (uint64_t)(qq / spb) * geo.block_elems + (uint64_t)(qq % spb) * eps;
                 }
                 for (uint32_t q = 0; q < g.nl; ++q) {
-                    const ara_layer& L = layers[g.l0 + q];
+                    const LayerI& L = layers[g.l0 + q];
                     for (uint32_t w = 0; w < (uint32_t)kMaxWin; ++w) {
                         const uint32_t col = g.q0 * eps + w;
-                        if (w / eps < g.nsec && col >= L.elt_begin && col < L.elt_end)
+                        if (w / eps < g.nsec && L.member(col))
                             p.term[q][w] = make_double2(ctx->terms[col].deductible, ctx->terms[col].limit);
                         else
                             p.term[q][w] = make_double2(INFINITY, INFINITY);   // contributes exactly +0
@@ -966,8 +1049,16 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
             ++launches;
         }
     }
+    if (n_programs) {   // program rows from the layer rows (Alg. 1 l.1)
+        uint32_t* d_pl = nullptr;
+        CK(cudaMallocAsync(&d_pl, (n_programs + 1) * sizeof(uint32_t), s));
+        CK(cudaMemcpyAsync(d_pl, program_layers, (n_programs + 1) * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+        CK(launch_program_sums(ctx->d_ylt_local, ld, T_local, n_programs, d_pl, n_layers, s));
+        wide_free.push_back(d_pl);
+        ++launches;
+    }
     CK(cudaEventRecord(ctx->ev[2], s));
-    if (d_cterm) CK(cudaFreeAsync(d_cterm, s));
+    for (void* q : wide_free) CK(cudaFreeAsync(q, s));
     for (auto e : chunk_ev) cudaEventDestroy(e);   // safe: destruction defers until complete
     if (stream_in) {
         ctx->chunked_pending = false;   // later runs reuse the device copy
@@ -1041,10 +1132,11 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
         return st;
     }
     ctx->last_layers = n_layers;
+    ctx->last_rows = rows;
     if (stats) {
         const uint64_t nev = T_local ? ctx->h_small[2] - ctx->h_small[1] : 0;
         uint64_t lookups = 0;
-        for (uint32_t l = 0; l < n_layers; ++l) lookups += nev * (layers[l].elt_end - layers[l].elt_begin);
+        for (uint32_t l = 0; l < n_layers; ++l) lookups += nev * layers[l].n_members();
         stats->n_trials_local = T_local;
         stats->n_events_local = nev;
         stats->n_lookups_local = lookups;
@@ -1057,6 +1149,8 @@ extern "C" ara_status ara_run(ara_ctx* ctx, uint32_t n_layers, const ara_layer* 
     }
     return ARA_OK;
 }
+
+}  // namespace
 
 // ============================================================ metrics
 extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* return_periods, uint64_t* k,
@@ -1072,7 +1166,7 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
         if (ara_return_period_rank(T, return_periods[r], &hk[r]) != ARA_OK)
             return fail(ctx, ARA_ERR_DOMAIN, "return period %g outside [1, %llu]", return_periods[r],
                         (unsigned long long)T);
-    const uint32_t rows = ctx->last_layers + 1;
+    const uint32_t rows = ctx->last_rows;
     const double* d_y;
     uint64_t ld;
     if (ctx->world > 1) {

@@ -109,8 +109,10 @@ cudaError_t launch_fold(const TrialParams& p, int fp32, uint32_t nsec, cudaStrea
 cudaError_t launch_unpack(const uint32_t* packed, uint32_t bits, uint64_t e0, uint64_t e1, uint32_t* ids,
                           cudaStream_t s);
 cudaError_t launch_trials_folded(const TrialParams& p, int grid_mult_x100, cudaStream_t s);
-cudaError_t launch_trials_wide(const TrialParams& p, int fp32, const double2* d_cterm, uint32_t col0,
+cudaError_t launch_trials_wide(const TrialParams& p, int fp32, const uint32_t* d_cols, const double2* d_cterm,
                                uint32_t ncol, int grid, cudaStream_t s);
+cudaError_t launch_program_sums(double* ylt, uint64_t ld, uint64_t t_local, uint32_t n_programs,
+                                const uint32_t* d_program_layers, uint32_t n_layers, cudaStream_t s);
 
 // metrics: radix select over the [rows][T] YLT (device), fixed-order tail sums
 struct MetricsScratch {
@@ -182,6 +184,7 @@ struct ara_ctx {
 
     // YLT
     uint32_t last_layers = 0;          // layers of the last run (0 = none)
+    uint32_t last_rows = 0;            // YLT rows of the last run (layers + programs + portfolio)
     double* d_ylt_local = nullptr;     // [(L+1)][T_local]
     size_t ylt_local_cap = 0;
     double* d_ylt_gather = nullptr;    // world>1: [(L+1)][world][Tpad]

@@ -720,8 +720,8 @@ __global__ void __launch_bounds__(kThreads, 1) trial_kernel_tma(const __grid_con
 // one layer per launch, scalar loads through the column-block address map.
 template <typename TV>
 __global__ void __launch_bounds__(kThreads) trial_kernel_wide(const __grid_constant__ TrialParams p,
-                                                              const double2* __restrict__ cterm,
-                                                              uint32_t col0, uint32_t ncol) {
+                                                              const uint32_t* __restrict__ cols,
+                                                              const double2* __restrict__ cterm, uint32_t ncol) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t gw = (uint64_t(blockIdx.x) * kThreads + threadIdx.x) >> 5;
     const uint64_t nw = (uint64_t(gridDim.x) * kThreads) >> 5;
@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(kThreads) trial_kernel_wide(const __grid_const
             }
             double le = 0.0;
             for (uint32_t c = 0; c < ncol; ++c) {
-                const uint32_t j = col0 + c;
+                const uint32_t j = __ldg(cols + c);
                 const double2 tc = cterm[c];
                 const double x = (double)__ldg(tab + (uint64_t)(j / p.row_stride) * p.block_stride +
                                                (uint64_t)v * p.row_stride + j % p.row_stride);
@@ -1074,15 +1074,39 @@ cudaError_t launch_trials_folded(const TrialParams& p, int grid_mult_x100, cudaS
     return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kThreads), args, 0, s);
 }
 
-cudaError_t launch_trials_wide(const TrialParams& p, int fp32, const double2* d_cterm, uint32_t col0, uint32_t ncol,
-                               int grid, cudaStream_t s) {
+// Program rows (Alg. 1 l.1): Y_prog[q][t] = sum of the program's layer rows, in
+// layer order, from +0 (the oracle's sequential order).
+__global__ void __launch_bounds__(256) program_sum_kernel(double* __restrict__ ylt, uint64_t ld, uint64_t t_local,
+                                                          uint32_t n_programs, const uint32_t* __restrict__ pl,
+                                                          uint32_t n_layers) {
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < t_local;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        for (uint32_t q = 0; q < n_programs; ++q) {
+            double acc = 0.0;
+            for (uint32_t l = __ldg(pl + q); l < __ldg(pl + q + 1); ++l) acc = __dadd_rn(acc, ylt[(uint64_t)l * ld + t]);
+            ylt[(uint64_t)(n_layers + q) * ld + t] = acc;
+        }
+    }
+}
+
+cudaError_t launch_program_sums(double* ylt, uint64_t ld, uint64_t t_local, uint32_t n_programs,
+                                const uint32_t* d_program_layers, uint32_t n_layers, cudaStream_t s) {
+    if (!n_programs || !t_local) return cudaSuccess;
+    uint64_t blocks = (t_local + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    program_sum_kernel<<<(unsigned)blocks, 256, 0, s>>>(ylt, ld, t_local, n_programs, d_program_layers, n_layers);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_trials_wide(const TrialParams& p, int fp32, const uint32_t* d_cols, const double2* d_cterm,
+                               uint32_t ncol, int grid, cudaStream_t s) {
     if (p.t_end <= p.t_begin) return cudaSuccess;
     const uint64_t need = ((p.t_end - p.t_begin) * 32 + kThreads - 1) / kThreads;
     const int g = (int)((uint64_t)grid < need ? (uint64_t)grid : need);
     if (fp32)
-        trial_kernel_wide<float><<<g, kThreads, 0, s>>>(p, d_cterm, col0, ncol);
+        trial_kernel_wide<float><<<g, kThreads, 0, s>>>(p, d_cols, d_cterm, ncol);
     else
-        trial_kernel_wide<double><<<g, kThreads, 0, s>>>(p, d_cterm, col0, ncol);
+        trial_kernel_wide<double><<<g, kThreads, 0, s>>>(p, d_cols, d_cterm, ncol);
     return cudaGetLastError();
 }
 

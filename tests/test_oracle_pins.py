@@ -332,3 +332,24 @@ def test_aggregate_terms_special_case():
     y = oracle.ara(off, ids, e, w.catalog, np.zeros(E), np.full(E, INF),
                    [(list(range(E)), 0.0, INF, aggr, aggl)])["ylt"][0]
     assert np.array_equal(y, np.minimum(np.maximum(raw - aggr, 0.0), aggl))
+
+
+def test_programs_closed_forms():
+    """Programs: a program of one layer is that layer's row; on
+    integer-valued data the program rows sum (exactly) to the portfolio of all
+    layers; malformed program lists are rejected.  Catches an off-by-one layer
+    range or a program summing the wrong rows."""
+    w, off, ids, e = _small(int_cap=2.0 ** 31)
+    d, li = w.elt_terms()
+    lay = [([0, 1, 2], 2.5e4, 5e5, 6.5e5, 2.5e6), ([1], 0.0, INF, 0.0, INF), ([0, 2], 1e4, 1e5, 0.0, 1e6),
+           ([2], 5e3, INF, 1e5, INF)]
+    r = oracle.ara(off, ids, e, w.catalog, d, li, lay)
+    single = oracle.programs(r["ylt"], [0, 1, 2, 3, 4])
+    assert np.array_equal(single, r["ylt"])
+    two = oracle.programs(r["ylt"], [0, 1, 4])
+    assert np.array_equal(two[0], r["ylt"][0])
+    assert np.array_equal(two[0] + two[1], r["portfolio"])
+    assert np.array_equal(two[1], r["ylt"][1] + r["ylt"][2] + r["ylt"][3])
+    for bad in ([0, 2, 2, 4], [1, 4], [0, 3]):
+        with pytest.raises(ValueError):
+            oracle.programs(r["ylt"], bad)

@@ -291,3 +291,39 @@ def test_packed_out_of_range_id_reported(cuda):
         with pytest.raises(ara.AraError) as e:
             ctx.run(w.layers)
         assert e.value.status == ara.ARA_ERR_OUT_OF_RANGE
+
+
+@pytest.mark.parametrize("run_mode", ["direct", "fold"])
+def test_portfolio_programs_and_explicit_elt_lists(cuda, run_mode):
+    """F4: programs of layers with explicit (non-contiguous, ascending) ELT
+    lists, including a >8-sector list (generic kernel); YLT rows = layers,
+    programs, portfolio; metrics over every row."""
+    w = synth.get_config("tiny").with_(n_elts=48, catalog=4000, rho=0.2, n_trials=800, nmin=0, nmax=200)
+    off, ids, elts = make_inputs(w)
+    d, li = w.elt_terms()
+    progs = [
+        [([0, 2, 5, 9, 14], 2.5e4, 5e5, 6.5e5, 2.5e6), ([1, 3], 0.0, INF, 0.0, INF)],
+        [([20, 21, 22, 23, 24, 25, 26, 27, 28, 29, 30, 31, 32, 33, 34, 35], 1e4, 1e6, 1e5, 8e6)],
+        [([4, 40, 47], 5e4, 2e5, 2e5, INF), ([6, 7, 8], 0.0, 3e5, 0.0, 5e6), (list(range(0, 48, 2)), 1e5, 1e6, 3e5, INF)],
+    ]
+    flat = [L for p in progs for L in p]
+    orc = oracle.ara(off, ids, oracle.Elts(*elts), w.catalog, d, li, flat, lookup="dense")
+    pl = np.cumsum([0] + [len(p) for p in progs])
+    orc_prog = oracle.programs(orc["ylt"], pl)
+    from paper_1606_04473_b200 import ara
+    with ara.Context(w.catalog, run_mode=run_mode) as ctx:
+        ctx.load_elts(*elts, terms=(d, li))
+        ctx.load_yet(w.n_trials, 0, off, ids)
+        ylt, lossy, st = ctx.run_portfolio_host(progs)
+        k, pml, tvar, _ = ctx.metrics((2, 10, 100))
+    L, P = len(flat), len(progs)
+    assert ylt.shape == (L + P + 1, w.n_trials) and pml.shape == (L + P + 1, 3)
+    tol = RTOL * np.maximum(orc["scale"], 1.0)
+    assert (np.abs(ylt[:L] - orc["ylt"]) <= tol).all()
+    assert np.array_equal(lossy, orc["lossy"])
+    for q in range(P):
+        assert (np.abs(ylt[L + q] - orc_prog[q]) <= tol[pl[q]:pl[q + 1]].sum(axis=0)).all()
+    assert (np.abs(ylt[L + P] - orc["portfolio"]) <= tol.sum(axis=0)).all()
+    for r in range(L + P + 1):
+        kk, p_o, _ = oracle.metrics(ylt[r], (2, 10, 100))
+        assert np.array_equal(p_o, pml[r]) and np.array_equal(kk, k)
