@@ -223,11 +223,30 @@ def reference_arm(a, rank, world):
             "cpu_baseline": {"value": tps, "unit": "trials/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": tps, "unit": "trials/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "host": host_info()}
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------ our arm
+_JSON_FD = None
+
+
+def emit(line: dict):
+    """The one stdout line of the bench contract.  Library/NCCL chatter written
+    to fd 1 by C code is routed to stderr (see main), so this write is the only
+    thing on the original stdout."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is not None:
+        os.write(_JSON_FD, data)
+    else:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+
+
 def main():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)          # anything else printed to fd 1 (NCCL version banners, ...) goes to stderr
     a = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -296,16 +315,26 @@ def main():
                       nccl_id=new_nccl_id(), l2_persist=a.l2_persist, run_mode=a.mode)
     kern_ms, ag_ms, met_ms, launches = [], [], [], []
 
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    part_ms = []
+
     def step(record):
+        evs[0].record(stream)
         ctx.load_elts(d_eo, d_ev, d_ls, terms, n_elts=w.n_elts)          # a0 (+ NVLink broadcast)
+        evs[1].record(stream)
         ctx.load_yet(T, first, d_off, d_ids)                             # a1 (device: borrowed)
+        evs[2].record(stream)
         st = ctx.run(w.layers)                                           # a2-a9
+        evs[3].record(stream)
         k, pml, tvar, mms = ctx.metrics(R)                               # a10
+        evs[4].record(stream)
         if record:
             kern_ms.append(st["kernel_ms"])
             ag_ms.append(st["allgather_ms"])
             met_ms.append(mms)
             launches.append(st["n_kernel_launches"])
+            evs[4].synchronize()
+            part_ms.append([evs[i].elapsed_time(evs[i + 1]) for i in range(4)])
         return st, pml, tvar
 
     clocks = ClockSampler(local)
@@ -430,12 +459,14 @@ def main():
                          "kernel": "ara::trial_kernel" if a.mode == "direct" else "ara::fold_kernel+trial_fold_kernel",
                          "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
             "breakdown_ms": {"ara_kernel": k_ms, "allgather": float(np.mean(ag_ms)), "metrics": float(np.mean(met_ms)),
-                             "step": ms},
+                             "step": ms,
+                             "calls": {k: float(np.median([p[i] for p in part_ms]))
+                                       for i, k in enumerate(("load_elts", "load_yet", "run", "metrics"))}},
             "gpu_launches": int(a.steps * (2 + np.mean(launches) + 10)),
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
             "host": host_info(), "gen_seconds": gen_s,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
 

@@ -80,23 +80,35 @@ __global__ void __launch_bounds__(256) radix_pass_kernel(const __grid_constant__
     __syncthreads();
     const uint32_t nu = s_nu;
     const double* y = P.ylt + (uint64_t)row * P.ld;
-    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < P.T;
-         i0 += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = i0 + lane;
-        const bool valid = i < P.T;
-        const uint64_t key = valid ? key_of(y[i]) : 0ull;
-        const uint32_t d = (uint32_t)(key >> shift) & 255u;
-        uint32_t which = 0xffffffffu;
-        if (valid) {
-            if (pass == 0) which = 0;
-            else
-                for (uint32_t u = 0; u < nu; ++u)
-                    if (((key ^ s_upre[u]) >> (shift + 8)) == 0) which = u;
+    // Keys are loaded KB at a time per lane (independent loads in flight),
+    // then binned.
+    constexpr int KB = 8;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < P.T; i0 += stride * KB) {
+        uint64_t keys[KB];
+#pragma unroll
+        for (int q = 0; q < KB; ++q) {
+            const uint64_t i = i0 + q * stride + lane;
+            keys[q] = i < P.T ? key_of(__ldcg(y + i)) : ~0ull;   // ~0: not a key (NaN pattern)
         }
-        const uint32_t tag = which == 0xffffffffu ? 0xffffffffu : (which << 8) | d;
-        const unsigned peers = __match_any_sync(0xffffffffu, tag);
-        if (tag != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
-            atomicAdd(&sh[s_ulist[which] * 256 + d], (uint32_t)__popc(peers));
+#pragma unroll
+        for (int q = 0; q < KB; ++q) {
+            if (i0 + q * stride >= P.T) break;   // warp-uniform
+            const uint64_t key = keys[q];
+            const bool valid = key != ~0ull;
+            const uint32_t d = (uint32_t)(key >> shift) & 255u;
+            uint32_t which = 0xffffffffu;
+            if (valid) {
+                if (pass == 0) which = 0;
+                else
+                    for (uint32_t u = 0; u < nu; ++u)
+                        if (((key ^ s_upre[u]) >> (shift + 8)) == 0) which = u;
+            }
+            const uint32_t tag = which == 0xffffffffu ? 0xffffffffu : (which << 8) | d;
+            const unsigned peers = __match_any_sync(0xffffffffu, tag);
+            if (tag != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
+                atomicAdd(&sh[s_ulist[which] * 256 + d], (uint32_t)__popc(peers));
+        }
     }
     __syncthreads();
     uint32_t* gh = P.hist + (uint64_t)row * n_rp * 256;
@@ -163,14 +175,22 @@ __global__ void __launch_bounds__(256) tail_kernel(const __grid_constant__ MPara
     __shared__ uint32_t s_last;
     const uint32_t row = blockIdx.y, n_rp = P.n_rp;
     const double* y = P.ylt + (uint64_t)row * P.ld;
+    constexpr int KB = 8;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint32_t r = 0; r < n_rp; ++r) {
         const double v = __longlong_as_double((long long)P.prefix[row * n_rp + r]);
         double s = 0.0;
         uint64_t c = 0;
-        for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < P.T;
-             i += (uint64_t)gridDim.x * blockDim.x) {
-            const double x = y[i] + 0.0;
-            if (x > v) { s = __dadd_rn(s, x); ++c; }
+        for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < P.T; i0 += stride * KB) {
+            double xs[KB];
+#pragma unroll
+            for (int q = 0; q < KB; ++q) {
+                const uint64_t i = i0 + q * stride;
+                xs[q] = i < P.T ? __ldcg(y + i) + 0.0 : -1.0;
+            }
+#pragma unroll
+            for (int q = 0; q < KB; ++q)   // fixed order per thread: deterministic
+                if (xs[q] > v) { s = __dadd_rn(s, xs[q]); ++c; }
         }
         s_sum[threadIdx.x] = s;
         s_cnt[threadIdx.x] = c;
