@@ -502,7 +502,9 @@ ara_status load_yet_impl(ara_ctx* ctx, uint64_t n_trials_global, uint64_t first_
                     (unsigned long long)n_trials_global);
     if (!trial_offsets) return fail(ctx, ARA_ERR_INVALID_ARG, "trial_offsets is NULL");
     if (bits > 32) return fail(ctx, ARA_ERR_INVALID_ARG, "bits must be in [1, 32]");
-    CK(cudaStreamSynchronize(ctx->stream));   // a previous run may still read the old YET
+    // Later work on the stream is ordered after any run still reading the old
+    // YET; only unregistering a host range we pinned needs the copies done.
+    if (ctx->h_registered) CK(cudaStreamSynchronize(ctx->copy_stream));
     release_yet(ctx);
 
     const Mem mo = classify(trial_offsets);
@@ -576,7 +578,10 @@ ara_status load_yet_impl(ara_ctx* ctx, uint64_t n_trials_global, uint64_t first_
     }
     ctx->pack_bits = bits;
     ctx->chunked_pending = chunked && (ctx->h_off || ctx->h_ids || ctx->h_packed);
-    if (!ctx->chunked_pending) CK(cudaStreamSynchronize(ctx->stream));
+    // Host sources are released to the caller on return (ALL_AT_ONCE copies
+    // must be complete); device-resident inputs need no sync.
+    if (!ctx->chunked_pending && (mo != Mem::Device || (mi != Mem::Device && n_ev)))
+        CK(cudaStreamSynchronize(ctx->stream));
     ctx->T_global = n_trials_global;
     ctx->first = first_trial;
     ctx->T_local = n_trials_local;
