@@ -168,6 +168,16 @@ def load_peaks():
         return {}
 
 
+def kernel_name(a):
+    """The ARA kernel the library picks by default (ara_host.cu, 'Kernel choice')."""
+    if a.mode != "direct":
+        return "ara::fold_kernel+trial_fold_kernel"
+    v = os.environ.get("ARA_KERNEL")
+    if v is not None and int(v) >= 0:
+        return f"ara::trial_kernel (ARA_KERNEL={v})"
+    return "ara::trial_kernel_co" if a.precision == "f64" else "ara::trial_kernel"
+
+
 def load_traffic(w, precision):
     """dram bytes per launch of the ARA kernel from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ara_kernel_traffic.json")
@@ -456,8 +466,12 @@ def main():
             "lookups_per_sec": lookups / (ms / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic if a.mode == "direct" else None,
-                         "kernel": "ara::trial_kernel" if a.mode == "direct" else "ara::fold_kernel+trial_fold_kernel",
-                         "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg, "peak_source": peak_src},
+                         "kernel": kernel_name(a),
+                         "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
+                         # algorithmic bytes count every gathered row, including the ones L2
+                         # serves, so frac can exceed 1; the DRAM-level figure is traffic / time
+                         "dram_achieved": (traffic / (k_ms * 1e6)) if (traffic and a.mode == "direct") else None,
+                         "dram_frac": (traffic / (k_ms * 1e6) / peak) if (traffic and a.mode == "direct") else None},
             "breakdown_ms": {"ara_kernel": k_ms, "allgather": float(np.mean(ag_ms)), "metrics": float(np.mean(met_ms)),
                              "step": ms,
                              "calls": {k: float(np.median([p[i] for p in part_ms]))

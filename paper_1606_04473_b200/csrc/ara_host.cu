@@ -229,6 +229,7 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
     if (const char* v = getenv("ARA_GRID_MULT")) ctx->grid_mult = atof(v);
     if (const char* v = getenv("ARA_KERNEL")) ctx->kernel_variant = atoi(v);
     if (const char* v = getenv("ARA_PFN")) ctx->pf_sectors = atoi(v);
+    if (const char* v = getenv("ARA_NO_SKIP")) ctx->no_skip = atoi(v) != 0;
     if (const char* v = getenv("ARA_BATCH")) ctx->batch = (uint32_t)atoi(v) ? (uint32_t)atoi(v) : 4u;
     auto bail = [&](ara_status st) {
         ara_destroy(ctx);
@@ -398,6 +399,9 @@ ara_status densify_local(ara_ctx* ctx, uint32_t n_elts, uint64_t nrec, const Spa
                       ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    ctx->occ_rows.assign(ctx->geo.n_blocks, 0u);
+    CK(cudaMemcpy(ctx->occ_rows.data(), static_cast<const char*>(ctx->d_table) + ctx->geo.occ_off,
+                  ctx->geo.n_blocks * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     return device_errors(ctx, (uint32_t)(ctx->h_small[0] & 0xffffffffu));
 }
 
@@ -912,6 +916,17 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
             const uint32_t qq = g.q0 + (sct < g.nsec ? sct : 0);
             p.sec_off[sct] = (uint64_t)(qq / spb) * geo.block_elems + (uint64_t)(qq % spb) * eps;
         }
+        // Row-occupancy bitmap of the window's column block (windows inside one
+        // block), used when at most half of the block's rows are occupied: the
+        // paper's ELTs hold 10k-30k losses over a catalogue of millions,
+        // so most lookups hit all-zero rows; on dense tables the extra occupancy
+        // read would only cost time (measured: +7 % at 100 % occupancy).
+        const uint32_t blk = g.q0 / spb;
+        const bool sparse = blk < ctx->occ_rows.size() && 2ull * ctx->occ_rows[blk] <= (uint64_t)ctx->catalog + 1;
+        p.bm = (g.nsec <= spb && (g.q0 % spb) + g.nsec <= spb && !ctx->no_skip && sparse)
+                   ? reinterpret_cast<const uint32_t*>(static_cast<const char*>(ctx->d_table) + geo.bm_off) +
+                         (uint64_t)(g.q0 / spb) * geo.bm_words
+                   : nullptr;
         for (uint32_t q = 0; q < g.nl; ++q) {
             const LayerI& L = layers[g.l0 + q];
             for (uint32_t w = 0; w < (uint32_t)kMaxWin; ++w) {
@@ -998,28 +1013,16 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 const int grid = trial_kernel_grid(fp32, g.nsec, 1, 0);
                 CK(launch_trials_wide(p, fp32, d_wc, d_wt, (uint32_t)wcols.size(), grid, s));
             } else {
-                for (uint32_t sct = 0; sct < (uint32_t)kMaxSec; ++sct) {
-                    const uint32_t qq = g.q0 + (sct < g.nsec ? sct : 0);
-                    p.sec_off[sct] = (uint64_t)(qq / spb) * geo.block_elems + (uint64_t)(qq % spb) * eps;
-                }
-                for (uint32_t q = 0; q < g.nl; ++q) {
-                    const LayerI& L = layers[g.l0 + q];
-                    for (uint32_t w = 0; w < (uint32_t)kMaxWin; ++w) {
-                        const uint32_t col = g.q0 * eps + w;
-                        if (w / eps < g.nsec && L.member(col))
-                            p.term[q][w] = make_double2(ctx->terms[col].deductible, ctx->terms[col].limit);
-                        else
-                            p.term[q][w] = make_double2(INFINITY, INFINITY);   // contributes exactly +0
-                    }
-                }
-                // Kernel choice (measured, profiles/r01_*): the register-pipelined LDG
-                // kernel at 3 CTAs/SM for single-layer launches, 2 CTAs/SM for shared-window
-                // towers.  The TMA gather4 ring (8) and the cp.async ring (1) are kept as
-                // ARA_KERNEL-selectable alternatives; both are slower on B200 today.
+                setup_window(g, p);
+                // Kernel choice (measured, profiles/r01_kernel_variants.md): fp64 windows of
+                // <= 4 sectors use the cooperative cp.async ring at 3 CTAs/SM (12); fp32
+                // windows the register-pipelined LDG kernel at 3 CTAs/SM (5) for single
+                // layers, 2 CTAs/SM (0) for shared-window towers.  The other variants stay
+                // ARA_KERNEL-selectable for A/B runs.
                 int variant = ctx->kernel_variant;
                 const uint32_t box_sec = g.nsec <= 1 ? 1 : (g.nsec <= 2 ? 2 : 4);
                 const bool tma_ok = g.nsec <= 4 && (g.q0 % spb) + g.nsec <= spb && encode_tiled() != nullptr;
-                if (variant < 0) variant = g.nl == 1 ? 5 : 0;
+                if (variant < 0) variant = (!fp32 && g.nsec <= 4) ? 12 : (g.nl == 1 ? 5 : 0);
                 if ((variant == 8 || variant == 9) && !tma_ok) variant = g.nl == 1 ? 5 : 0;
                 if (variant == 8 || variant == 9) {
                     if (!make_block_map(ctx, g.q0 / spb, box_sec, &p.tmap))

@@ -44,7 +44,10 @@ struct TableGeo {
     uint32_t epb = 0;            // elements per block row
     uint32_t n_blocks = 0;
     uint64_t block_elems = 0;    // (C+1) * epb
-    size_t bytes = 0;            // allocation incl. pad
+    uint64_t bm_words = 0;       // row-occupancy bitmap words per block (ceil((C+1)/32), padded)
+    size_t bm_off = 0;           // byte offset of the bitmaps in the allocation
+    size_t occ_off = 0;          // byte offset of the per-block occupied-row counters (u32)
+    size_t bytes = 0;            // allocation incl. pad and bitmaps
 };
 inline TableGeo table_geometry(uint32_t n_elts, uint32_t catalog, int fp32) {
     TableGeo g;
@@ -55,7 +58,14 @@ inline TableGeo table_geometry(uint32_t n_elts, uint32_t catalog, int fp32) {
     g.epb = (uint32_t)(row / g.esz);
     g.n_blocks = (n_elts + g.epb - 1) / g.epb;
     g.block_elems = ((uint64_t)catalog + 1) * g.epb;
-    g.bytes = (size_t)g.n_blocks * g.block_elems * g.esz + kTablePadBytes;
+    // Row-occupancy bitmap per column block: bit e of block b is set when ELT
+    // record (e, j) exists for some column j of the block.  A clear bit means
+    // the row is all zeros, so its lookup can be skipped (a zero row adds an
+    // exact +0 to every sum: every deductible and retention is >= 0).
+    g.bm_words = (((uint64_t)catalog + 1 + 31) / 32 + 63) / 64 * 64;
+    g.bm_off = ((size_t)g.n_blocks * g.block_elems * g.esz + kTablePadBytes + 255) / 256 * 256;
+    g.occ_off = g.bm_off + (size_t)g.n_blocks * g.bm_words * 4;
+    g.bytes = g.occ_off + ((size_t)g.n_blocks * 4 + 255) / 256 * 256;
     return g;
 }
 
@@ -77,6 +87,7 @@ struct TrialParams {
     uint32_t catalog;
     uint32_t n_layers;          // layers in this launch (<= kMaxLB)
     const void* table;          // column-blocked direct-access table (+ pad)
+    const uint32_t* bm;         // row-occupancy bitmap of the window's column block, or null (no skipping)
     uint64_t row_stride;        // elements per block row (= epb)
     uint64_t block_stride;      // elements per column block (= (C+1) * epb)
     uint64_t sec_off[kMaxSec];  // window sector offsets (elements, event 0)
@@ -206,5 +217,7 @@ struct ara_ctx {
     double grid_mult = 1.0;           // ARA_GRID_MULT
     int kernel_variant = -1;          // ARA_KERNEL (-1 auto; see pick_kernel in ara_kernel.cu)
     int pf_sectors = 1;               // ARA_PFN
+    bool no_skip = false;             // ARA_NO_SKIP=1: never skip zero rows via the occupancy bitmap (A/B)
+    std::vector<uint32_t> occ_rows;   // occupied rows per column block (from densify)
     cudaEvent_t ev[8] = {};
 };

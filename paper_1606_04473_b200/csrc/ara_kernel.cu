@@ -125,6 +125,43 @@ __device__ __forceinline__ void event_compute(const TrialParams& p, const double
     }
 }
 
+// event_compute for a window staged in shared memory (swizzled 16-B chunks):
+// each sector is read right before its ELTs are summed, so only one sector of
+// the row is live in registers.  Same arithmetic and order as event_compute.
+template <typename TV, int NSEC, int NLB>
+__device__ __forceinline__ void event_compute_smem(const TrialParams& p, const double2 (*s_term)[kMaxWin],
+                                                   uint32_t src, uint32_t swz, double (&G)[NLB],
+                                                   uint32_t (&m)[NLB]) {
+    constexpr int EPS = SecT<TV>::N;
+    constexpr bool SM = TermsInSmem<TV, NSEC, NLB>::value;
+#pragma unroll
+    for (int l = 0; l < NLB; ++l) {
+        if (l >= (int)p.n_layers) break;
+        double le = 0.0;
+#pragma unroll
+        for (int s = 0; s < NSEC; ++s) {
+            TV x[EPS];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint4 v;
+                asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                             : "r"(src + (((uint32_t)(2 * s + h) ^ swz) << 4))
+                             : "memory");
+                memcpy(&x[h * (EPS / 2)], &v, 16);
+            }
+#pragma unroll
+            for (int c = 0; c < EPS; ++c) {
+                const double2 tc = SM ? lds_term(&s_term[l][s * EPS + c]) : p.term[l][s * EPS + c];
+                le = __dadd_rn(le, terms((double)x[c], tc.x, tc.y));
+            }
+        }
+        const double o = terms(le, p.lw[l].occ_r, p.lw[l].occ_l);
+        G[l] = __dadd_rn(G[l], o);
+        m[l] += (o > 0.0) ? 1u : 0u;
+    }
+}
+
 // Events per lane per pipeline step (~16-32 row registers per stage); windows
 // wider than 32 registers run without the row double buffer (PIPE = false).
 template <typename TV, int NSEC>
@@ -716,6 +753,229 @@ __global__ void __launch_bounds__(kThreads, 1) trial_kernel_tma(const __grid_con
     if (err) atomicOr(p.err, err);
 }
 
+// ---------------------------------------------------------------------------
+// Cooperative cp.async ring.  Like trial_kernel_sm, the row windows of a step
+// land in a per-warp shared-memory ring NS steps deep, so in-flight rows hold
+// no registers and the ring runs across trial boundaries (no pipeline drain
+// per trial).  Unlike trial_kernel_sm (each lane copying its own row in 16-B
+// pieces, which re-fetches every 32-B sector twice), each cp.async
+// instruction here copies 32/CH whole rows, CH lanes per row, so one warp
+// request covers every sector of a row exactly once — the L2->SM traffic
+// equals the algorithmic bytes.  Rows are stored with a per-row chunk swizzle
+// so that each lane's read of its own row is bank-conflict free.  Same lane
+// mapping, per-lane order and arithmetic as trial_kernel: identical YLT bits.
+template <typename TV, int NSEC, int BUDGET_KB>
+struct CoGeo {
+    static constexpr int WARPS = kThreads / 32;
+    static constexpr int ROWB = NSEC * kSectorBytes;   // bytes per row window
+    static constexpr int CH = ROWB / 16;               // 16-B chunks per row
+    static constexpr int LPR = CH < 32 ? CH : 32;      // lanes per row in one copy instruction
+    static constexpr int RPI = 32 / LPR;               // rows per copy instruction
+    static constexpr int STAGE = 32 * ROWB;            // one row per lane
+    static constexpr int NS0 = (BUDGET_KB * 1024) / (WARPS * (STAGE + (int)sizeof(StepMeta)));
+    static constexpr int NS = NS0 > 16 ? 16 : (NS0 < 2 ? 2 : NS0);
+    static constexpr int BYTES = WARPS * NS * STAGE + WARPS * NS * (int)sizeof(StepMeta);
+    // conflict-free chunk permutation of row r (8 consecutive rows of a
+    // quarter-warp phase hit 8 distinct 16-B bank groups)
+    static __device__ __forceinline__ uint32_t swz(uint32_t r) {
+        return (r * (uint32_t)ROWB / 128u) & (uint32_t)(CH - 1);
+    }
+};
+
+template <typename TV, int NSEC, int NLB, int BUDGET_KB, int MINB, bool EARLY>
+__global__ void __launch_bounds__(kThreads, MINB) trial_kernel_co(const __grid_constant__ TrialParams p) {
+    using Geo = CoGeo<TV, NSEC, BUDGET_KB>;
+    constexpr int NS = Geo::NS;
+    constexpr int CH = Geo::CH, LPR = Geo::LPR, RPI = Geo::RPI;
+    constexpr bool SM = TermsInSmem<TV, NSEC, NLB>::value;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double2 s_term[SM ? NLB : 1][kMaxWin];
+    const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem) + wib * NS * Geo::STAGE;
+    StepMeta* meta = reinterpret_cast<StepMeta*>(smem + Geo::WARPS * NS * Geo::STAGE) + wib * NS;
+    if (SM) {
+        for (int i = threadIdx.x; i < NLB * kMaxWin; i += kThreads)
+            s_term[i / kMaxWin][i % kMaxWin] = p.term[i / kMaxWin][i % kMaxWin];
+    }
+    __syncthreads();
+
+    const uint64_t nw = (uint64_t)gridDim.x * Geo::WARPS;
+    const uint64_t pol = policy_evict_first();
+    const uint64_t base = __ldg(p.off);
+    uint32_t err = 0;
+    // This lane's part of every cooperative copy: chunk c_chunk of row
+    // i * RPI + c_row in copy instruction i.  Row addresses are one
+    // IMAD.WIDE.U32 (id x row bytes + per-lane base); the destination's
+    // swizzle repeats with period 2 in i (swz(i*RPI + c_row) for any window).
+    const uint32_t c_chunk = lane % LPR, c_row = lane / LPR;
+    const uint32_t row_bytes = (uint32_t)(p.row_stride * sizeof(TV));
+    const char* c_src = reinterpret_cast<const char*>(p.table) +
+                        (p.sec_off[c_chunk >> 1] + (c_chunk & 1) * (16 / sizeof(TV))) * sizeof(TV);
+    uint32_t c_dst[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const uint32_t r = (uint32_t)h * RPI + c_row;
+        c_dst[h] = c_row * Geo::ROWB + ((c_chunk ^ Geo::swz(r)) << 4);
+    }
+    const uint32_t my_row = ring + lane * Geo::ROWB;
+    const uint32_t my_swz = Geo::swz(lane);
+
+    // ---- step iterator (ids two steps ahead of the copies)
+    uint64_t it_t = p.t_begin + (uint64_t)blockIdx.x * Geo::WARPS + wib;
+    uint64_t it_a = 0, nx_a = 0, nx_b = 0;
+    uint32_t it_n = 0, it_k0 = 0;
+    bool it_valid = it_t < p.t_end;
+    auto fetch_next_offsets = [&](uint64_t tn) {
+        if (tn < p.t_end) { nx_a = __ldg(p.off + tn); nx_b = __ldg(p.off + tn + 1); }
+    };
+    auto enter_trial = [&](uint64_t a, uint64_t b) {
+        if (b < a) { err |= ERRBIT_OFFSETS; b = a; }
+        it_a = a - base;
+        it_n = (uint32_t)(b - a);
+        it_k0 = 0;
+    };
+    if (it_valid) {
+        enter_trial(__ldg(p.off + it_t), __ldg(p.off + it_t + 1));
+        fetch_next_offsets(it_t + nw);
+    }
+    // Two-slot queue of steps whose ids are in flight; step j lives in slot
+    // j & 1 (compile-time below: the loops are unrolled by two).
+    uint64_t q_t[2];
+    uint32_t q_n[2], q_k0[2], q_e[2], q_w[2];
+    auto load_step = [&](const int slot) {
+        if (it_valid) {
+            q_t[slot] = it_t;
+            q_n[slot] = it_n;
+            q_k0[slot] = it_k0;
+            const uint32_t k = it_k0 + lane;
+            uint32_t v = 0u;
+            if (k < it_n) {
+                v = ld_stream_u32(p.ids + it_a + k, pol);
+                if (v == 0u || v > p.catalog) { err |= ERRBIT_EVENT_RANGE; v = 0u; }
+            }
+            q_e[slot] = v;
+            it_k0 += 32u;
+            if (it_k0 >= it_n) {
+                it_t += nw;
+                it_valid = it_t < p.t_end;
+                if (it_valid) {
+                    enter_trial(nx_a, nx_b);
+                    fetch_next_offsets(it_t + nw);
+                }
+            }
+        } else {
+            q_t[slot] = ~0ull;
+            q_e[slot] = 0u;
+        }
+    };
+    // copy the rows of step j (queue slot j & 1) into ring slot j % NS, then
+    // reuse the queue slot for the ids of step j + 2
+    // The occupancy word of a step's id is fetched one iteration after the id
+    // (and one before the copies): a clear bit marks an all-zero row, whose
+    // copy becomes a zero-fill with no memory request.  The arithmetic is
+    // unchanged (it runs on the zeros), so the YLT bits are too.
+    const uint32_t* bm = p.bm;
+    auto load_occupancy = [&](const int slot) {
+        q_w[slot] = bm ? __ldg(bm + (q_e[slot] >> 5)) : ~0u;
+    };
+    auto issue = [&](const uint32_t j, const int qs) {
+        const uint64_t ct = q_t[qs];
+        const uint32_t cn = q_n[qs], ck0 = q_k0[qs];
+        const uint32_t ce = ((q_w[qs] >> (q_e[qs] & 31u)) & 1u) ? q_e[qs] : 0u;
+        load_occupancy(qs ^ 1);
+        load_step(qs);
+        const uint32_t slot = j % NS;
+        if (ct != ~0ull) {
+            const uint32_t dst = ring + slot * Geo::STAGE;
+#pragma unroll
+            for (int i = 0; i < CH; ++i) {
+                const uint32_t e = __shfl_sync(0xffffffffu, ce, (uint32_t)i * RPI + c_row);
+                // rows without an event (e == 0): zero-fill, no memory request
+                cp_async16(dst + (uint32_t)i * RPI * Geo::ROWB + c_dst[i & 1], c_src + (uint64_t)e * row_bytes,
+                           e ? 16u : 0u);
+            }
+        }
+        if (lane == 0) meta[slot] = StepMeta{ct, cn, ck0};
+        cp_commit();
+    };
+    load_step(0);
+    load_occupancy(0);
+    load_step(1);
+#pragma unroll
+    for (int j = 0; j < NS; ++j) issue((uint32_t)j, j & 1);
+
+    double G[NLB];
+    uint32_t m[NLB];
+#pragma unroll
+    for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
+
+    // consumer: step c lands, its rows move to registers, the slot is
+    // refilled with step c + NS (before or after the fp64 work, EARLY).
+#pragma unroll 1
+    for (uint32_t c0 = 0;; c0 += 2) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint32_t c = c0 + (uint32_t)h;
+            cp_wait<NS - 1>();
+            __syncwarp();   // other lanes' copies of my row are complete and visible
+            const uint32_t slot = c % NS;
+            const StepMeta md = meta[slot];
+            if (md.t == ~0ull) goto done;
+            const uint32_t src = my_row + slot * Geo::STAGE;
+            if (EARLY) {
+                Row<TV, NSEC> r;
+#pragma unroll
+                for (int q = 0; q < CH; ++q) {
+                    uint4 v;
+                    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                 : "r"(src + (((uint32_t)q ^ my_swz) << 4))
+                                 : "memory");
+                    memcpy(&r.x[q >> 1][(q & 1) * (16 / sizeof(TV))], &v, 16);
+                }
+                __syncwarp();   // every lane's reads of the slot precede the copies refilling it
+                issue(c + NS, (h + NS) & 1);   // NS steps in flight during the arithmetic
+                event_compute<TV, NSEC, NLB>(p, s_term, r, G, m);
+            } else {
+                // the row is consumed from shared memory one sector at a time
+                // (8 live row registers instead of 32), then the slot is refilled
+                event_compute_smem<TV, NSEC, NLB>(p, s_term, src, my_swz, G, m);
+                __syncwarp();   // every lane's reads of the slot precede the copies refilling it
+                issue(c + NS, (h + NS) & 1);
+            }
+            if (md.k0 + 32u >= md.n) {   // last step of trial md.t: a7 + a8
+#pragma unroll
+                for (int l = 0; l < NLB; ++l) {
+#pragma unroll
+                    for (int off = 16; off >= 1; off >>= 1) {
+                        G[l] = __dadd_rn(G[l], __shfl_xor_sync(0xffffffffu, G[l], off));
+                        m[l] += __shfl_xor_sync(0xffffffffu, m[l], off);
+                    }
+                }
+                if (lane == 0) {
+                    const uint64_t t = md.t;
+                    double port = 0.0;
+                    if (p.portfolio_mode == 1) port = p.ylt[(uint64_t)p.portfolio_row * p.ld + t];
+#pragma unroll
+                    for (int l = 0; l < NLB; ++l) {
+                        if (l >= (int)p.n_layers) break;
+                        const double y = terms(G[l], p.lw[l].agg_r, p.lw[l].agg_l);
+                        p.ylt[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = y;
+                        if (p.lossy) p.lossy[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = m[l];
+                        port = __dadd_rn(port, y);
+                    }
+                    if (p.portfolio_mode >= 0) p.ylt[(uint64_t)p.portfolio_row * p.ld + t] = port;
+                }
+#pragma unroll
+                for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
+            }
+        }
+    }
+done:
+    cp_wait<0>();
+    if (err) atomicOr(p.err, err);
+}
+
 // Wide layers (window > kMaxSec sectors): same arithmetic and lane mapping,
 // one layer per launch, scalar loads through the column-block address map.
 template <typename TV>
@@ -977,15 +1237,47 @@ void* pick_tma(uint32_t nsec, int nl, int* smem) {
     return pick_nsec_tma<TV, 4>(nsec, smem);
 }
 
+template <typename TV, int NLB, int BUDGET_KB, int MINB, bool EARLY>
+void* pick_nsec_co(uint32_t nsec, int* smem) {
+    if (nsec <= 1) {
+        *smem = CoGeo<TV, 1, BUDGET_KB>::BYTES;
+        return (void*)trial_kernel_co<TV, 1, NLB, BUDGET_KB, MINB, EARLY>;
+    }
+    if (nsec <= 2) {
+        *smem = CoGeo<TV, 2, BUDGET_KB>::BYTES;
+        return (void*)trial_kernel_co<TV, 2, NLB, BUDGET_KB, MINB, EARLY>;
+    }
+    *smem = CoGeo<TV, 4, BUDGET_KB>::BYTES;
+    return (void*)trial_kernel_co<TV, 4, NLB, BUDGET_KB, MINB, EARLY>;
+}
+
+// 10: one CTA/SM, ~200 KB ring; 11: two CTAs/SM, ~100 KB each; 12: three CTAs/SM,
+// ~66 KB each (refill after the arithmetic); 13: as 12, refill before it
+template <typename TV>
+void* pick_co(uint32_t nsec, int nl, int variant, int* smem) {
+#define ARA_CO_V(NLB)                                                             \
+    if (variant == 11) return pick_nsec_co<TV, NLB, 100, 2, true>(nsec, smem);    \
+    if (variant == 12) return pick_nsec_co<TV, NLB, 66, 3, false>(nsec, smem);    \
+    if (variant == 13) return pick_nsec_co<TV, NLB, 66, 3, true>(nsec, smem);     \
+    return pick_nsec_co<TV, NLB, 200, 1, true>(nsec, smem);
+    if (nl <= 1) { ARA_CO_V(1) }
+    if (nl <= 2) { ARA_CO_V(2) }
+    ARA_CO_V(4)
+#undef ARA_CO_V
+}
+
 // variant: 0 = register-pipelined, 1 = shared-memory staged (cp.async ring),
 // 2-4 = register + L2 prefetch, 5-7 = register at higher occupancy,
-// 8 = TMA gather4 ring (needs p.tmap; windows of <= 4 sectors in one block).
+// 8 = TMA gather4 ring (needs p.tmap; windows of <= 4 sectors in one block),
+// 10-13 = cooperative cp.async ring (whole rows per instruction) at 1/2/3 CTAs/SM.
 void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
     *smem = 0;
     if (variant == 8 && nsec <= 4)
         return fp32 ? pick_tma<float>(nsec, nl, smem) : pick_tma<double>(nsec, nl, smem);
     if (nsec > (uint32_t)kMaxSec) return fp32 ? (void*)trial_kernel_wide<float> : (void*)trial_kernel_wide<double>;
     if (variant == 1) return fp32 ? pick_sm<float>(nsec, nl, smem) : pick_sm<double>(nsec, nl, smem);
+    if (variant >= 10 && variant <= 13 && nsec <= 4)
+        return fp32 ? pick_co<float>(nsec, nl, variant, smem) : pick_co<double>(nsec, nl, variant, smem);
     return fp32 ? pick<float>(nsec, nl, variant) : pick<double>(nsec, nl, variant);
 }
 

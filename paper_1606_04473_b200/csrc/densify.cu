@@ -8,8 +8,9 @@
 // sectors (geometry: ara::TableGeo).  Row 0 stays zero (event
 // ids are 1-based, reading A14); a missing (event, ELT) pair reads 0 (A4).
 //
-// The table was zero-filled by cudaMemsetAsync; this kernel scatters the
-// sparse records and validates them (fused, error bits).
+// The table (and its row-occupancy bitmaps) was zero-filled by
+// cudaMemsetAsync; this kernel scatters the sparse records, marks their rows in
+// the bitmap of their column block, and validates them (fused, error bits).
 #include <cfloat>
 
 #include "ara_internal.cuh"
@@ -22,7 +23,8 @@ __global__ void __launch_bounds__(256) densify_kernel(const uint64_t* __restrict
                                                       const uint32_t* __restrict__ ev,
                                                       const double* __restrict__ loss,
                                                       uint32_t catalog, TV* __restrict__ tab,
-                                                      uint32_t epb, uint64_t block_elems, uint32_t* err) {
+                                                      uint32_t epb, uint64_t block_elems, uint32_t* __restrict__ bm,
+                                                      uint64_t bm_words, uint32_t* __restrict__ occ, uint32_t* err) {
     const uint32_t j = blockIdx.y;
     const uint64_t lo = eoff[j], hi = eoff[j + 1];
     uint32_t bad = 0;
@@ -37,6 +39,8 @@ __global__ void __launch_bounds__(256) densify_kernel(const uint64_t* __restrict
             continue;
         }
         tab[(uint64_t)(j / epb) * block_elems + (uint64_t)e * epb + j % epb] = (TV)(x + 0.0);   // canonical +0 (A16)
+        const uint32_t bit = 1u << (e & 31u);   // row e of column block j / epb is occupied
+        if (!(atomicOr(bm + (uint64_t)(j / epb) * bm_words + (e >> 5), bit) & bit)) atomicAdd(occ + j / epb, 1u);
     }
     if (bad) atomicOr(err, bad);
 }
@@ -74,12 +78,14 @@ cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const d
     if (bx > 1024) bx = 1024;
     if (bx < 1) bx = 1;
     dim3 grid((unsigned)bx, n_elts);
+    uint32_t* bm = reinterpret_cast<uint32_t*>(static_cast<char*>(d_table) + geo.bm_off);
+    uint32_t* occ = reinterpret_cast<uint32_t*>(static_cast<char*>(d_table) + geo.occ_off);
     if (fp32)
-        densify_kernel<float><<<grid, 256, 0, s>>>(d_eoff, d_ev, d_loss, catalog,
-                                                   static_cast<float*>(d_table), geo.epb, geo.block_elems, d_err);
+        densify_kernel<float><<<grid, 256, 0, s>>>(d_eoff, d_ev, d_loss, catalog, static_cast<float*>(d_table),
+                                                   geo.epb, geo.block_elems, bm, geo.bm_words, occ, d_err);
     else
-        densify_kernel<double><<<grid, 256, 0, s>>>(d_eoff, d_ev, d_loss, catalog,
-                                                    static_cast<double*>(d_table), geo.epb, geo.block_elems, d_err);
+        densify_kernel<double><<<grid, 256, 0, s>>>(d_eoff, d_ev, d_loss, catalog, static_cast<double*>(d_table),
+                                                    geo.epb, geo.block_elems, bm, geo.bm_words, occ, d_err);
     return cudaGetLastError();
 }
 

@@ -31,6 +31,15 @@ CONFIGS = {
                 LayerSpec(16, 32, 1e5, 4e5, 6.5e6, 4e6),
                 LayerSpec(32, 48, 2.5e5, 5e5, 4e6, 3.5e6),
                 LayerSpec(48, 64, 5e5, 5e5, 0.0, INF))),
+    # SURVEY §8d config 4 "tower" variant: 4 layers over the same 16 ELTs
+    # (one row window serves every layer), multilayer terms
+    "tower": Workload(
+        name="tower", seed=1606044734, n_trials=1_000_000, nmin=800, nmax=1200,
+        catalog=2_000_000, n_elts=16, rho=0.01,
+        layers=(LayerSpec(0, 16, 2.5e4, 7.5e5, 1.2e7, 8e6),
+                LayerSpec(0, 16, 1e5, 4e5, 6.5e6, 4e6),
+                LayerSpec(0, 16, 2.5e5, 5e5, 4e6, 3.5e6),
+                LayerSpec(0, 16, 5e5, 5e5, 0.0, INF))),
     # BASELINE configs[4]: streamed 10M-trial YET (40 GB of ids)
     "stream10m": Workload(
         name="stream10m", seed=1606044735, n_trials=10_000_000, nmin=800, nmax=1200,

@@ -30,27 +30,30 @@ def run_oracle(off, ids, elts, w, layers, fp32=False, terms=None):
                       oracle.layers_from_specs(layers), lookup="dense", fp32_storage=fp32)
 
 
-KERNEL_VARIANTS = (-1, 0, 1, 5, 8, 9)   # ARA_KERNEL: auto, register, cp.async ring, register/3 CTAs, TMA gather4, hybrid
+KERNEL_VARIANTS = (-1, 0, 1, 5, 8, 9, 10, 11, 12, 13)   # ARA_KERNEL: auto, register, cp.async ring, register/3 CTAs, TMA gather4, hybrid, cooperative cp.async ring at 1/2/3 CTAs/SM
 
 
 def run_gpu(off, ids, elts, w, layers, precision="f64", terms=None, load_mode="all", chunk_trials=0,
-            device_inputs=False, return_periods=None, variant=None, run_mode="direct"):
+            device_inputs=False, return_periods=None, variant=None, run_mode="direct", env=None):
+    """env: extra ARA_* tuning variables read at ara_create (e.g. ARA_NO_SKIP)."""
     import os
     import torch
     from paper_1606_04473_b200 import ara
     d, li = (w.elt_terms() if terms is None else terms)
-    old = os.environ.get("ARA_KERNEL")
+    env = dict(env or {})
     if variant is not None:
-        os.environ["ARA_KERNEL"] = str(variant)
+        env["ARA_KERNEL"] = str(variant)
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
     try:
         ctx = ara.Context(w.catalog, precision=precision, load_mode=load_mode, chunk_trials=chunk_trials,
                           run_mode=run_mode)
     finally:
-        if variant is not None:
-            if old is None:
-                os.environ.pop("ARA_KERNEL", None)
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
             else:
-                os.environ["ARA_KERNEL"] = old
+                os.environ[k] = v
     with ctx:
         eo, ev, ls = elts
         if device_inputs:

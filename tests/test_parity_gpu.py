@@ -50,6 +50,25 @@ def test_tiny_integer_valued_is_bitwise(cuda, precision, cap, variant):
     assert_metrics_close(met, oracle_rows(orc), orc["scale"], w.return_periods, exact=True)
 
 
+@pytest.mark.parametrize("variant", KERNEL_VARIANTS)
+@pytest.mark.parametrize("rho", [0.02, 0.3])
+def test_sparse_elts_row_skipping_is_exact(cuda, variant, rho):
+    """ELTs as sparse as the paper's (10k-30k losses over a large catalogue,
+    P:237): most rows of the direct-access table are all zero and the kernel
+    skips their lookups via the row-occupancy bitmap.  A zero row adds an
+    exact +0 (deductibles and retentions are >= 0), so the YLT must match the
+    oracle and be bit-identical to a run without skipping (ARA_NO_SKIP)."""
+    w = synth.get_config("tiny").with_(rho=rho, return_periods=(2, 10, 100))
+    off, ids, elts = make_inputs(w)
+    orc = run_oracle(off, ids, elts, w, w.layers)
+    ylt, lossy, _, met = run_gpu(off, ids, elts, w, w.layers, return_periods=w.return_periods, variant=variant)
+    assert_ylt_close(ylt, orc)
+    assert np.array_equal(lossy, orc["lossy"])
+    assert_metrics_close(met, oracle_rows(orc), orc["scale"], w.return_periods)
+    ylt2, lossy2, _, _ = run_gpu(off, ids, elts, w, w.layers, variant=variant, env={"ARA_NO_SKIP": 1})
+    assert np.array_equal(ylt, ylt2) and np.array_equal(lossy, lossy2)
+
+
 def test_device_pointer_inputs_match_host_inputs(cuda):
     w = synth.get_config("tiny")
     off, ids, elts = make_inputs(w)

@@ -1,0 +1,18 @@
+# A/B: cooperative cp.async ring (ARA_KERNEL 10-12), refill-before-compute ordering.
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_parity_gpu.py -q -p no:cacheprovider -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+P="python tools/prof_ara.py --steps 3"
+: > gpurun_out/ab.jsonl
+for k in 5 10 11 12; do
+  ARA_KERNEL=$k timeout 300 $P >> gpurun_out/ab.jsonl 2>> gpurun_out/ab.err
+done
+for k in 11 12; do
+  ARA_KERNEL=$k timeout 300 $P --precision f32 >> gpurun_out/ab.jsonl 2>> gpurun_out/ab.err
+  ARA_KERNEL=$k timeout 300 $P --config multilayer >> gpurun_out/ab.jsonl 2>> gpurun_out/ab.err
+done
+tail -2 gpurun_out/pytest_gpu.log
+python -c "
+import json
+for l in open('gpurun_out/ab.jsonl'):
+    d=json.loads(l); print(d['config'], d['precision'], d['env'], [round(x,3) for x in d['kernel_ms']])
+"

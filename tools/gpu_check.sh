@@ -1,0 +1,7 @@
+# Round-1 re-entry check: smoke, GPU tests, default bench line.
+set -x
+mkdir -p gpurun_out
+timeout 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+tail -3 gpurun_out/smoke.log; tail -3 gpurun_out/pytest_gpu.log; cut -c1-2500 gpurun_out/bench.json
