@@ -141,24 +141,37 @@ class ClockSampler:
                 "samples": len(sel), "window": "timed region" if sel is inside else "whole run"}
 
 
-def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str = "direct") -> int:
-    """direct mode — per event 4 B of id + the 32-B
-    sectors of every layer window; per trial 8 B of offsets + 8 B per YLT row.
-    Fold mode — the fold pass reads every catalogue row window once and writes
-    8 B per (event id, layer); the trial pass reads 4 B of id + one fold row
-    (8 B x layers, padded to a power of two) per event."""
+def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str = "direct",
+                      occupancy: float = 1.0) -> int:
+    """DESIGN.md section 6 "Algorithmic bytes".  Direct mode, per launch (layers
+    sharing one row window share a launch): per event 4 B of id, plus -- when
+    zero rows are skipped (occupancy < 1) -- the 4-B occupancy word, plus the
+    32-B sectors of the launch's row window for the occupied fraction of events;
+    per trial 8 B of offsets + 8 B per YLT row.  Fold mode: the fold pass reads
+    every catalogue row window once and writes 8 B per (event id, layer); the
+    trial pass reads 4 B of id + one fold row (8 B x layers, padded to a power
+    of two) per event."""
     eps = 4 if precision == "f64" else 8
-    sec = 0
+    windows = []
     for L in w.layers:
-        sec += (L.elt_end + eps - 1) // eps - L.elt_begin // eps
+        win = (L.elt_begin // eps, (L.elt_end + eps - 1) // eps)
+        if not windows or windows[-1][0] != win or windows[-1][1] == 4:
+            windows.append([win, 1])
+        else:
+            windows[-1][1] += 1
     per_trial = n_trials * (8 + 8 * (len(w.layers) + 1))
     if mode == "fold":
+        sec = sum(b - a for (a, b), _ in windows)
         nl = len(w.layers)
         nlc = 1
         while nlc < nl and nlc < 8:
             nlc *= 2
-        return (w.catalog + 1) * (32 * sec + 8 * nl) + n_events * (4 + 8 * nlc) * ((nl + nlc - 1) // nlc) + per_trial
-    return n_events * (4 + 32 * sec) + per_trial
+        return int((w.catalog + 1) * (32 * sec + 8 * nl) + n_events * (4 + 8 * nlc) * ((nl + nlc - 1) // nlc)
+                   + per_trial)
+    per_event = 0.0
+    for (a, b), _ in windows:
+        per_event += 4 + (4 if occupancy < 1.0 else 0) + occupancy * 32 * (b - a)
+    return int(n_events * per_event + per_trial)
 
 
 def load_peaks():
@@ -168,24 +181,25 @@ def load_peaks():
         return {}
 
 
-def kernel_name(a):
-    """The ARA kernel the library picks by default (ara_host.cu, 'Kernel choice')."""
-    if a.mode != "direct":
-        return "ara::fold_kernel+trial_fold_kernel"
-    v = os.environ.get("ARA_KERNEL")
-    if v is not None and int(v) >= 0:
-        return f"ara::trial_kernel (ARA_KERNEL={v})"
-    return "ara::trial_kernel_co" if a.precision == "f64" else "ara::trial_kernel"
+KERNEL_NAMES = {14: "ara::trial_kernel_cq (compacted rounds)", 12: "ara::trial_kernel_co (cooperative ring)",
+                5: "ara::trial_kernel (register pipeline)", 0: "ara::trial_kernel (register pipeline)",
+                -2: "ara::fold_kernel+trial_fold_kernel"}
 
 
-def load_traffic(w, precision):
-    """dram bytes per launch of the ARA kernel from the committed ncu --set full summary."""
+def kernel_name(variant):
+    """The trial kernel the library reports it launched (ara_run_stats.kernel_variant)."""
+    return KERNEL_NAMES.get(int(variant), f"ara::trial_kernel (ARA_KERNEL={variant})")
+
+
+def load_traffic(w, precision, variant):
+    """DRAM bytes (and L2 sectors) per launch of the ARA kernel from the
+    committed ncu --set full capture of the same kernel variant, or None."""
     p = os.path.join(ROOT, "profiles", "ara_kernel_traffic.json")
     try:
-        d = json.load(open(p))
-        return d.get(f"{w.name}/{precision}", {}).get("dram_bytes_per_launch")
+        d = json.load(open(p)).get(f"{w.name}/{precision}", {})
     except (OSError, ValueError):
         return None
+    return d if d.get("variant") == variant else None
 
 
 # ------------------------------------------------------------------ oracle (cpu baseline / reference arm)
@@ -324,6 +338,7 @@ def main():
     ctx = ara.Context(w.catalog, device=local, precision=a.precision, stream=stream, rank=rank, world=world,
                       nccl_id=new_nccl_id(), l2_persist=a.l2_persist, run_mode=a.mode)
     kern_ms, ag_ms, met_ms, launches = [], [], [], []
+    used = {}
 
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     part_ms = []
@@ -343,6 +358,7 @@ def main():
             ag_ms.append(st["allgather_ms"])
             met_ms.append(mms)
             launches.append(st["n_kernel_launches"])
+            used.update(variant=st["kernel_variant"], occupancy=st["occupancy"])
             evs[4].synchronize()
             part_ms.append([evs[i].elapsed_time(evs[i + 1]) for i in range(4)])
         return st, pml, tvar
@@ -376,14 +392,15 @@ def main():
 
     # roofline of the dominant kernel (the ARA trial kernel) on this rank
     k_ms = float(np.mean(kern_ms))
-    alg = algorithmic_bytes(w, ev_local, count, a.precision, a.mode)
+    alg = algorithmic_bytes(w, ev_local, count, a.precision, a.mode, occupancy=used.get("occupancy", 1.0))
     peaks = load_peaks()
     peak = peaks.get("hbm_gbs")
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
     if not peak:
         peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
     achieved = alg / (k_ms / 1e3) / 1e9
-    traffic = load_traffic(w, a.precision)
+    trec = load_traffic(w, a.precision, used.get("variant")) if a.mode == "direct" else None
+    traffic = trec.get("dram_bytes_per_launch") if trec else None
     ctx.close()
 
     # ---- end-to-end arm: host buffers through the C-ABI
@@ -466,12 +483,15 @@ def main():
             "lookups_per_sec": lookups / (ms / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic if a.mode == "direct" else None,
-                         "kernel": kernel_name(a),
+                         "kernel": kernel_name(used.get("variant", -1)),
+                         "table_occupancy": used.get("occupancy"),
                          "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
                          # algorithmic bytes count every gathered row, including the ones L2
                          # serves, so frac can exceed 1; the DRAM-level figure is traffic / time
                          "dram_achieved": (traffic / (k_ms * 1e6)) if (traffic and a.mode == "direct") else None,
-                         "dram_frac": (traffic / (k_ms * 1e6) / peak) if (traffic and a.mode == "direct") else None},
+                         "dram_frac": (traffic / (k_ms * 1e6) / peak) if (traffic and a.mode == "direct") else None,
+                         "l2_sector_bytes": (32 * trec["l2_sectors_per_launch"]) if trec else None,
+                         "traffic_source": trec.get("source") if trec else None},
             "breakdown_ms": {"ara_kernel": k_ms, "allgather": float(np.mean(ag_ms)), "metrics": float(np.mean(met_ms)),
                              "step": ms,
                              "calls": {k: float(np.median([p[i] for p in part_ms]))

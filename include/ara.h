@@ -120,6 +120,11 @@ typedef struct {
     double total_ms;         /* whole ara_run on the stream, first enqueue to completion */
     uint64_t h2d_bytes;      /* bytes copied host->device inside this run */
     uint32_t n_kernel_launches;
+    int32_t kernel_variant;  /* trial kernel of the last direct launch: 14 compacted rounds (sparse
+                                tables), 12 cooperative cp.async ring, 5/0 register pipeline, ...
+                                (ARA_KERNEL numbering); -2 = fold mode, -1 = none */
+    double occupancy;        /* fraction of row windows the last direct launch gathers: the occupied-row
+                                fraction of its column block when zero rows are skipped, else 1.0 */
 } ara_run_stats;
 
 /* ---- host-only helpers (no GPU needed) ---------------------------------- */

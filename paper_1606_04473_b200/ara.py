@@ -62,7 +62,8 @@ class ara_run_stats(ctypes.Structure):
                 ("n_lookups_local", ctypes.c_uint64), ("kernel_ms", ctypes.c_double),
                 ("h2d_ms", ctypes.c_double), ("allgather_ms", ctypes.c_double),
                 ("total_ms", ctypes.c_double), ("h2d_bytes", ctypes.c_uint64),
-                ("n_kernel_launches", ctypes.c_uint32)]
+                ("n_kernel_launches", ctypes.c_uint32), ("kernel_variant", ctypes.c_int32),
+                ("occupancy", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -905,6 +905,8 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     base.pf_sectors = ctx->pf_sectors;
     base.portfolio_row = n_layers + n_programs;
     uint32_t launches = 0;
+    int used_variant = fold ? -2 : -1;
+    double used_occupancy = 1.0;
     std::vector<void*> wide_free;   // per-run column lists / terms of wide layers
     // per-group window setup shared by the direct and fold launches
     auto setup_window = [&](const Group& g, TrialParams& p) {
@@ -1014,12 +1016,20 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 CK(launch_trials_wide(p, fp32, d_wc, d_wt, (uint32_t)wcols.size(), grid, s));
             } else {
                 setup_window(g, p);
-                // Kernel choice (measured, profiles/r01_kernel_variants.md): fp64 windows of
-                // <= 4 sectors use the cooperative cp.async ring at 3 CTAs/SM (12); fp32
-                // windows the register-pipelined LDG kernel at 3 CTAs/SM (5) for single
-                // layers, 2 CTAs/SM (0) for shared-window towers.  The other variants stay
-                // ARA_KERNEL-selectable for A/B runs.
+                // Kernel choice (measured, profiles/r01_kernel_variants.md): windows over a
+                // sparse column block (occupancy bitmap set) use the compacted-rounds kernel
+                // (14); dense fp64 windows of <= 4 sectors the cooperative cp.async ring at
+                // 3 CTAs/SM (12); dense fp32 windows the register-pipelined LDG kernel at
+                // 3 CTAs/SM (5) for single layers, 2 CTAs/SM (0) for shared-window towers.
+                // The other variants stay ARA_KERNEL-selectable for A/B runs.
                 int variant = ctx->kernel_variant;
+                if (variant < 0 && p.bm) variant = 14;
+                if (p.bm) {   // rows actually gathered: the occupied fraction of the block
+                    const uint32_t blk = g.q0 / spb;
+                    used_occupancy = (double)ctx->occ_rows[blk] / ((double)ctx->catalog + 1.0);
+                } else {
+                    used_occupancy = 1.0;
+                }
                 const uint32_t box_sec = g.nsec <= 1 ? 1 : (g.nsec <= 2 ? 2 : 4);
                 const bool tma_ok = g.nsec <= 4 && (g.q0 % spb) + g.nsec <= spb && encode_tiled() != nullptr;
                 if (variant < 0) variant = (!fp32 && g.nsec <= 4) ? 12 : (g.nl == 1 ? 5 : 0);
@@ -1029,6 +1039,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                         return fail(ctx, ARA_ERR_CUDA, "cuTensorMapEncodeTiled failed");
                     p.tma_col = (g.q0 % spb) * eps;
                 }
+                used_variant = variant;
                 if (variant == 9) {
                     // Hybrid: the register-pipelined LDG kernel (2 CTAs/SM) and the TMA
                     // gather4 kernel (1 CTA/SM, shared-memory ring) run side by side on two
@@ -1154,6 +1165,8 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         stats->h2d_ms = stream_in ? ev_ms(ctx->ev[6], ctx->ev[7]) : 0.0;
         stats->h2d_bytes = h2d_bytes;
         stats->n_kernel_launches = launches;
+        stats->kernel_variant = used_variant;
+        stats->occupancy = used_occupancy;
     }
     return ARA_OK;
 }

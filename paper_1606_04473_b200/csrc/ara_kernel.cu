@@ -976,6 +976,316 @@ done:
     if (err) atomicOr(p.err, err);
 }
 
+// ---------------------------------------------------------------------------
+// Compacted rounds (sparse ELTs).  On the paper's ELTs most rows of the
+// direct-access table are all zero (10k-30k losses per ELT over a catalogue of
+// millions), and a zero row adds an exact +0 to every sum.  This kernel
+// keeps the warp-per-trial mapping (event k -> lane k % 32, each lane in
+// increasing k) but lets every lane skip its zero-row events: a scan stage
+// walks the trial 32 events per step, tests each event's row in the
+// occupancy bitmap and appends occupied events to a per-lane FIFO (QC deep);
+// a round -- one occupied event per lane -- is emitted into the cooperative
+// cp.async ring whenever a lane's FIFO is full and, at the end of the trial,
+// until every FIFO is empty (the last round of a trial finalises it).  Each
+// lane still adds its occupied events' losses in increasing k, so G per lane,
+// the xor tree and the YLT bits equal trial_kernel's, while the fp64 term
+// arithmetic runs once per round (~0.3 rounds per step at the paper's
+// occupancy) instead of once per step.
+//
+// Latency: the scan's ids (QD steps ahead) and occupancy words (DW steps
+// ahead) are cp.async copies into small per-warp rings, so nothing in flight
+// holds a register; every copy belongs to a commit group whose sequence
+// number is tracked, and each consumer waits for exactly the group it needs
+// (cp.async.wait_group with a run-time count).
+__device__ __forceinline__ void cp_async4(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+// Scan steps cover 128 events of one trial (4 sub-steps of 32: event
+// k0 + 32 j + lane), so the fixed per-step work (waits, step metadata, the id
+// iterator) is paid once per 128 events.  A step's ids arrive as one aligned
+// 16-B-chunk copy of the id range (33 chunks); its occupancy words as one
+// 4-B gather per event.
+struct CqStep {
+    uint64_t t;            // trial (UINT64_MAX: no more steps)
+    uint32_t n, k0;        // trial length, first event of the step
+    uint32_t sh, pad;      // position of event k0 in the step's id slot
+};
+
+template <int MINB_>
+struct CqRings {
+    static constexpr int QD = 3;        // ids are copied QD steps ahead
+    static constexpr int DW = 1;        // occupancy words DW steps ahead (QD >= 2 DW + 1)
+    static constexpr int IR = QD + 1;   // id ring slots (33 x 16 B)
+    static constexpr int WR = DW + 1;   // occupancy ring slots (128 x u32)
+    static constexpr int MR = 8;        // step-meta ring slots (> QD)
+    static constexpr int IDB = 33 * 16;
+    static constexpr int BYTES = IR * IDB + WR * 512 + MR * (int)sizeof(CqStep);   // per warp
+};
+
+template <typename TV, int NSEC, int BUDGET_KB, int MINB>
+struct CqGeo {
+    using Ring = CoGeo<TV, NSEC, BUDGET_KB>;
+    using R = CqRings<MINB>;
+    static constexpr int BYTES = Ring::WARPS * Ring::NS * Ring::STAGE + Ring::WARPS * Ring::NS * (int)sizeof(StepMeta) +
+                                 Ring::WARPS * R::BYTES;
+};
+
+// cp.async.wait_group with a run-time count n, clamped to 7 (a smaller count
+// only waits for more groups)
+__device__ __forceinline__ void cp_wait_upto(uint32_t n) {
+    if (n >= 4) {
+        if (n >= 6) { if (n >= 7) cp_wait<7>(); else cp_wait<6>(); }
+        else { if (n >= 5) cp_wait<5>(); else cp_wait<4>(); }
+    } else {
+        if (n >= 2) { if (n >= 3) cp_wait<3>(); else cp_wait<2>(); }
+        else { if (n >= 1) cp_wait<1>(); else cp_wait<0>(); }
+    }
+}
+
+template <typename TV, int NSEC, int NLB, int BUDGET_KB, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_constant__ TrialParams p) {
+    using Geo = CoGeo<TV, NSEC, BUDGET_KB>;
+    using RG = typename CqGeo<TV, NSEC, BUDGET_KB, MINB>::R;
+    constexpr int NS = Geo::NS;
+    constexpr int CH = Geo::CH, LPR = Geo::LPR, RPI = Geo::RPI;
+    constexpr int QD = RG::QD, DW = RG::DW, IR = RG::IR, WR = RG::WR, MR = RG::MR, IDB = RG::IDB;
+    constexpr int QC = 4;   // per-lane FIFO of occupied events
+    constexpr bool SM = TermsInSmem<TV, NSEC, NLB>::value;
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ double2 s_term[SM ? NLB : 1][kMaxWin];
+    const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem) + wib * NS * Geo::STAGE;
+    StepMeta* rmeta = reinterpret_cast<StepMeta*>(smem + Geo::WARPS * NS * Geo::STAGE) + wib * NS;
+    unsigned char* wsm = smem + Geo::WARPS * NS * (Geo::STAGE + (int)sizeof(StepMeta)) + wib * RG::BYTES;
+    const uint32_t idr = (uint32_t)__cvta_generic_to_shared(wsm);   // id ring [IR][33 x 16 B]
+    const uint32_t ocr = idr + IR * IDB;                            // occupancy ring [WR][128]
+    CqStep* smeta = reinterpret_cast<CqStep*>(wsm + IR * IDB + WR * 512);
+    if (SM) {
+        for (int i = threadIdx.x; i < NLB * kMaxWin; i += kThreads)
+            s_term[i / kMaxWin][i % kMaxWin] = p.term[i / kMaxWin][i % kMaxWin];
+    }
+    __syncthreads();
+
+    const uint64_t nw = (uint64_t)gridDim.x * Geo::WARPS;
+    const uint64_t base = __ldg(p.off);
+    const uint32_t* bm = p.bm;
+    uint32_t err = 0;
+    const uint32_t c_chunk = lane % LPR, c_row = lane / LPR;
+    const uint32_t row_bytes = (uint32_t)(p.row_stride * sizeof(TV));
+    const char* c_src = reinterpret_cast<const char*>(p.table) +
+                        (p.sec_off[c_chunk >> 1] + (c_chunk & 1) * (16 / sizeof(TV))) * sizeof(TV);
+    uint32_t c_dst[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) c_dst[h] = c_row * Geo::ROWB + ((c_chunk ^ Geo::swz((uint32_t)h * RPI + c_row)) << 4);
+    const uint32_t my_row = ring + lane * Geo::ROWB;
+    const uint32_t my_swz = Geo::swz(lane);
+
+    uint32_t gseq = 0;   // commit groups so far (warp-uniform)
+    auto commit = [&]() { cp_commit(); return gseq++; };
+    auto wait_group = [&](uint32_t g) { cp_wait_upto(gseq - 1u - g); };
+    auto lds_u32 = [&](uint32_t a) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+        return v;
+    };
+
+    // ---- fetch iterator: QD steps ahead of the scan
+    uint64_t it_t = p.t_begin + (uint64_t)blockIdx.x * Geo::WARPS + wib;
+    uint64_t it_a = 0, nx_a = 0, nx_b = 0;
+    uint32_t it_n = 0, it_k0 = 0;
+    bool it_valid = it_t < p.t_end;
+    auto fetch_next_offsets = [&](uint64_t tn) {
+        if (tn < p.t_end) { nx_a = __ldg(p.off + tn); nx_b = __ldg(p.off + tn + 1); }
+    };
+    auto enter_trial = [&](uint64_t a, uint64_t b) {
+        if (b < a) { err |= ERRBIT_OFFSETS; b = a; }
+        it_a = a - base;
+        it_n = (uint32_t)(b - a);
+        it_k0 = 0;
+    };
+    if (it_valid) {
+        enter_trial(__ldg(p.off + it_t), __ldg(p.off + it_t + 1));
+        fetch_next_offsets(it_t + nw);
+    }
+    // copy step x's ids (the 16-B chunks spanning them; bytes past the step's
+    // last id are zero-filled, never read) and record the step's metadata;
+    // validation happens at the scan
+    auto fetch_ids = [&](uint32_t x) {
+        CqStep md{~0ull, 0u, 0u, 0u, 0u};
+        if (it_valid) {
+            const uint32_t cnt = it_n - it_k0 < 128u ? it_n - it_k0 : 128u;
+            const uintptr_t ab = reinterpret_cast<uintptr_t>(p.ids + it_a + it_k0);
+            const uintptr_t al = ab & ~(uintptr_t)15;
+            const uintptr_t end = ab + 4u * cnt;
+            const uint32_t dst = idr + (x % IR) * IDB;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const uint32_t c = lane + 32u * (uint32_t)r;
+                if (r == 0 || lane == 0) {
+                    const uintptr_t cs = al + 16u * c;
+                    const uint32_t nb = cs >= end ? 0u : (end - cs >= 16u ? 16u : (uint32_t)(end - cs));
+                    cp_async16(dst + 16u * c, reinterpret_cast<const void*>(nb ? cs : al), nb);
+                }
+            }
+            md = CqStep{it_t, it_n, it_k0, (uint32_t)(ab - al) / 4u, 0u};
+            it_k0 += 128u;
+            if (it_k0 >= it_n) {
+                it_t += nw;
+                it_valid = it_t < p.t_end;
+                if (it_valid) {
+                    enter_trial(nx_a, nx_b);
+                    fetch_next_offsets(it_t + nw);
+                }
+            }
+        }
+        if (lane == 0) smeta[x % MR] = md;
+    };
+    // copy the occupancy words of step x's events (its ids have landed)
+    auto fetch_occupancy = [&](uint32_t x) {
+        const uint32_t sh = smeta[x % MR].sh;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t e = lds_u32(idr + (x % IR) * IDB + (sh + 32u * j + lane) * 4u);
+            e = e <= p.catalog ? e : 0u;   // not validated yet
+            cp_async4(ocr + ((x % WR) * 128u + 32u * j + lane) * 4u, bm + (e >> 5), bm ? 4u : 0u);
+        }
+    };
+
+    // prologue: ids of steps 0..QD-1 (one group), then occupancy of steps 0..DW-1
+#pragma unroll 1
+    for (uint32_t x = 0; x < (uint32_t)QD; ++x) fetch_ids(x);
+    wait_group(commit());
+    __syncwarp();
+    uint32_t g_occ = 0;   // commit group of the occupancy words of the next step to scan
+#pragma unroll 1
+    for (uint32_t x = 0; x < (uint32_t)DW; ++x) {
+        fetch_occupancy(x);
+        g_occ = commit();
+    }
+
+    // ---- per-lane FIFO of occupied events (entries at and beyond fc are 0)
+    uint32_t f[QC];
+#pragma unroll
+    for (int i = 0; i < QC; ++i) f[i] = 0u;
+    uint32_t fc = 0;
+
+    double G[NLB];
+    uint32_t m[NLB];
+#pragma unroll
+    for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
+    uint32_t head = 0, tail = 0;   // ring slots: next to consume / next to fill (warp-uniform)
+    uint32_t rg[NS];               // commit group of each ring slot's rows
+
+    auto consume = [&]() {
+        const uint32_t slot = head % NS;
+        uint32_t g = rg[0];
+#pragma unroll
+        for (int i = 1; i < NS; ++i) g = (slot == (uint32_t)i) ? rg[i] : g;
+        wait_group(g);
+        __syncwarp();   // other lanes' copies of my row are complete and visible
+        const StepMeta rm = rmeta[slot];
+        event_compute_smem<TV, NSEC, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m);
+        __syncwarp();   // every lane's reads of the slot precede the copies refilling it
+        ++head;
+        if (rm.n) {   // last round of trial rm.t: a7 + a8
+#pragma unroll
+            for (int l = 0; l < NLB; ++l) {
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                    G[l] = __dadd_rn(G[l], __shfl_xor_sync(0xffffffffu, G[l], off));
+                    m[l] += __shfl_xor_sync(0xffffffffu, m[l], off);
+                }
+            }
+            if (lane == 0) {
+                const uint64_t t = rm.t;
+                double port = 0.0;
+                if (p.portfolio_mode == 1) port = p.ylt[(uint64_t)p.portfolio_row * p.ld + t];
+#pragma unroll
+                for (int l = 0; l < NLB; ++l) {
+                    if (l >= (int)p.n_layers) break;
+                    const double y = terms(G[l], p.lw[l].agg_r, p.lw[l].agg_l);
+                    p.ylt[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = y;
+                    if (p.lossy) p.lossy[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = m[l];
+                    port = __dadd_rn(port, y);
+                }
+                if (p.portfolio_mode >= 0) p.ylt[(uint64_t)p.portfolio_row * p.ld + t] = port;
+            }
+#pragma unroll
+            for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
+        }
+    };
+    // emit a round: every lane pops its FIFO head (0 = nothing: zero-fill)
+    // (the caller has made room in the ring)
+    auto emit = [&](uint64_t t, uint32_t last) {
+        const uint32_t ce = f[0];
+#pragma unroll
+        for (int i = 0; i + 1 < QC; ++i) f[i] = f[i + 1];
+        f[QC - 1] = 0u;
+        fc -= fc ? 1u : 0u;
+        const uint32_t slot = tail % NS;
+        const uint32_t dst = ring + slot * Geo::STAGE;
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            const uint32_t e = __shfl_sync(0xffffffffu, ce, (uint32_t)i * RPI + c_row);
+            cp_async16(dst + (uint32_t)i * RPI * Geo::ROWB + c_dst[i & 1], c_src + (uint64_t)e * row_bytes,
+                       e ? 16u : 0u);
+        }
+        if (lane == 0) rmeta[slot] = StepMeta{t, last, 0u};
+        const uint32_t g = commit();
+#pragma unroll
+        for (int i = 0; i < NS; ++i) rg[i] = (slot == (uint32_t)i) ? g : rg[i];
+        ++tail;
+    };
+
+    // One call site each for emit and (in the loop) consume keeps the loop
+    // body small enough for the instruction cache.
+#pragma unroll 1
+    for (uint32_t sc = 0;; ++sc) {
+        // step sc's occupancy words (and, older, its ids) have landed
+        wait_group(g_occ);
+        __syncwarp();
+        const CqStep md = smeta[sc % MR];
+        if (md.t == ~0ull) break;
+        // refill first: occupancy of step sc+DW (its ids landed: QD >= 2 DW + 1),
+        // then ids of step sc+QD; separate groups, so the next scan waits for
+        // the occupancy words only
+        fetch_occupancy(sc + DW);
+        g_occ = commit();
+        fetch_ids(sc + QD);
+        commit();
+        const bool trial_end = md.k0 + 128u >= md.n;
+#pragma unroll 1
+        for (uint32_t j = 0; j < 4u; ++j) {
+            const uint32_t k = md.k0 + 32u * j + lane;
+            uint32_t e = lds_u32(idr + (sc % IR) * IDB + (md.sh + 32u * j + lane) * 4u);
+            const uint32_t w = lds_u32(ocr + ((sc % WR) * 128u + 32u * j + lane) * 4u);
+            if (k >= md.n) e = 0u;
+            else if (e == 0u || e > p.catalog) { err |= ERRBIT_EVENT_RANGE; e = 0u; }   // A14
+            e = (!bm || ((w >> (e & 31u)) & 1u)) ? e : 0u;
+            if (e) {   // append (entries beyond fc are 0, so f[fc] is free)
+#pragma unroll
+                for (int i = 0; i < QC; ++i) f[i] = (fc == (uint32_t)i) ? e : f[i];
+                ++fc;
+            }
+            // a full FIFO emits one round; the end of the trial emits rounds
+            // until every FIFO is empty, the last one finalising the trial
+            const bool flush = trial_end && j == 3u;
+            for (;;) {
+                uint32_t last = 0u;
+                if (flush) last = __any_sync(0xffffffffu, fc > 1u) ? 0u : 1u;
+                else if (!__any_sync(0xffffffffu, fc == (uint32_t)QC)) break;
+                if (tail - head == (uint32_t)NS) consume();
+                emit(md.t, last);
+                if (!flush || last) break;
+            }
+        }
+        __syncwarp();   // reads of this step's slots precede their refills
+    }
+    while (head != tail) consume();
+    cp_wait<0>();
+    if (err) atomicOr(p.err, err);
+}
+
 // Wide layers (window > kMaxSec sectors): same arithmetic and lane mapping,
 // one layer per launch, scalar loads through the column-block address map.
 template <typename TV>
@@ -1266,10 +1576,36 @@ void* pick_co(uint32_t nsec, int nl, int variant, int* smem) {
 #undef ARA_CO_V
 }
 
+template <typename TV, int NLB, int BUDGET_KB, int MINB>
+void* pick_nsec_cq(uint32_t nsec, int* smem) {
+    if (nsec <= 1) {
+        *smem = CqGeo<TV, 1, BUDGET_KB, MINB>::BYTES;
+        return (void*)trial_kernel_cq<TV, 1, NLB, BUDGET_KB, MINB>;
+    }
+    if (nsec <= 2) {
+        *smem = CqGeo<TV, 2, BUDGET_KB, MINB>::BYTES;
+        return (void*)trial_kernel_cq<TV, 2, NLB, BUDGET_KB, MINB>;
+    }
+    *smem = CqGeo<TV, 4, BUDGET_KB, MINB>::BYTES;
+    return (void*)trial_kernel_cq<TV, 4, NLB, BUDGET_KB, MINB>;
+}
+
+// two CTAs/SM: a 2-stage row ring (64 KB) plus the id/occupancy rings per CTA
+template <typename TV>
+void* pick_cq(uint32_t nsec, int nl, int variant, int* smem) {
+    (void)variant;
+#define ARA_CQ_V(NLB) return pick_nsec_cq<TV, NLB, 64, 2>(nsec, smem);
+    if (nl <= 1) { ARA_CQ_V(1) }
+    if (nl <= 2) { ARA_CQ_V(2) }
+    ARA_CQ_V(4)
+#undef ARA_CQ_V
+}
+
 // variant: 0 = register-pipelined, 1 = shared-memory staged (cp.async ring),
 // 2-4 = register + L2 prefetch, 5-7 = register at higher occupancy,
 // 8 = TMA gather4 ring (needs p.tmap; windows of <= 4 sectors in one block),
-// 10-13 = cooperative cp.async ring (whole rows per instruction) at 1/2/3 CTAs/SM.
+// 10-13 = cooperative cp.async ring (whole rows per instruction) at 1/2/3 CTAs/SM,
+// 14 = compacted rounds over the cooperative ring (skips zero rows' arithmetic).
 void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
     *smem = 0;
     if (variant == 8 && nsec <= 4)
@@ -1278,6 +1614,8 @@ void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
     if (variant == 1) return fp32 ? pick_sm<float>(nsec, nl, smem) : pick_sm<double>(nsec, nl, smem);
     if (variant >= 10 && variant <= 13 && nsec <= 4)
         return fp32 ? pick_co<float>(nsec, nl, variant, smem) : pick_co<double>(nsec, nl, variant, smem);
+    if (variant == 14 && nsec <= 4)
+        return fp32 ? pick_cq<float>(nsec, nl, variant, smem) : pick_cq<double>(nsec, nl, variant, smem);
     return fp32 ? pick<float>(nsec, nl, variant) : pick<double>(nsec, nl, variant);
 }
 
