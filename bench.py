@@ -191,6 +191,14 @@ def kernel_name(variant):
     return KERNEL_NAMES.get(int(variant), f"ara::trial_kernel (ARA_KERNEL={variant})")
 
 
+def l2_gather_peak():
+    """Measured L2 gather ceiling (GB/s): random 32-B gathers from an L2-resident table."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "r01_microbench.json")))["gather_16MB_32B_gbs"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def load_traffic(w, precision, variant):
     """DRAM bytes (and L2 sectors) per launch of the ARA kernel from the
     committed ncu --set full capture of the same kernel variant, or None."""
@@ -491,6 +499,10 @@ def main():
                          "dram_achieved": (traffic / (k_ms * 1e6)) if (traffic and a.mode == "direct") else None,
                          "dram_frac": (traffic / (k_ms * 1e6) / peak) if (traffic and a.mode == "direct") else None,
                          "l2_sector_bytes": (32 * trec["l2_sectors_per_launch"]) if trec else None,
+                         # L2 -> SM sector traffic against the measured L2 gather ceiling
+                         # (profiles/r01_microbench.json: random 32-B gathers, L2-resident table)
+                         "l2_frac": (32 * trec["l2_sectors_per_launch"] / (k_ms * 1e6) / l2_gather_peak())
+                         if (trec and l2_gather_peak()) else None,
                          "traffic_source": trec.get("source") if trec else None},
             "breakdown_ms": {"ara_kernel": k_ms, "allgather": float(np.mean(ag_ms)), "metrics": float(np.mean(met_ms)),
                              "step": ms,

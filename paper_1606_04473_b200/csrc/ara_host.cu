@@ -398,10 +398,16 @@ ara_status densify_local(ara_ctx* ctx, uint32_t n_elts, uint64_t nrec, const Spa
     CK(launch_densify(sp.off, sp.ev, sp.ls, n_elts, nrec, ctx->catalog, ctx->d_table, ctx->geo, fp32, ctx->d_err,
                       ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    // occupied-row counters per column block: into the pinned scratch when they fit (same sync)
+    const uint32_t nb = ctx->geo.n_blocks;
+    const void* d_occ = static_cast<const char*>(ctx->d_table) + ctx->geo.occ_off;
+    uint32_t* h_occ = reinterpret_cast<uint32_t*>(ctx->h_small + 16);
+    const bool small = nb <= 96;
+    if (small) CK(cudaMemcpyAsync(h_occ, d_occ, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    ctx->occ_rows.assign(ctx->geo.n_blocks, 0u);
-    CK(cudaMemcpy(ctx->occ_rows.data(), static_cast<const char*>(ctx->d_table) + ctx->geo.occ_off,
-                  ctx->geo.n_blocks * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    ctx->occ_rows.assign(nb, 0u);
+    if (small) std::memcpy(ctx->occ_rows.data(), h_occ, nb * sizeof(uint32_t));
+    else CK(cudaMemcpy(ctx->occ_rows.data(), d_occ, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     return device_errors(ctx, (uint32_t)(ctx->h_small[0] & 0xffffffffu));
 }
 
@@ -1128,7 +1134,14 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         CK(cudaMemcpy2DAsync(lossy, T_local * sizeof(uint32_t), d_lossy, ld * sizeof(uint32_t),
                              T_local * sizeof(uint32_t), n_layers, kind, s));
     }
-    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    if (world > 1) {   // every rank must see the same verdict: max of the error words, on the device
+        CK(cudaMemsetAsync(ctx->d_small, 0, sizeof(uint64_t), s));
+        CK(cudaMemcpyAsync(ctx->d_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        NK(ncclAllReduce(ctx->d_small, ctx->d_small, 1, ncclUint64, ncclMax, ctx->comm, s));
+        CK(cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    } else {
+        CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    }
     if (T_local) {
         CK(cudaMemcpyAsync(ctx->h_small + 1, ctx->d_off, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(ctx->h_small + 2, ctx->d_off + T_local, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
@@ -1136,15 +1149,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     CK(cudaEventRecord(ctx->ev[5], s));
     CK(cudaStreamSynchronize(s));
     if (stream_in) CK(cudaStreamSynchronize(ctx->copy_stream));
-    uint32_t bits = (uint32_t)(ctx->h_small[0] & 0xffffffffu);
-    if (world > 1) {   // every rank must see the same verdict
-        ctx->h_small[0] = bits;
-        CK(cudaMemcpyAsync(ctx->d_small, ctx->h_small, sizeof(uint64_t), cudaMemcpyHostToDevice, s));
-        NK(ncclAllReduce(ctx->d_small, ctx->d_small, 1, ncclUint64, ncclMax, ctx->comm, s));
-        CK(cudaMemcpyAsync(ctx->h_small + 3, ctx->d_small, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        bits = (uint32_t)ctx->h_small[3];
-    }
+    const uint32_t bits = (uint32_t)(ctx->h_small[0] & 0xffffffffu);
     st = device_errors(ctx, bits);
     if (st != ARA_OK) {
         ctx->last_layers = 0;
@@ -1203,7 +1208,7 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
     const int maxblk = (2 * ctx->n_sm + (int)rows - 1) / (int)rows;
     if (nblk > maxblk) nblk = maxblk;
     if (nblk < 1) nblk = 1;
-    CK(metrics_alloc(ctx->ms, rows, n_rp, nblk));
+    CK(metrics_alloc(ctx->ms, rows, n_rp, nblk > 2 * ctx->n_sm ? nblk : 2 * ctx->n_sm));   // + cooperative grid
     cudaStream_t s = ctx->stream;
     CK(cudaEventRecord(ctx->ev[0], s));
     CK(launch_metrics(d_y, T, ld, rows, n_rp, hk, ctx->ms, nblk, s));

@@ -134,6 +134,7 @@ struct MetricsScratch {
     uint64_t* part_cnt = nullptr;   // [rows][n_rp][nblk]
     double* out = nullptr;          // [rows][n_rp][2] pml, tvar
     uint32_t* done = nullptr;       // block-completion counters
+    uint32_t* coop_hist = nullptr;  // [3][rows * n_rp][256] rotating histograms (cooperative path)
     size_t cap_rows_rp = 0;
     uint32_t cap_rows = 0;
     int nblk = 0;                   // capacity in blocks

@@ -19,6 +19,7 @@ def main():
     import synth
     from paper_1606_04473_b200 import ara
     name, n_trials, out = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+    rho = float(sys.argv[4]) if len(sys.argv) > 4 else None
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
@@ -26,6 +27,8 @@ def main():
     obj = [ara.ara_nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     w = synth.get_config(name).with_(n_trials=n_trials)
+    if rho is not None:
+        w = w.with_(rho=rho)
     first, count = ara.ara_partition(w.n_trials, world, rank)
     off, ids = synth.gen_yet(w, first=first, n=count)
     with ara.Context(w.catalog, device=local, rank=rank, world=world, nccl_id=obj[0]) as ctx:

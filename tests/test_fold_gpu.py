@@ -69,6 +69,7 @@ def test_fold_fullsize_equals_direct(cuda):
         with ara.Context(w.catalog, run_mode=mode, stream=torch.cuda.current_stream()) as ctx:
             ctx.load_elts(eo, ev, ls, w.elt_terms())
             ctx.load_yet(w.n_trials, 0, d_off, d_ids)
+            ctx.run(w.layers, y)            # first launch (module loading) untimed
             st = ctx.run(w.layers, y)
         torch.cuda.synchronize()
         out.append((y.cpu().numpy(), st))

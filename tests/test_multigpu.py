@@ -29,8 +29,9 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("name,n_trials", [("tiny", 1000), ("tiny", 997), ("mini", 20_000)])
-def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials):
+@pytest.mark.parametrize("name,n_trials,rho", [("tiny", 1000, None), ("tiny", 997, None), ("mini", 20_000, None),
+                                               ("mini", 20_001, 0.01)])
+def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials, rho):
     n = _ngpu()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -38,12 +39,14 @@ def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials):
     out = str(tmp_path / "r0.npz")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(HERE, "mgpu_worker.py"),
-           name, str(n_trials), out]
+           name, str(n_trials), out] + ([str(rho)] if rho is not None else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     got = np.load(out)
     assert bool(got["same"])
     w = synth.get_config(name).with_(n_trials=n_trials)
+    if rho is not None:        # sparse ELTs: zero rows skipped, compacted rounds on every rank
+        w = w.with_(rho=rho)
     off, ids, elts = make_inputs(w)
     R = [x for x in w.return_periods if x <= w.n_trials]
     ylt, _, _, met = run_gpu(off, ids, elts, w, w.layers, return_periods=R)

@@ -89,9 +89,10 @@ def _edge_yet(C, rng):
 
 
 @pytest.mark.parametrize("variant", KERNEL_VARIANTS)
-def test_edge_trials_and_unaligned_layers(cuda, variant):
+@pytest.mark.parametrize("rho", [0.5, 0.04])
+def test_edge_trials_and_unaligned_layers(cuda, variant, rho):
     rng = np.random.default_rng(9)
-    w = synth.get_config("tiny").with_(n_elts=5, catalog=777, rho=0.5, n_trials=16)
+    w = synth.get_config("tiny").with_(n_elts=5, catalog=777, rho=rho, n_trials=16)
     _, _, elts = make_inputs(w)
     off, ids = _edge_yet(w.catalog, rng)
     layers = (synth.LayerSpec(0, 5, 2.5e4, 5e5, 6.5e5, 2.5e6), synth.LayerSpec(1, 4, 0.0, INF, 0.0, INF),
@@ -105,11 +106,13 @@ def test_edge_trials_and_unaligned_layers(cuda, variant):
 
 
 @pytest.mark.parametrize("variant", KERNEL_VARIANTS)
-def test_wide_windows_tower_and_many_layers(cuda, variant):
+@pytest.mark.parametrize("rho", [0.2, 0.01])
+def test_wide_windows_tower_and_many_layers(cuda, variant, rho):
     """40 ELTs: aligned, unaligned, 8-sector, >8-sector (generic kernel) and
     single-ELT layers; 4 identical windows (shared-load path); 9 layers ->
-    three launches with the portfolio accumulated across them."""
-    w = synth.get_config("tiny").with_(n_elts=40, catalog=3000, rho=0.2, n_trials=700, nmin=1, nmax=300)
+    three launches with the portfolio accumulated across them.  rho = 0.01
+    makes every column block sparse (zero rows skipped, compacted rounds)."""
+    w = synth.get_config("tiny").with_(n_elts=40, catalog=3000, rho=rho, n_trials=700, nmin=1, nmax=300)
     off, ids, elts = make_inputs(w)
     rng = np.random.default_rng(4)
     d = rng.uniform(0, 2e4, w.n_elts)
@@ -139,10 +142,11 @@ def test_single_elt_single_event_lookup(cuda):
 
 # ------------------------------------------------------------------ invariants
 @pytest.mark.parametrize("variant", KERNEL_VARIANTS)
-def test_partition_and_alignment_invariance(cuda, variant):
+@pytest.mark.parametrize("rho", [0.3, 0.03])
+def test_partition_and_alignment_invariance(cuda, variant, rho):
     """P11 on the GPU: shards loaded as independent YETs (different base
     alignment of every trial) reproduce the unsharded YLT bit for bit."""
-    w = synth.get_config("tiny").with_(n_trials=1001)
+    w = synth.get_config("tiny").with_(n_trials=1001, rho=rho)
     off, ids, elts = make_inputs(w)
     full, _, _, _ = run_gpu(off, ids, elts, w, w.layers, variant=variant)
     for v2 in KERNEL_VARIANTS:                  # every kernel: same summation order, same bits
@@ -181,9 +185,10 @@ def test_monotone_in_retentions_and_bounded(cuda):
 
 
 @pytest.mark.parametrize("pinned", [True, False])
-def test_chunked_h2d_equals_all_at_once(cuda, pinned):
+@pytest.mark.parametrize("rho", [0.3, 0.03])
+def test_chunked_h2d_equals_all_at_once(cuda, pinned, rho):
     import torch
-    w = synth.get_config("tiny").with_(n_trials=3000)
+    w = synth.get_config("tiny").with_(n_trials=3000, rho=rho)
     off, ids, elts = make_inputs(w)
     ref, ref_lossy, _, _ = run_gpu(off, ids, elts, w, w.layers)
     if pinned:
@@ -212,6 +217,21 @@ def test_set_elt_terms_equals_fresh_load(cuda):
         ctx.set_elt_terms((d2, li2))
         b, _, _ = ctx.run_host(w.layers)
     assert np.array_equal(b, fresh) and not np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("rows_rho", [(1, 0.3), (3, 0.02)])
+def test_metrics_single_launch_path_matches_oracle(cuda, rows_rho):
+    """ARA_METRICS_COOP=1: the cooperative single-launch radix select gives the
+    oracle's PML (bit for bit) and TVaR, like the default multi-launch path."""
+    n_layers, rho = rows_rho
+    w = synth.get_config("tiny").with_(n_trials=5003, rho=rho, return_periods=(1, 2, 3.5, 10, 100, 1000, 5003))
+    layers = tuple(synth.LayerSpec(0, 3, 2.5e4 * (i + 1), 5e5, 6.5e6 / (i + 1), 2.5e6) for i in range(n_layers))
+    off, ids, elts = make_inputs(w)
+    orc = run_oracle(off, ids, elts, w, layers)
+    _, _, _, met = run_gpu(off, ids, elts, w, layers, return_periods=w.return_periods, env={"ARA_METRICS_COOP": 1})
+    _, _, _, met0 = run_gpu(off, ids, elts, w, layers, return_periods=w.return_periods)
+    assert_metrics_close(met, oracle_rows(orc), orc["scale"], w.return_periods)
+    assert np.array_equal(met[1], met0[1]) and np.allclose(met[2], met0[2], rtol=1e-12, atol=0)
 
 
 def test_metrics_ties_extremes(cuda):
