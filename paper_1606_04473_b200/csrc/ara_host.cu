@@ -327,12 +327,15 @@ ara_status check_terms(ara_ctx* ctx, uint32_t n, const ara_elt_terms* t) {
 // (Re)allocate the column-blocked table for n_elts ELTs (ara::TableGeo).
 ara_status alloc_table(ara_ctx* ctx, uint32_t n_elts) {
     const TableGeo g = table_geometry(n_elts, ctx->catalog, ctx->precision == ARA_F32_STORAGE);
-    if (g.bytes != ctx->table_bytes) {
-        cudaFree(ctx->d_table);
-        ctx->d_table = nullptr;
-        ctx->table_bytes = 0;
-        CK(cudaMalloc(&ctx->d_table, g.bytes));
-        ctx->table_bytes = g.bytes;
+    if (g.bytes != ctx->table_bytes || g.epb != ctx->geo.epb || g.n_blocks != ctx->geo.n_blocks) {
+        ctx->table_clean = false;
+        if (g.bytes != ctx->table_bytes) {
+            cudaFree(ctx->d_table);
+            ctx->d_table = nullptr;
+            ctx->table_bytes = 0;
+            CK(cudaMalloc(&ctx->d_table, g.bytes));
+            ctx->table_bytes = g.bytes;
+        }
     }
     ctx->geo = g;
     return ARA_OK;
@@ -393,7 +396,11 @@ ara_status densify_local(ara_ctx* ctx, uint32_t n_elts, uint64_t nrec, const Spa
     const int fp32 = ctx->precision == ARA_F32_STORAGE;
     ara_status ast = alloc_table(ctx, n_elts);
     if (ast != ARA_OK) return ast;
-    CK(cudaMemsetAsync(ctx->d_table, 0, ctx->table_bytes, ctx->stream));
+    // a table whose non-zero rows are all marked in its bitmaps (a previous
+    // densify) is cleared row by row; otherwise the whole allocation is zeroed
+    if (ctx->table_clean) CK(launch_clear_rows(ctx->d_table, ctx->geo, ctx->catalog, ctx->stream));
+    else CK(cudaMemsetAsync(ctx->d_table, 0, ctx->table_bytes, ctx->stream));
+    ctx->table_clean = false;
     CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(uint32_t), ctx->stream));
     CK(launch_densify(sp.off, sp.ev, sp.ls, n_elts, nrec, ctx->catalog, ctx->d_table, ctx->geo, fp32, ctx->d_err,
                       ctx->stream));
@@ -408,6 +415,7 @@ ara_status densify_local(ara_ctx* ctx, uint32_t n_elts, uint64_t nrec, const Spa
     ctx->occ_rows.assign(nb, 0u);
     if (small) std::memcpy(ctx->occ_rows.data(), h_occ, nb * sizeof(uint32_t));
     else CK(cudaMemcpy(ctx->occ_rows.data(), d_occ, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    ctx->table_clean = true;   // every stored element's row is marked (even for rejected ELTs)
     return device_errors(ctx, (uint32_t)(ctx->h_small[0] & 0xffffffffu));
 }
 

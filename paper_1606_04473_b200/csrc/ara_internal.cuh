@@ -113,6 +113,8 @@ cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const d
                            uint32_t n_elts, uint64_t n_records, uint32_t catalog, void* d_table,
                            const TableGeo& geo, int fp32, uint32_t* d_err, cudaStream_t s);
 
+// zero exactly the rows the occupancy bitmaps mark, then the bitmaps and counters
+cudaError_t launch_clear_rows(void* d_table, const TableGeo& geo, uint32_t catalog, cudaStream_t s);
 cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int grid, int variant, cudaStream_t s);
 int trial_kernel_grid(int fp32, uint32_t max_nsec, int n_layers, int variant);
 void set_ldg_carveout(int fp32, uint32_t nsec, int nl, int pct);
@@ -220,5 +222,6 @@ struct ara_ctx {
     int pf_sectors = 1;               // ARA_PFN
     bool no_skip = false;             // ARA_NO_SKIP=1: never skip zero rows via the occupancy bitmap (A/B)
     std::vector<uint32_t> occ_rows;   // occupied rows per column block (from densify)
+    bool table_clean = false;         // table content is exactly described by its occupancy bitmaps
     cudaEvent_t ev[8] = {};
 };

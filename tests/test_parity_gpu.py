@@ -203,6 +203,28 @@ def test_chunked_h2d_equals_all_at_once(cuda, pinned, rho):
         assert st["h2d_bytes"] == ids.nbytes + off.nbytes
 
 
+@pytest.mark.parametrize("rho_a,rho_b", [(0.3, 0.02), (0.02, 0.3), (0.02, 0.02)])
+def test_reload_elts_equals_fresh_context(cuda, rho_a, rho_b):
+    """Reloading ELTs into a used context (the table is cleared row by row via
+    the previous load's occupancy bitmap, not re-zeroed in full) gives exactly
+    the YLT of a fresh context."""
+    from paper_1606_04473_b200 import ara
+    wa = synth.get_config("tiny").with_(rho=rho_a)
+    wb = synth.get_config("tiny").with_(rho=rho_b, seed=wa.seed + 7)
+    off, ids = synth.gen_yet(wb)
+    ea, eb = synth.gen_elts(wa), synth.gen_elts(wb)
+    with ara.Context(wb.catalog) as ctx:
+        ctx.load_elts(*ea, wa.elt_terms())
+        ctx.load_yet(wb.n_trials, 0, off, ids)
+        ctx.run_host(wb.layers)
+        ctx.load_elts(*eb, wb.elt_terms())
+        ylt, lossy, _ = ctx.run_host(wb.layers)
+    fresh, flossy, _, _ = run_gpu(off, ids, eb, wb, wb.layers)
+    assert np.array_equal(ylt, fresh) and np.array_equal(lossy, flossy)
+    orc = run_oracle(off, ids, eb, wb, wb.layers)
+    assert_ylt_close(ylt, orc)
+
+
 def test_set_elt_terms_equals_fresh_load(cuda):
     ara = _ara()
     w = synth.get_config("tiny")
