@@ -143,11 +143,13 @@ class ClockSampler:
 
 def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str = "direct",
                       occupancy: float = 1.0) -> int:
-    """DESIGN.md section 6 "Algorithmic bytes".  Direct mode, per launch (layers
-    sharing one row window share a launch): per event 4 B of id, plus -- when
-    zero rows are skipped (occupancy < 1) -- the 4-B occupancy word, plus the
-    32-B sectors of the launch's row window for the occupied fraction of events;
-    per trial 8 B of offsets + 8 B per YLT row.  Fold mode: the fold pass reads
+    """DESIGN.md section 6 "Algorithmic bytes": the north star's count, YET
+    bytes streamed + 32 B per gathered ELT sector.  Direct mode, per launch
+    (layers sharing one row window share a launch): per event 4 B of id, plus
+    -- when zero rows are skipped (occupancy < 1) -- the sector holding the
+    event's row-occupancy bit, plus the 32-B sectors of the launch's row window
+    for the occupied fraction of events; per trial 8 B of offsets + 8 B per
+    YLT row.  Fold mode: the fold pass reads
     every catalogue row window once and writes 8 B per (event id, layer); the
     trial pass reads 4 B of id + one fold row (8 B x layers, padded to a power
     of two) per event."""
@@ -170,7 +172,7 @@ def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str
                    + per_trial)
     per_event = 0.0
     for (a, b), _ in windows:
-        per_event += 4 + (4 if occupancy < 1.0 else 0) + occupancy * 32 * (b - a)
+        per_event += 4 + (32 if occupancy < 1.0 else 0) + occupancy * 32 * (b - a)
     return int(n_events * per_event + per_trial)
 
 
@@ -498,6 +500,7 @@ def main():
                          # serves, so frac can exceed 1; the DRAM-level figure is traffic / time
                          "dram_achieved": (traffic / (k_ms * 1e6)) if (traffic and a.mode == "direct") else None,
                          "dram_frac": (traffic / (k_ms * 1e6) / peak) if (traffic and a.mode == "direct") else None,
+                         "l2_hit_rate_pct": trec.get("l2_hit_rate_pct") if trec else None,
                          "l2_sector_bytes": (32 * trec["l2_sectors_per_launch"]) if trec else None,
                          # L2 -> SM sector traffic against the measured L2 gather ceiling
                          # (profiles/r01_microbench.json: random 32-B gathers, L2-resident table)

@@ -175,17 +175,26 @@ __global__ void __launch_bounds__(256) radix_pass_kernel(const __grid_constant__
 }
 
 __global__ void __launch_bounds__(256) tail_kernel(const __grid_constant__ MParams P) {
-    __shared__ double s_sum[256];
-    __shared__ uint64_t s_cnt[256];
+    // RC return periods per sweep over the row (each accumulator is the same
+    // per-thread sequential sum over the same keys as a one-period sweep)
+    constexpr int RC = 8;
+    __shared__ double s_sum[RC][256];
+    __shared__ uint64_t s_cnt[RC][256];
     __shared__ uint32_t s_last;
     const uint32_t row = blockIdx.y, n_rp = P.n_rp;
     const double* y = P.ylt + (uint64_t)row * P.ld;
     constexpr int KB = 8;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint32_t r = 0; r < n_rp; ++r) {
-        const double v = __longlong_as_double((long long)P.prefix[row * n_rp + r]);
-        double s = 0.0;
-        uint64_t c = 0;
+    for (uint32_t r0 = 0; r0 < n_rp; r0 += RC) {
+        double v[RC], s[RC];
+        uint64_t c[RC];
+#pragma unroll
+        for (int j = 0; j < RC; ++j) {
+            // periods past n_rp compare against +inf: nothing is added
+            v[j] = r0 + j < n_rp ? __longlong_as_double((long long)P.prefix[row * n_rp + r0 + j]) : INFINITY;
+            s[j] = 0.0;
+            c[j] = 0;
+        }
         for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < P.T; i0 += stride * KB) {
             double xs[KB];
 #pragma unroll
@@ -195,21 +204,30 @@ __global__ void __launch_bounds__(256) tail_kernel(const __grid_constant__ MPara
             }
 #pragma unroll
             for (int q = 0; q < KB; ++q)   // fixed order per thread: deterministic
-                if (xs[q] > v) { s = __dadd_rn(s, xs[q]); ++c; }
+#pragma unroll
+                for (int j = 0; j < RC; ++j)
+                    if (xs[q] > v[j]) { s[j] = __dadd_rn(s[j], xs[q]); ++c[j]; }
         }
-        s_sum[threadIdx.x] = s;
-        s_cnt[threadIdx.x] = c;
+#pragma unroll
+        for (int j = 0; j < RC; ++j) {
+            s_sum[j][threadIdx.x] = s[j];
+            s_cnt[j][threadIdx.x] = c[j];
+        }
         __syncthreads();
         for (int w = 128; w >= 1; w >>= 1) {
             if ((int)threadIdx.x < w) {
-                s_sum[threadIdx.x] = __dadd_rn(s_sum[threadIdx.x], s_sum[threadIdx.x + w]);
-                s_cnt[threadIdx.x] += s_cnt[threadIdx.x + w];
+#pragma unroll
+                for (int j = 0; j < RC; ++j) {
+                    s_sum[j][threadIdx.x] = __dadd_rn(s_sum[j][threadIdx.x], s_sum[j][threadIdx.x + w]);
+                    s_cnt[j][threadIdx.x] += s_cnt[j][threadIdx.x + w];
+                }
             }
             __syncthreads();
         }
-        if (threadIdx.x == 0) {
-            P.part_sum[((uint64_t)row * n_rp + r) * P.nblk + blockIdx.x] = s_sum[0];
-            P.part_cnt[((uint64_t)row * n_rp + r) * P.nblk + blockIdx.x] = s_cnt[0];
+        if (threadIdx.x < RC && r0 + threadIdx.x < n_rp) {
+            const uint32_t r = r0 + threadIdx.x;
+            P.part_sum[((uint64_t)row * n_rp + r) * P.nblk + blockIdx.x] = s_sum[threadIdx.x][0];
+            P.part_cnt[((uint64_t)row * n_rp + r) * P.nblk + blockIdx.x] = s_cnt[threadIdx.x][0];
         }
         __syncthreads();
     }

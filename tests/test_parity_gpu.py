@@ -106,6 +106,38 @@ def test_edge_trials_and_unaligned_layers(cuda, variant, rho):
 
 
 @pytest.mark.parametrize("variant", KERNEL_VARIANTS)
+def test_compacted_rounds_fifo_pressure(cuda, variant):
+    """Sparse table, adversarial occupancy patterns for the compacted-rounds
+    kernel: every event occupied (every lane's FIFO full on every sub-step),
+    occupied events on one lane only, alternating, none, and random."""
+    rng = np.random.default_rng(11)
+    w = synth.get_config("tiny").with_(catalog=5000, rho=0.03, n_trials=8)
+    _, _, elts = make_inputs(w)
+    occupied = np.unique(elts[1])
+    empty = np.setdiff1d(np.arange(1, w.catalog + 1), occupied)
+    hot, cold = int(occupied[0]), int(empty[0])
+    trials = [
+        np.full(3000, hot),                                          # all occupied
+        np.where(np.arange(2000) % 32 == 5, hot, cold),             # one lane only
+        np.where(np.arange(1500) % 2 == 0, hot, cold),              # alternating
+        np.full(700, cold),                                          # none
+        rng.choice(occupied, 1000),                                  # random occupied ids
+        rng.integers(1, w.catalog + 1, 4097),                        # random
+        np.array([hot]),
+        np.array([], dtype=np.int64),
+    ]
+    off = np.zeros(len(trials) + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(t) for t in trials])
+    ids = np.concatenate(trials).astype(np.uint32)
+    orc = run_oracle(off, ids, elts, w, w.layers)
+    ylt, lossy, _, _ = run_gpu(off, ids, elts, w, w.layers, variant=variant)
+    assert_ylt_close(ylt, orc)
+    assert np.array_equal(lossy, orc["lossy"])
+    ylt2, lossy2, _, _ = run_gpu(off, ids, elts, w, w.layers, variant=variant, env={"ARA_NO_SKIP": 1})
+    assert np.array_equal(ylt, ylt2) and np.array_equal(lossy, lossy2)
+
+
+@pytest.mark.parametrize("variant", KERNEL_VARIANTS)
 @pytest.mark.parametrize("rho", [0.2, 0.01])
 def test_wide_windows_tower_and_many_layers(cuda, variant, rho):
     """40 ELTs: aligned, unaligned, 8-sector, >8-sector (generic kernel) and
