@@ -230,6 +230,7 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
     if (const char* v = getenv("ARA_KERNEL")) ctx->kernel_variant = atoi(v);
     if (const char* v = getenv("ARA_PFN")) ctx->pf_sectors = atoi(v);
     if (const char* v = getenv("ARA_NO_SKIP")) ctx->no_skip = atoi(v) != 0;
+    if (const char* v = getenv("ARA_NO_P2P")) ctx->use_p2p = atoi(v) == 0;
     if (const char* v = getenv("ARA_BATCH")) ctx->batch = (uint32_t)atoi(v) ? (uint32_t)atoi(v) : 4u;
     auto bail = [&](ara_status st) {
         ara_destroy(ctx);
@@ -281,6 +282,11 @@ extern "C" void ara_destroy(ara_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     release_yet(ctx);
+    for (int b = 0; b < 2; ++b) {   // peers' global YLTs mapped by IPC, then our own
+        for (int r = 0; r < ctx->world && r < ara::kMaxPeers; ++r)
+            if (ctx->peer_p2p[b][r] && r != ctx->rank) cudaIpcCloseMemHandle(ctx->peer_p2p[b][r]);
+        cudaFree(ctx->d_p2p[b]);
+    }
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     cudaFree(ctx->d_table);
     cudaFree(ctx->d_off_own);
@@ -768,6 +774,72 @@ extern "C" ara_status ara_run_portfolio(ara_ctx* ctx, uint32_t n_programs, const
 
 namespace {
 
+// ---- fused YLT assembly over NVLink (world > 1; SURVEY §8e "fused P2P epilogue")
+void p2p_release(ara_ctx* ctx) {
+    for (int b = 0; b < 2; ++b) {
+        for (int r = 0; r < ctx->world && r < kMaxPeers; ++r)
+            if (ctx->peer_p2p[b][r] && r != ctx->rank) cudaIpcCloseMemHandle(ctx->peer_p2p[b][r]);
+        for (int r = 0; r < kMaxPeers; ++r) ctx->peer_p2p[b][r] = nullptr;
+        cudaFree(ctx->d_p2p[b]);
+        ctx->d_p2p[b] = nullptr;
+    }
+    ctx->p2p_cap = 0;
+    cudaGetLastError();
+}
+
+// Collective: make sure both global-YLT buffers hold `need` doubles and every
+// rank has every other rank's buffers mapped (CUDA IPC handles exchanged with
+// one NCCL all-gather).  All ranks reach the same verdict (an all-reduce of
+// the per-rank outcome); on failure the run falls back to ncclAllGather.
+ara_status p2p_ensure(ara_ctx* ctx, size_t need) {
+    if (ctx->p2p_state < 0) return ARA_OK;
+    if (ctx->p2p_state > 0 && ctx->p2p_cap >= need) return ARA_OK;
+    const int world = ctx->world, rank = ctx->rank;
+    cudaStream_t s = ctx->stream;
+    p2p_release(ctx);
+    uint64_t ok = 1;
+    cudaIpcMemHandle_t mine[2];
+    for (int b = 0; b < 2 && ok; ++b) {
+        if (cudaMalloc(&ctx->d_p2p[b], need * sizeof(double)) != cudaSuccess ||
+            cudaIpcGetMemHandle(&mine[b], ctx->d_p2p[b]) != cudaSuccess)
+            ok = 0;
+    }
+    if (!ok) std::memset(mine, 0, sizeof(mine));
+    cudaGetLastError();
+    // exchange the handles: [world][2] x 64 B
+    const size_t hb = sizeof(mine);
+    char* d_h = nullptr;
+    CK(cudaMalloc(&d_h, hb * (size_t)(world + 1)));
+    CK(cudaMemcpyAsync(d_h + hb * (size_t)world, mine, hb, cudaMemcpyHostToDevice, s));
+    NK(ncclAllGather(d_h + hb * (size_t)world, d_h, hb, ncclChar, ctx->comm, s));
+    std::vector<cudaIpcMemHandle_t> all((size_t)world * 2);
+    CK(cudaMemcpyAsync(all.data(), d_h, hb * (size_t)world, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(d_h);
+    for (int r = 0; r < world && ok; ++r)
+        for (int b = 0; b < 2 && ok; ++b) {
+            if (r == rank) { ctx->peer_p2p[b][r] = ctx->d_p2p[b]; continue; }
+            void* ptr = nullptr;
+            if (cudaIpcOpenMemHandle(&ptr, all[(size_t)r * 2 + b], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) ok = 0;
+            else ctx->peer_p2p[b][r] = static_cast<double*>(ptr);
+        }
+    cudaGetLastError();
+    // every rank must agree
+    ctx->h_small[0] = ok;
+    CK(cudaMemcpyAsync(ctx->d_small, ctx->h_small, sizeof(uint64_t), cudaMemcpyHostToDevice, s));
+    NK(ncclAllReduce(ctx->d_small, ctx->d_small, 1, ncclUint64, ncclMin, ctx->comm, s));
+    CK(cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (ctx->h_small[0] == 1) {
+        ctx->p2p_state = 1;
+        ctx->p2p_cap = need;
+    } else {
+        p2p_release(ctx);
+        ctx->p2p_state = -1;
+    }
+    return ARA_OK;
+}
+
 ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint32_t n_programs,
                     const uint32_t* program_layers, double* ylt, uint32_t* lossy, ara_run_stats* stats) {
     const uint32_t world = (uint32_t)ctx->world;
@@ -905,7 +977,26 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     // Kernels.
     const TableGeo& geo = ctx->geo;
     const uint32_t spb = geo.epb / eps;   // sectors per block row
+    // Fused YLT assembly: one launch group per chunk (no wide layers, no
+    // programs, one fold chunk) with a kernel whose epilogue stores to peers.
+    bool p2p_ok_kernel = ctx->kernel_variant < 0 || ctx->kernel_variant == 0 || ctx->kernel_variant == 5 ||
+                         ctx->kernel_variant == 12 || ctx->kernel_variant == 14;
+    bool single_group = groups.size() == 1 && !groups[0].wide && n_programs == 0 &&
+                        (!fold || (n_layers + nlc - 1) / nlc == 1) && world <= (uint32_t)kMaxPeers;
+    bool use_p2p = false;
+    if (world > 1 && ctx->use_p2p && p2p_ok_kernel && single_group) {
+        st = p2p_ensure(ctx, (size_t)rows * T_global);
+        if (st != ARA_OK) return st;
+        use_p2p = ctx->p2p_state > 0;
+    }
+    const int p2p_buf = ctx->p2p_next;
     TrialParams base{};
+    if (use_p2p) {
+        base.n_peers = world;
+        for (uint32_t r = 0; r < world; ++r) base.peer_ylt[r] = ctx->peer_p2p[p2p_buf][r];
+        base.peer_ld = T_global;
+        base.peer_t0 = ctx->first;
+    }
     base.off = ctx->d_off;
     base.ids = ctx->d_ids;
     base.catalog = ctx->catalog;
@@ -1097,11 +1188,17 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         ctx->chunked_pending = false;   // later runs reuse the device copy
     }
 
-    // YLT assembly across ranks (a9): one all-gather per YLT row over NVLink.
+    // YLT assembly across ranks (a9).  Fused path: the kernels already stored
+    // every trial's YLT entries into every rank's global buffer over NVLink;
+    // the all-reduce of the error words below is the barrier after which all
+    // of them are complete.  Otherwise one ncclAllGather per YLT row.
     double* d_full = ctx->d_ylt_local;
     uint64_t ld_full = ld;
     CK(cudaEventRecord(ctx->ev[3], s));
-    if (world > 1) {
+    if (use_p2p) {
+        d_full = ctx->d_p2p[p2p_buf];
+        ld_full = T_global;
+    } else if (world > 1) {
         st = ensure(ctx, ctx->d_ylt_gather, ctx->ylt_gather_cap, (size_t)rows * world * Tpad);
         if (st != ARA_OK) return st;
         NK(ncclGroupStart());
@@ -1126,6 +1223,12 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         }
         ld_full = T_global;
     }
+    if (world > 1) {   // every rank must see the same verdict: max of the error words, on the device
+        CK(cudaMemsetAsync(ctx->d_small, 0, sizeof(uint64_t), s));
+        CK(cudaMemcpyAsync(ctx->d_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
+        NK(ncclAllReduce(ctx->d_small, ctx->d_small, 1, ncclUint64, ncclMax, ctx->comm, s));
+        CK(cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    }
     CK(cudaEventRecord(ctx->ev[4], s));
 
     // Outputs.
@@ -1142,14 +1245,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         CK(cudaMemcpy2DAsync(lossy, T_local * sizeof(uint32_t), d_lossy, ld * sizeof(uint32_t),
                              T_local * sizeof(uint32_t), n_layers, kind, s));
     }
-    if (world > 1) {   // every rank must see the same verdict: max of the error words, on the device
-        CK(cudaMemsetAsync(ctx->d_small, 0, sizeof(uint64_t), s));
-        CK(cudaMemcpyAsync(ctx->d_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToDevice, s));
-        NK(ncclAllReduce(ctx->d_small, ctx->d_small, 1, ncclUint64, ncclMax, ctx->comm, s));
-        CK(cudaMemcpyAsync(ctx->h_small, ctx->d_small, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    } else {
-        CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    }
+    if (world == 1) CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     if (T_local) {
         CK(cudaMemcpyAsync(ctx->h_small + 1, ctx->d_off, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(ctx->h_small + 2, ctx->d_off + T_local, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
@@ -1165,6 +1261,8 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     }
     ctx->last_layers = n_layers;
     ctx->last_rows = rows;
+    ctx->d_last_full = d_full;
+    if (use_p2p) ctx->p2p_next ^= 1;
     if (stats) {
         const uint64_t nev = T_local ? ctx->h_small[2] - ctx->h_small[1] : 0;
         uint64_t lookups = 0;
@@ -1204,9 +1302,7 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
     const double* d_y;
     uint64_t ld;
     if (ctx->world > 1) {
-        const uint64_t Tpad = (T + ctx->world - 1) / ctx->world;
-        if (Tpad * (uint64_t)ctx->world == T) d_y = ctx->d_ylt_gather;
-        else d_y = ctx->d_ylt_global;
+        d_y = ctx->d_last_full;   // the run's global YLT (fused buffer or all-gather output)
         ld = T;
     } else {
         d_y = ctx->d_ylt_local;

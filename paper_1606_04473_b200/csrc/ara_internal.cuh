@@ -31,6 +31,7 @@ constexpr int kMaxFoldL = 8;         // layers per folded trial launch (fold mod
 constexpr int kMaxWin = kMaxSec * kSectorBytes / 4;   // 64 columns (fp32) per window
 constexpr int kThreads = 256;        // 8 warps per CTA
 constexpr int kTablePadBytes = kMaxSec * kSectorBytes;  // over-read slack after the last row
+constexpr int kMaxPeers = 8;         // ranks whose global YLT a kernel epilogue writes over NVLink
 
 // Direct-access table geometry: ELT columns are cut
 // into blocks of `epb` elements (<= 128 B); block b is a dense [C+1][epb]
@@ -106,6 +107,12 @@ struct TrialParams {
     uint32_t fold_col0;         // fold column of the launch's first layer
     LayerWin lw[kMaxFoldL];
     double2 term[kMaxLB][kMaxWin];   // (deductible, limit) per window column
+    // fused YLT assembly (world > 1): every rank's global YLT [rows][peer_ld],
+    // mapped into this process (CUDA IPC over NVLink); 0 peers = not used
+    double* peer_ylt[kMaxPeers];
+    uint32_t n_peers;
+    uint64_t peer_ld;           // = T_global
+    uint64_t peer_t0;           // global index of local trial 0 (this rank's first trial)
 };
 
 // ---- launchers (defined in the .cu files; all enqueue on `s`)
@@ -213,6 +220,17 @@ struct ara_ctx {
     uint64_t* d_small = nullptr;
 
     ara::MetricsScratch ms;
+    // fused YLT assembly over NVLink (world > 1): two global-YLT buffers used
+    // alternately by consecutive runs (a run's peer stores cannot overwrite a
+    // buffer another rank is still reading: the error all-reduce that closes
+    // every run orders them), their IPC mappings on every rank
+    double* d_p2p[2] = {nullptr, nullptr};
+    double* peer_p2p[2][ara::kMaxPeers] = {};
+    size_t p2p_cap = 0;               // doubles per buffer
+    int p2p_state = 0;                // 0 unknown, 1 usable, -1 not usable (collective verdict)
+    int p2p_next = 0;                 // buffer of the next run
+    bool use_p2p = true;              // ARA_NO_P2P=1: assemble the YLT with ncclAllGather instead
+    const double* d_last_full = nullptr;   // global YLT of the last run (metrics input)
     int run_mode = 0;                  // ARA_RUN_DIRECT / ARA_RUN_FOLD
     double* d_fold = nullptr;          // fold mode: per-event occurrence-net losses
     size_t fold_cap = 0;

@@ -162,6 +162,37 @@ __device__ __forceinline__ void event_compute_smem(const TrialParams& p, const d
     }
 }
 
+// a8 epilogue of one trial (lane 0): aggregate terms per layer, the YLT and
+// lossy-count stores, the portfolio row (A8) -- and, when the run assembles
+// the global YLT over NVLink (p.n_peers > 0), the same values stored straight
+// into every rank's global YLT (peer memory mapped by CUDA IPC), which fuses
+// the YLT all-gather (a9) into the kernel epilogue.
+template <int NL>
+__device__ __forceinline__ void store_trial(const TrialParams& p, uint64_t t, const double (&G)[NL],
+                                            const uint32_t (&m)[NL]) {
+    double port = 0.0;
+    if (p.portfolio_mode == 1) port = p.ylt[(uint64_t)p.portfolio_row * p.ld + t];
+    const uint64_t tg = p.peer_t0 + t;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+        if (l >= (int)p.n_layers) break;
+        const double y = terms(G[l], p.lw[l].agg_r, p.lw[l].agg_l);
+        p.ylt[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = y;
+        if (p.lossy) p.lossy[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = m[l];
+        port = __dadd_rn(port, y);
+        for (uint32_t r = 0; r < p.n_peers; ++r) p.peer_ylt[r][(uint64_t)(p.ylt_row0 + l) * p.peer_ld + tg] = y;
+    }
+    if (p.portfolio_mode >= 0) {
+        p.ylt[(uint64_t)p.portfolio_row * p.ld + t] = port;
+        for (uint32_t r = 0; r < p.n_peers; ++r) p.peer_ylt[r][(uint64_t)p.portfolio_row * p.peer_ld + tg] = port;
+    }
+}
+
+// peer stores of this warp are performed before the kernel is seen complete
+__device__ __forceinline__ void peer_fence(const TrialParams& p) {
+    if (p.n_peers && (threadIdx.x & 31u) == 0) __threadfence_system();
+}
+
 // Events per lane per pipeline step (~16-32 row registers per stage); windows
 // wider than 32 registers run without the row double buffer (PIPE = false).
 template <typename TV, int NSEC>
@@ -332,19 +363,10 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel(const __grid_cons
         }
         // a8: aggregate terms, store the YLT entries (+ portfolio, A8).
         if (lane == 0) {
-            double port = 0.0;
-            if (p.portfolio_mode == 1) port = p.ylt[(uint64_t)p.portfolio_row * p.ld + t];
-#pragma unroll
-            for (int l = 0; l < NLB; ++l) {
-                if (l >= (int)p.n_layers) break;
-                const double y = terms(G[l], p.lw[l].agg_r, p.lw[l].agg_l);
-                p.ylt[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = y;
-                if (p.lossy) p.lossy[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = m[l];
-                port = __dadd_rn(port, y);
-            }
-            if (p.portfolio_mode >= 0) p.ylt[(uint64_t)p.portfolio_row * p.ld + t] = port;
+            store_trial(p, t, G, m);
         }
     }
+    peer_fence(p);
     if (err) atomicOr(p.err, err);
 }
 
@@ -520,17 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1) trial_kernel_sm(const __grid_cons
                 }
                 if (lane == 0) {
                     const uint64_t t = md.t;
-                    double port = 0.0;
-                    if (p.portfolio_mode == 1) port = p.ylt[(uint64_t)p.portfolio_row * p.ld + t];
-#pragma unroll
-                    for (int l = 0; l < NLB; ++l) {
-                        if (l >= (int)p.n_layers) break;
-                        const double y = terms(G[l], p.lw[l].agg_r, p.lw[l].agg_l);
-                        p.ylt[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = y;
-                        if (p.lossy) p.lossy[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = m[l];
-                        port = __dadd_rn(port, y);
-                    }
-                    if (p.portfolio_mode >= 0) p.ylt[(uint64_t)p.portfolio_row * p.ld + t] = port;
+                    store_trial(p, t, G, m);
                 }
 #pragma unroll
                 for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
@@ -731,17 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1) trial_kernel_tma(const __grid_con
                 }
                 if (lane == 0) {
                     const uint64_t t = md.t;
-                    double port = 0.0;
-                    if (p.portfolio_mode == 1) port = p.ylt[(uint64_t)p.portfolio_row * p.ld + t];
-#pragma unroll
-                    for (int l = 0; l < NLB; ++l) {
-                        if (l >= (int)p.n_layers) break;
-                        const double y = terms(G[l], p.lw[l].agg_r, p.lw[l].agg_l);
-                        p.ylt[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = y;
-                        if (p.lossy) p.lossy[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = m[l];
-                        port = __dadd_rn(port, y);
-                    }
-                    if (p.portfolio_mode >= 0) p.ylt[(uint64_t)p.portfolio_row * p.ld + t] = port;
+                    store_trial(p, t, G, m);
                 }
 #pragma unroll
                 for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
@@ -954,17 +956,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_co(const __grid_c
                 }
                 if (lane == 0) {
                     const uint64_t t = md.t;
-                    double port = 0.0;
-                    if (p.portfolio_mode == 1) port = p.ylt[(uint64_t)p.portfolio_row * p.ld + t];
-#pragma unroll
-                    for (int l = 0; l < NLB; ++l) {
-                        if (l >= (int)p.n_layers) break;
-                        const double y = terms(G[l], p.lw[l].agg_r, p.lw[l].agg_l);
-                        p.ylt[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = y;
-                        if (p.lossy) p.lossy[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = m[l];
-                        port = __dadd_rn(port, y);
-                    }
-                    if (p.portfolio_mode >= 0) p.ylt[(uint64_t)p.portfolio_row * p.ld + t] = port;
+                    store_trial(p, t, G, m);
                 }
 #pragma unroll
                 for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
@@ -973,6 +965,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_co(const __grid_c
     }
 done:
     cp_wait<0>();
+    peer_fence(p);
     if (err) atomicOr(p.err, err);
 }
 
@@ -1198,17 +1191,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
             }
             if (lane == 0) {
                 const uint64_t t = rm.t;
-                double port = 0.0;
-                if (p.portfolio_mode == 1) port = p.ylt[(uint64_t)p.portfolio_row * p.ld + t];
-#pragma unroll
-                for (int l = 0; l < NLB; ++l) {
-                    if (l >= (int)p.n_layers) break;
-                    const double y = terms(G[l], p.lw[l].agg_r, p.lw[l].agg_l);
-                    p.ylt[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = y;
-                    if (p.lossy) p.lossy[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = m[l];
-                    port = __dadd_rn(port, y);
-                }
-                if (p.portfolio_mode >= 0) p.ylt[(uint64_t)p.portfolio_row * p.ld + t] = port;
+                store_trial(p, t, G, m);
             }
 #pragma unroll
             for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
@@ -1283,6 +1266,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
     }
     while (head != tail) consume();
     cp_wait<0>();
+    peer_fence(p);
     if (err) atomicOr(p.err, err);
 }
 
@@ -1475,19 +1459,10 @@ __global__ void __launch_bounds__(kThreads) trial_fold_kernel(const __grid_const
             }
         }
         if (lane == 0) {
-            double port = 0.0;
-            if (p.portfolio_mode == 1) port = p.ylt[(uint64_t)p.portfolio_row * p.ld + t];
-#pragma unroll
-            for (int l = 0; l < NL; ++l) {
-                if (l >= (int)p.n_layers) break;
-                const double y = terms(G[l], p.lw[l].agg_r, p.lw[l].agg_l);
-                p.ylt[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = y;
-                if (p.lossy) p.lossy[(uint64_t)(p.ylt_row0 + l) * p.ld + t] = m[l];
-                port = __dadd_rn(port, y);
-            }
-            if (p.portfolio_mode >= 0) p.ylt[(uint64_t)p.portfolio_row * p.ld + t] = port;
+            store_trial(p, t, G, m);
         }
     }
+    peer_fence(p);
     if (err) atomicOr(p.err, err);
 }
 

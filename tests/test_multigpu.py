@@ -29,9 +29,13 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("name,n_trials,rho", [("tiny", 1000, None), ("tiny", 997, None), ("mini", 20_000, None),
-                                               ("mini", 20_001, 0.01)])
-def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials, rho):
+@pytest.mark.parametrize("name,n_trials,rho,p2p", [("tiny", 1000, None, True), ("tiny", 997, None, True),
+                                                   ("mini", 20_000, None, True), ("mini", 20_001, 0.01, True),
+                                                   ("tiny", 997, None, False), ("mini", 20_001, 0.01, False)])
+def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials, rho, p2p):
+    """p2p: the kernels store the YLT straight into every rank's global buffer
+    over NVLink (fused assembly, the default); otherwise ncclAllGather
+    (ARA_NO_P2P=1).  Both must equal the 1-GPU run bit for bit."""
     n = _ngpu()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -40,7 +44,10 @@ def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials, rho):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(HERE, "mgpu_worker.py"),
            name, str(n_trials), out] + ([str(rho)] if rho is not None else [])
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ)
+    if not p2p:
+        env["ARA_NO_P2P"] = "1"
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     got = np.load(out)
     assert bool(got["same"])
@@ -53,3 +60,9 @@ def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials, rho):
     assert np.array_equal(got["ylt"], ylt)
     assert np.array_equal(got["pml"], met[1]) and np.array_equal(got["k"], met[0])
     assert np.allclose(got["tvar"], met[2], rtol=1e-12, atol=0)
+    # the second and third consecutive runs (other terms, then the first again)
+    sys.path.insert(0, HERE)
+    from mgpu_worker import bumped_layers
+    ylt_b, _, _, met_b = run_gpu(off, ids, elts, w, bumped_layers(w.layers), return_periods=R)
+    assert np.array_equal(got["ylt_b"], ylt_b) and np.array_equal(got["pml_b"], met_b[1])
+    assert np.array_equal(got["ylt_c"], ylt)
