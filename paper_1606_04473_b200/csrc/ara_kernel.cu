@@ -193,6 +193,65 @@ __device__ __forceinline__ void peer_fence(const TrialParams& p) {
     if (p.n_peers && (threadIdx.x & 31u) == 0) __threadfence_system();
 }
 
+// event_compute for the sparse path: on the paper's ELTs an occupied row holds
+// about one non-zero loss in 16, and a +0 loss adds an exact +0 to l_e (every
+// deductible is >= 0 and l_e >= +0), so only the non-zero elements of the
+// window are visited -- in ascending ELT order, which keeps l_e bit-identical
+// to the dense sum.  The lane reads its staged row once to build the non-zero
+// mask, then loads each non-zero element (and its terms) by index.
+__device__ __forceinline__ uint4 lds_v4(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a)
+                 : "memory");
+    return v;
+}
+template <typename TV, int NSEC, int NLB>
+__device__ __forceinline__ void event_compute_sparse(const TrialParams& p, const double2 (*s_term)[kMaxWin],
+                                                     uint32_t src, uint32_t swz, double (&G)[NLB],
+                                                     uint32_t (&m)[NLB]) {
+    constexpr int CH = NSEC * 2;                 // 16-B chunks of the window
+    constexpr int EPC = 16 / (int)sizeof(TV);    // elements per chunk
+    constexpr bool SM = TermsInSmem<TV, NSEC, NLB>::value;
+    uint32_t nz = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        const uint4 v = lds_v4(src + (((uint32_t)c ^ swz) << 4));
+        if (EPC == 2) {
+            nz |= ((v.x | v.y) != 0u ? 1u : 0u) << (2 * c);
+            nz |= ((v.z | v.w) != 0u ? 1u : 0u) << (2 * c + 1);
+        } else {
+            nz |= (v.x != 0u ? 1u : 0u) << (4 * c);
+            nz |= (v.y != 0u ? 1u : 0u) << (4 * c + 1);
+            nz |= (v.z != 0u ? 1u : 0u) << (4 * c + 2);
+            nz |= (v.w != 0u ? 1u : 0u) << (4 * c + 3);
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < NLB; ++l) {
+        if (l >= (int)p.n_layers) break;
+        double le = 0.0;
+        uint32_t mm = nz;
+        while (mm) {
+            const uint32_t j = (uint32_t)(__ffs(mm) - 1);
+            mm &= mm - 1u;
+            const uint32_t a = src + (((j / EPC) ^ swz) << 4) + (j % EPC) * (uint32_t)sizeof(TV);
+            double x;
+            if (EPC == 2) {
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a) : "memory");
+            } else {
+                float xf;
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xf) : "r"(a) : "memory");
+                x = (double)xf;
+            }
+            const double2 tc = SM ? lds_term(&s_term[l][j]) : p.term[l][j];
+            le = __dadd_rn(le, terms(x, tc.x, tc.y));
+        }
+        const double o = terms(le, p.lw[l].occ_r, p.lw[l].occ_l);
+        G[l] = __dadd_rn(G[l], o);
+        m[l] += (o > 0.0) ? 1u : 0u;
+    }
+}
+
 // Events per lane per pipeline step (~16-32 row registers per stage); windows
 // wider than 32 registers run without the row double buffer (PIPE = false).
 template <typename TV, int NSEC>
@@ -1177,7 +1236,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         wait_group(g);
         __syncwarp();   // other lanes' copies of my row are complete and visible
         const StepMeta rm = rmeta[slot];
-        event_compute_smem<TV, NSEC, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m);
+        event_compute_sparse<TV, NSEC, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m);
         __syncwarp();   // every lane's reads of the slot precede the copies refilling it
         ++head;
         if (rm.n) {   // last round of trial rm.t: a7 + a8
@@ -1238,28 +1297,33 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         commit();
         const bool trial_end = md.k0 + 128u >= md.n;
 #pragma unroll 1
+        const uint32_t id_base = idr + (sc % IR) * IDB + (md.sh + lane) * 4u;
+        const uint32_t oc_base = ocr + ((sc % WR) * 128u + lane) * 4u;
+        const uint32_t n_here = md.n - md.k0;   // events of the trial from this step on
+#pragma unroll 1
         for (uint32_t j = 0; j < 4u; ++j) {
-            const uint32_t k = md.k0 + 32u * j + lane;
-            uint32_t e = lds_u32(idr + (sc % IR) * IDB + (md.sh + 32u * j + lane) * 4u);
-            const uint32_t w = lds_u32(ocr + ((sc % WR) * 128u + 32u * j + lane) * 4u);
-            if (k >= md.n) e = 0u;
-            else if (e == 0u || e > p.catalog) { err |= ERRBIT_EVENT_RANGE; e = 0u; }   // A14
-            e = (!bm || ((w >> (e & 31u)) & 1u)) ? e : 0u;
-            if (e) {   // append (entries beyond fc are 0, so f[fc] is free)
+            uint32_t e = lds_u32(id_base + 128u * j);
+            const uint32_t w = lds_u32(oc_base + 128u * j);
+            const bool live = 32u * j + lane < n_here;
+            const bool bad = live && e - 1u >= p.catalog;            // id 0 or > C (A14)
+            err |= bad ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
+            e = (live && !bad && (!bm || ((w >> (e & 31u)) & 1u))) ? e : 0u;
+            // append (entries at and beyond fc are 0, so f[fc] is free); branch-free
+            const bool add = e != 0u;
 #pragma unroll
-                for (int i = 0; i < QC; ++i) f[i] = (fc == (uint32_t)i) ? e : f[i];
-                ++fc;
-            }
+            for (int i = 0; i < QC; ++i) f[i] = (add && fc == (uint32_t)i) ? e : f[i];
+            fc += add ? 1u : 0u;
             // a full FIFO emits one round; the end of the trial emits rounds
             // until every FIFO is empty, the last one finalising the trial
             const bool flush = trial_end && j == 3u;
-            for (;;) {
-                uint32_t last = 0u;
-                if (flush) last = __any_sync(0xffffffffu, fc > 1u) ? 0u : 1u;
-                else if (!__any_sync(0xffffffffu, fc == (uint32_t)QC)) break;
-                if (tail - head == (uint32_t)NS) consume();
-                emit(md.t, last);
-                if (!flush || last) break;
+            const bool full = __any_sync(0xffffffffu, fc == (uint32_t)QC);
+            if (full || flush) {
+                for (;;) {
+                    const uint32_t last = (flush && !__any_sync(0xffffffffu, fc > 1u)) ? 1u : 0u;
+                    if (tail - head == (uint32_t)NS) consume();
+                    emit(md.t, last);
+                    if (!flush || last) break;
+                }
             }
         }
         __syncwarp();   // reads of this step's slots precede their refills
