@@ -506,7 +506,15 @@ def main():
                          # (profiles/r01_microbench.json: random 32-B gathers, L2-resident table)
                          "l2_frac": (32 * trec["l2_sectors_per_launch"] / (k_ms * 1e6) / l2_gather_peak())
                          if (trec and l2_gather_peak()) else None,
-                         "traffic_source": trec.get("source") if trec else None},
+                         "traffic_source": trec.get("source") if trec else None,
+                         # SURVEY 8(d) F_roof: the binding hardware roof is the larger of the DRAM
+                         # time (ncu DRAM bytes / HBM peak) and the L2 time (ncu L2 sector bytes /
+                         # measured L2 gather ceiling); hierarchical_frac = that time / kernel time
+                         "hierarchical_frac": (max(traffic / peak, 32 * trec["l2_sectors_per_launch"] / l2_gather_peak())
+                                               / 1e6 / k_ms) if (trec and l2_gather_peak()) else None,
+                         "note": ("algorithmic bytes = YET bytes + 32 B per gathered ELT sector (north star); "
+                                  "most gathered sectors are L2 hits (l2_hit_rate_pct), so achieved can exceed "
+                                  "the HBM peak; hierarchical_frac is the fraction of the binding roof")},
             "breakdown_ms": {"ara_kernel": k_ms, "allgather": float(np.mean(ag_ms)), "metrics": float(np.mean(met_ms)),
                              "step": ms,
                              "calls": {k: float(np.median([p[i] for p in part_ms]))
