@@ -297,6 +297,7 @@ extern "C" void ara_destroy(ara_ctx* ctx) {
     cudaFree(ctx->d_ylt_global);
     cudaFree(ctx->d_lossy);
     cudaFree(ctx->d_fold);
+    cudaFree(ctx->d_occ4);
     cudaFree(ctx->d_sp_off);
     cudaFree(ctx->d_sp_ev);
     cudaFree(ctx->d_sp_ls);
@@ -977,11 +978,32 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     // Kernels.
     const TableGeo& geo = ctx->geo;
     const uint32_t spb = geo.epb / eps;   // sectors per block row
+    // Multi-window compacted rounds: 2-4 disjoint single-layer windows of equal
+    // width, each inside one sparse column block, scanned by ONE launch (one id
+    // stream and one combined occupancy word per event instead of one launch
+    // per layer re-reading the YET).
+    bool multiwin = false;
+    {
+        const TableGeo& g0 = ctx->geo;
+        const uint32_t spb0 = g0.epb / eps;
+        // opt-in (ARA_KERNEL=15): measured slower than one launch per layer on the
+        // 4-layer config (33.1 vs 32.0 ms): the per-window FIFOs must be 2 deep
+        // to fit the registers, which raises the round count, and the four
+        // blocks' occupied rows (152 MB) no longer fit in L2
+        multiwin = !fold && n_programs == 0 && groups.size() >= 2 && groups.size() <= (size_t)kMaxLB &&
+                   ctx->kernel_variant == 15 && !ctx->no_skip;
+        for (size_t gi = 0; gi < groups.size() && multiwin; ++gi) {
+            const Group& g = groups[gi];
+            const uint32_t blk = g.q0 / spb0;
+            multiwin = g.nl == 1 && !g.wide && g.nsec == groups[0].nsec && g.nsec <= 4 && (g.q0 % spb0) + g.nsec <= spb0 &&
+                       blk < ctx->occ_rows.size() && 2ull * ctx->occ_rows[blk] <= (uint64_t)ctx->catalog + 1;
+        }
+    }
     // Fused YLT assembly: one launch group per chunk (no wide layers, no
     // programs, one fold chunk) with a kernel whose epilogue stores to peers.
     bool p2p_ok_kernel = ctx->kernel_variant < 0 || ctx->kernel_variant == 0 || ctx->kernel_variant == 5 ||
-                         ctx->kernel_variant == 12 || ctx->kernel_variant == 14;
-    bool single_group = groups.size() == 1 && !groups[0].wide && n_programs == 0 &&
+                         ctx->kernel_variant == 12 || ctx->kernel_variant == 14 || ctx->kernel_variant == 15;
+    bool single_group = (groups.size() == 1 || multiwin) && !groups[0].wide && n_programs == 0 &&
                         (!fold || (n_layers + nlc - 1) / nlc == 1) && world <= (uint32_t)kMaxPeers;
     bool use_p2p = false;
     if (world > 1 && ctx->use_p2p && p2p_ok_kernel && single_group) {
@@ -1045,6 +1067,15 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
             }
         }
     };
+    if (multiwin) {   // the windows' combined occupancy map (4 bits per event)
+        const size_t words = ((size_t)ctx->catalog + 1 + 7) / 8;
+        st = ensure(ctx, ctx->d_occ4, ctx->occ4_cap, words);
+        if (st != ARA_OK) return st;
+        uint32_t blk[kMaxLB] = {};
+        for (size_t gi = 0; gi < groups.size(); ++gi) blk[gi] = groups[gi].q0 / spb;
+        CK(launch_occ4(reinterpret_cast<const uint32_t*>(static_cast<const char*>(ctx->d_table) + geo.bm_off),
+                       geo.bm_words, blk, (uint32_t)groups.size(), ctx->catalog, ctx->d_occ4, s));
+    }
     const uint32_t n_chunks_fold = (n_layers + nlc - 1) / nlc;
     const uint64_t fold_rows = (uint64_t)ctx->catalog + 1;
     CK(cudaEventRecord(ctx->ev[1], s));
@@ -1088,6 +1119,38 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
             }
             continue;
         }
+        if (multiwin) {
+            TrialParams p = base;
+            p.t_begin = chunks[c].first;
+            p.t_end = chunks[c].second;
+            p.n_layers = (uint32_t)groups.size();
+            p.ylt_row0 = 0;
+            p.portfolio_mode = 0;
+            double occ_sum = 0.0;
+            for (uint32_t u = 0; u < p.n_layers; ++u) {
+                const Group& g = groups[u];
+                const LayerI& L = layers[g.l0];
+                p.lw[u] = {L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit};
+                p.win0[u] = (uint64_t)(g.q0 / spb) * geo.block_elems + (uint64_t)(g.q0 % spb) * eps;
+                for (uint32_t w = 0; w < (uint32_t)kMaxWin; ++w) {
+                    const uint32_t col = g.q0 * eps + w;
+                    if (w / eps < g.nsec && L.member(col))
+                        p.term[u][w] = make_double2(ctx->terms[col].deductible, ctx->terms[col].limit);
+                    else
+                        p.term[u][w] = make_double2(INFINITY, INFINITY);   // contributes exactly +0
+                }
+                occ_sum += (double)ctx->occ_rows[g.q0 / spb] / ((double)ctx->catalog + 1.0);
+            }
+            for (uint32_t sct = 0; sct < (uint32_t)kMaxSec; ++sct)
+                p.sec_off[sct] = p.win0[0] + (uint64_t)(sct < groups[0].nsec ? sct : 0) * eps;
+            p.bm = ctx->d_occ4;
+            used_variant = 15;
+            used_occupancy = occ_sum / p.n_layers;
+            const int grid = (int)(trial_kernel_grid(fp32, groups[0].nsec, 4, 15) * ctx->grid_mult);
+            CK(launch_trials(p, fp32, groups[0].nsec, grid > 0 ? grid : 1, 15, s));
+            ++launches;
+            continue;
+        }
         for (size_t gi = 0; gi < groups.size(); ++gi) {
             const Group& g = groups[gi];
             TrialParams p = base;
@@ -1128,6 +1191,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 // 3 CTAs/SM (5) for single layers, 2 CTAs/SM (0) for shared-window towers.
                 // The other variants stay ARA_KERNEL-selectable for A/B runs.
                 int variant = ctx->kernel_variant;
+                if (variant == 15) variant = 14;   // multi-window only for multi-window runs (above)
                 if (variant < 0 && p.bm) variant = 14;
                 if (p.bm) {   // rows actually gathered: the occupied fraction of the block
                     const uint32_t blk = g.q0 / spb;

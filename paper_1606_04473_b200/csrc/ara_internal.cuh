@@ -111,6 +111,10 @@ struct TrialParams {
     // mapped into this process (CUDA IPC over NVLink); 0 peers = not used
     double* peer_ylt[kMaxPeers];
     uint32_t n_peers;
+    // multi-window compacted rounds (disjoint layers, one launch): element
+    // offset of layer u's window (event 0); bm then points at the combined
+    // 4-bit-per-event occupancy map of the windows' column blocks
+    uint64_t win0[kMaxLB];
     uint64_t peer_ld;           // = T_global
     uint64_t peer_t0;           // global index of local trial 0 (this rank's first trial)
 };
@@ -120,6 +124,9 @@ cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const d
                            uint32_t n_elts, uint64_t n_records, uint32_t catalog, void* d_table,
                            const TableGeo& geo, int fp32, uint32_t* d_err, cudaStream_t s);
 
+// combined occupancy of up to 4 column blocks: 4 bits per event (bit u = block blk[u])
+cudaError_t launch_occ4(const uint32_t* bitmaps, uint64_t bm_words, const uint32_t* blk, uint32_t n_win,
+                        uint32_t catalog, uint32_t* occ4, cudaStream_t s);
 // zero exactly the rows the occupancy bitmaps mark, then the bitmaps and counters
 cudaError_t launch_clear_rows(void* d_table, const TableGeo& geo, uint32_t catalog, cudaStream_t s);
 cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int grid, int variant, cudaStream_t s);
@@ -231,6 +238,8 @@ struct ara_ctx {
     int p2p_next = 0;                 // buffer of the next run
     bool use_p2p = true;              // ARA_NO_P2P=1: assemble the YLT with ncclAllGather instead
     const double* d_last_full = nullptr;   // global YLT of the last run (metrics input)
+    uint32_t* d_occ4 = nullptr;       // combined occupancy map of a multi-window launch
+    size_t occ4_cap = 0;
     int run_mode = 0;                  // ARA_RUN_DIRECT / ARA_RUN_FOLD
     double* d_fold = nullptr;          // fold mode: per-event occurrence-net losses
     size_t fold_cap = 0;

@@ -252,6 +252,55 @@ __device__ __forceinline__ void event_compute_sparse(const TrialParams& p, const
     }
 }
 
+// The same for a multi-window launch: the staged row belongs to the window of
+// layer u (one layer per window); only that layer's accumulators change.
+template <typename TV, int NSEC, int NLB>
+__device__ __forceinline__ void event_compute_sparse_win(const TrialParams& p, const double2 (*s_term)[kMaxWin],
+                                                         uint32_t src, uint32_t swz, double (&G)[NLB],
+                                                         uint32_t (&m)[NLB], uint32_t u) {
+    constexpr int CH = NSEC * 2;
+    constexpr int EPC = 16 / (int)sizeof(TV);
+    constexpr bool SM = TermsInSmem<TV, NSEC, NLB>::value;
+    uint32_t nz = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+        const uint4 v = lds_v4(src + (((uint32_t)c ^ swz) << 4));
+        if (EPC == 2) {
+            nz |= ((v.x | v.y) != 0u ? 1u : 0u) << (2 * c);
+            nz |= ((v.z | v.w) != 0u ? 1u : 0u) << (2 * c + 1);
+        } else {
+            nz |= (v.x != 0u ? 1u : 0u) << (4 * c);
+            nz |= (v.y != 0u ? 1u : 0u) << (4 * c + 1);
+            nz |= (v.z != 0u ? 1u : 0u) << (4 * c + 2);
+            nz |= (v.w != 0u ? 1u : 0u) << (4 * c + 3);
+        }
+    }
+    double le = 0.0;
+    while (nz) {
+        const uint32_t j = (uint32_t)(__ffs(nz) - 1);
+        nz &= nz - 1u;
+        const uint32_t a = src + (((j / EPC) ^ swz) << 4) + (j % EPC) * (uint32_t)sizeof(TV);
+        double x;
+        if (EPC == 2) {
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a) : "memory");
+        } else {
+            float xf;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xf) : "r"(a) : "memory");
+            x = (double)xf;
+        }
+        const double2 tc = SM ? lds_term(&s_term[u][j]) : p.term[u][j];
+        le = __dadd_rn(le, terms(x, tc.x, tc.y));
+    }
+    const double o = terms(le, p.lw[u].occ_r, p.lw[u].occ_l);
+    const uint32_t hit = (o > 0.0) ? 1u : 0u;
+#pragma unroll
+    for (int l = 0; l < NLB; ++l) {
+        const double gl = __dadd_rn(G[l], o);
+        G[l] = (l == (int)u) ? gl : G[l];
+        m[l] += (l == (int)u) ? hit : 0u;
+    }
+}
+
 // Events per lane per pipeline step (~16-32 row registers per stage); windows
 // wider than 32 registers run without the row double buffer (PIPE = false).
 template <typename TV, int NSEC>
@@ -1094,14 +1143,19 @@ __device__ __forceinline__ void cp_wait_upto(uint32_t n) {
     }
 }
 
-template <typename TV, int NSEC, int NLB, int BUDGET_KB, int MINB>
+template <typename TV, int NSEC, int NLB, int BUDGET_KB, int MINB, int NWIN>
 __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_constant__ TrialParams p) {
+    // NWIN == 1: one row window (layers 0..n_layers-1 share it: towers);
+    // NWIN > 1: p.n_layers disjoint windows, one layer each, scanned together
+    // (one id stream, one combined 4-bit occupancy word per event, one FIFO
+    // per window; the last round of a trial is an empty finalising marker)
+    static_assert(NWIN == 1 || NWIN == NLB, "one layer per window");
     using Geo = CoGeo<TV, NSEC, BUDGET_KB>;
     using RG = typename CqGeo<TV, NSEC, BUDGET_KB, MINB>::R;
     constexpr int NS = Geo::NS;
     constexpr int CH = Geo::CH, LPR = Geo::LPR, RPI = Geo::RPI;
     constexpr int QD = RG::QD, DW = RG::DW, IR = RG::IR, WR = RG::WR, MR = RG::MR, IDB = RG::IDB;
-    constexpr int QC = 4;   // per-lane FIFO of occupied events
+    constexpr int QC = NWIN > 1 ? 2 : 4;   // per-lane FIFO of occupied events (per window)
     constexpr bool SM = TermsInSmem<TV, NSEC, NLB>::value;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double2 s_term[SM ? NLB : 1][kMaxWin];
@@ -1199,7 +1253,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         for (int j = 0; j < 4; ++j) {
             uint32_t e = lds_u32(idr + (x % IR) * IDB + (sh + 32u * j + lane) * 4u);
             e = e <= p.catalog ? e : 0u;   // not validated yet
-            cp_async4(ocr + ((x % WR) * 128u + 32u * j + lane) * 4u, bm + (e >> 5), bm ? 4u : 0u);
+            cp_async4(ocr + ((x % WR) * 128u + 32u * j + lane) * 4u, bm + (e >> (NWIN > 1 ? 3 : 5)), bm ? 4u : 0u);
         }
     };
 
@@ -1215,11 +1269,14 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         g_occ = commit();
     }
 
-    // ---- per-lane FIFO of occupied events (entries at and beyond fc are 0)
-    uint32_t f[QC];
+    // ---- per-lane FIFOs of occupied events, one per window (entries at and beyond fc are 0)
+    uint32_t f[NWIN][QC], fc[NWIN];
 #pragma unroll
-    for (int i = 0; i < QC; ++i) f[i] = 0u;
-    uint32_t fc = 0;
+    for (int u = 0; u < NWIN; ++u) {
+        fc[u] = 0;
+#pragma unroll
+        for (int i = 0; i < QC; ++i) f[u][i] = 0u;
+    }
 
     double G[NLB];
     uint32_t m[NLB];
@@ -1236,7 +1293,8 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         wait_group(g);
         __syncwarp();   // other lanes' copies of my row are complete and visible
         const StepMeta rm = rmeta[slot];
-        event_compute_sparse<TV, NSEC, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m);
+        if (NWIN == 1) event_compute_sparse<TV, NSEC, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m);
+        else event_compute_sparse_win<TV, NSEC, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m, rm.k0);
         __syncwarp();   // every lane's reads of the slot precede the copies refilling it
         ++head;
         if (rm.n) {   // last round of trial rm.t: a7 + a8
@@ -1256,23 +1314,33 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
             for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
         }
     };
-    // emit a round: every lane pops its FIFO head (0 = nothing: zero-fill)
+    // emit a round of window u: every lane pops that FIFO's head (0 = nothing:
+    // zero-fill); u == NWIN: the empty finalising marker (multi-window)
     // (the caller has made room in the ring)
-    auto emit = [&](uint64_t t, uint32_t last) {
-        const uint32_t ce = f[0];
+    auto emit = [&](uint64_t t, uint32_t last, uint32_t u) {
+        uint32_t ce = 0;
 #pragma unroll
-        for (int i = 0; i + 1 < QC; ++i) f[i] = f[i + 1];
-        f[QC - 1] = 0u;
-        fc -= fc ? 1u : 0u;
+        for (int w = 0; w < NWIN; ++w) {
+            if ((uint32_t)w != u) continue;
+            ce = f[w][0];
+#pragma unroll
+            for (int i = 0; i + 1 < QC; ++i) f[w][i] = f[w][i + 1];
+            f[w][QC - 1] = 0u;
+            fc[w] -= fc[w] ? 1u : 0u;
+        }
+        const char* src = c_src;
+        if (NWIN > 1)
+            src = reinterpret_cast<const char*>(p.table) +
+                  (p.win0[u < (uint32_t)NWIN ? u : 0u] + c_chunk * (16 / sizeof(TV))) * sizeof(TV);
         const uint32_t slot = tail % NS;
         const uint32_t dst = ring + slot * Geo::STAGE;
 #pragma unroll
         for (int i = 0; i < CH; ++i) {
             const uint32_t e = __shfl_sync(0xffffffffu, ce, (uint32_t)i * RPI + c_row);
-            cp_async16(dst + (uint32_t)i * RPI * Geo::ROWB + c_dst[i & 1], c_src + (uint64_t)e * row_bytes,
+            cp_async16(dst + (uint32_t)i * RPI * Geo::ROWB + c_dst[i & 1], src + (uint64_t)e * row_bytes,
                        e ? 16u : 0u);
         }
-        if (lane == 0) rmeta[slot] = StepMeta{t, last, 0u};
+        if (lane == 0) rmeta[slot] = StepMeta{t, last, u < (uint32_t)NWIN ? u : 0u};
         const uint32_t g = commit();
 #pragma unroll
         for (int i = 0; i < NS; ++i) rg[i] = (slot == (uint32_t)i) ? g : rg[i];
@@ -1307,22 +1375,49 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
             const bool live = 32u * j + lane < n_here;
             const bool bad = live && e - 1u >= p.catalog;            // id 0 or > C (A14)
             err |= bad ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
-            e = (live && !bad && (!bm || ((w >> (e & 31u)) & 1u))) ? e : 0u;
-            // append (entries at and beyond fc are 0, so f[fc] is free); branch-free
-            const bool add = e != 0u;
+            if (NWIN == 1) {
+                e = (live && !bad && (!bm || ((w >> (e & 31u)) & 1u))) ? e : 0u;
+                // append (entries at and beyond fc are 0, so f[fc] is free); branch-free
+                const bool add = e != 0u;
 #pragma unroll
-            for (int i = 0; i < QC; ++i) f[i] = (add && fc == (uint32_t)i) ? e : f[i];
-            fc += add ? 1u : 0u;
-            // a full FIFO emits one round; the end of the trial emits rounds
-            // until every FIFO is empty, the last one finalising the trial
+                for (int i = 0; i < QC; ++i) f[0][i] = (add && fc[0] == (uint32_t)i) ? e : f[0][i];
+                fc[0] += add ? 1u : 0u;
+            } else {
+                const uint32_t bits = (live && !bad) ? (bm ? (w >> ((e & 7u) * 4u)) & 15u : 15u) : 0u;
+#pragma unroll
+                for (int u = 0; u < NWIN; ++u) {
+                    const bool add = (bits >> u) & 1u;
+#pragma unroll
+                    for (int i = 0; i < QC; ++i) f[u][i] = (add && fc[u] == (uint32_t)i) ? e : f[u][i];
+                    fc[u] += add ? 1u : 0u;
+                }
+            }
+            // a full FIFO emits one round (per window); the end of the trial
+            // emits rounds until every FIFO is empty, then finalises the trial
             const bool flush = trial_end && j == 3u;
-            const bool full = __any_sync(0xffffffffu, fc == (uint32_t)QC);
-            if (full || flush) {
+            uint32_t fullmask = 0;
+#pragma unroll
+            for (int u = 0; u < NWIN; ++u) fullmask |= __any_sync(0xffffffffu, fc[u] == (uint32_t)QC) ? 1u << u : 0u;
+            if (fullmask || flush) {
                 for (;;) {
-                    const uint32_t last = (flush && !__any_sync(0xffffffffu, fc > 1u)) ? 1u : 0u;
+                    uint32_t u = 0, last = 0;
+                    if (NWIN == 1) {
+                        if (!fullmask && !flush) break;
+                        last = (flush && !__any_sync(0xffffffffu, fc[0] > 1u)) ? 1u : 0u;
+                    } else {
+                        // the first window with a full FIFO (or, flushing, any entry)
+                        uint32_t pend = 0;
+#pragma unroll
+                        for (int w = 0; w < NWIN; ++w)
+                            pend |= __any_sync(0xffffffffu, flush ? fc[w] > 0u : fc[w] == (uint32_t)QC) ? 1u << w : 0u;
+                        if (!pend && !flush) break;
+                        u = pend ? (uint32_t)(__ffs(pend) - 1) : (uint32_t)NWIN;   // NWIN: the marker
+                        last = pend ? 0u : 1u;
+                    }
                     if (tail - head == (uint32_t)NS) consume();
-                    emit(md.t, last);
-                    if (!flush || last) break;
+                    emit(md.t, last, u);
+                    if (NWIN == 1 ? (!flush || last) : last) break;
+                    fullmask = 0;   // (multi-window) re-evaluated from the FIFOs above
                 }
             }
         }
@@ -1619,14 +1714,14 @@ template <typename TV, int NLB, int BUDGET_KB, int MINB>
 void* pick_nsec_cq(uint32_t nsec, int* smem) {
     if (nsec <= 1) {
         *smem = CqGeo<TV, 1, BUDGET_KB, MINB>::BYTES;
-        return (void*)trial_kernel_cq<TV, 1, NLB, BUDGET_KB, MINB>;
+        return (void*)trial_kernel_cq<TV, 1, NLB, BUDGET_KB, MINB, 1>;
     }
     if (nsec <= 2) {
         *smem = CqGeo<TV, 2, BUDGET_KB, MINB>::BYTES;
-        return (void*)trial_kernel_cq<TV, 2, NLB, BUDGET_KB, MINB>;
+        return (void*)trial_kernel_cq<TV, 2, NLB, BUDGET_KB, MINB, 1>;
     }
     *smem = CqGeo<TV, 4, BUDGET_KB, MINB>::BYTES;
-    return (void*)trial_kernel_cq<TV, 4, NLB, BUDGET_KB, MINB>;
+    return (void*)trial_kernel_cq<TV, 4, NLB, BUDGET_KB, MINB, 1>;
 }
 
 // two CTAs/SM: a 2-stage row ring (64 KB) plus the id/occupancy rings per CTA
@@ -1640,11 +1735,21 @@ void* pick_cq(uint32_t nsec, int nl, int variant, int* smem) {
 #undef ARA_CQ_V
 }
 
+// multi-window compacted rounds: up to 4 disjoint windows of equal width
+template <typename TV>
+void* pick_cqm(uint32_t nsec, int* smem) {
+    if (nsec <= 1) { *smem = CqGeo<TV, 1, 64, 2>::BYTES; return (void*)trial_kernel_cq<TV, 1, 4, 64, 2, 4>; }
+    if (nsec <= 2) { *smem = CqGeo<TV, 2, 64, 2>::BYTES; return (void*)trial_kernel_cq<TV, 2, 4, 64, 2, 4>; }
+    *smem = CqGeo<TV, 4, 64, 2>::BYTES;
+    return (void*)trial_kernel_cq<TV, 4, 4, 64, 2, 4>;
+}
+
 // variant: 0 = register-pipelined, 1 = shared-memory staged (cp.async ring),
 // 2-4 = register + L2 prefetch, 5-7 = register at higher occupancy,
 // 8 = TMA gather4 ring (needs p.tmap; windows of <= 4 sectors in one block),
 // 10-13 = cooperative cp.async ring (whole rows per instruction) at 1/2/3 CTAs/SM,
-// 14 = compacted rounds over the cooperative ring (skips zero rows' arithmetic).
+// 14 = compacted rounds over the cooperative ring (skips zero rows' arithmetic),
+// 15 = the same over up to 4 disjoint layer windows in one launch (host-selected).
 void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
     *smem = 0;
     if (variant == 8 && nsec <= 4)
@@ -1655,6 +1760,7 @@ void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
         return fp32 ? pick_co<float>(nsec, nl, variant, smem) : pick_co<double>(nsec, nl, variant, smem);
     if (variant == 14 && nsec <= 4)
         return fp32 ? pick_cq<float>(nsec, nl, variant, smem) : pick_cq<double>(nsec, nl, variant, smem);
+    if (variant == 15 && nsec <= 4) return fp32 ? pick_cqm<float>(nsec, smem) : pick_cqm<double>(nsec, smem);
     return fp32 ? pick<float>(nsec, nl, variant) : pick<double>(nsec, nl, variant);
 }
 

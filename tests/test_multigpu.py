@@ -31,7 +31,8 @@ def _port():
 
 @pytest.mark.parametrize("name,n_trials,rho,p2p", [("tiny", 1000, None, True), ("tiny", 997, None, True),
                                                    ("mini", 20_000, None, True), ("mini", 20_001, 0.01, True),
-                                                   ("tiny", 997, None, False), ("mini", 20_001, 0.01, False)])
+                                                   ("tiny", 997, None, False), ("mini", 20_001, 0.01, False),
+                                                   ("multilayer", 4001, None, True)])
 def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials, rho, p2p):
     """p2p: the kernels store the YLT straight into every rank's global buffer
     over NVLink (fused assembly, the default); otherwise ncclAllGather

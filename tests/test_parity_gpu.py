@@ -105,6 +105,31 @@ def test_edge_trials_and_unaligned_layers(cuda, variant, rho):
         assert (ylt[:, [0, 6, 15]] == 0).all()
 
 
+@pytest.mark.parametrize("n_win,width", [(2, 16), (3, 16), (4, 16), (4, 8), (2, 3)])
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_multi_window_launch(cuda, n_win, width, precision):
+    """ARA_KERNEL=15: disjoint single-layer windows over sparse column blocks
+    run as ONE compacted-rounds launch (one scan, a 4-bit occupancy word per
+    event, one FIFO per window): oracle parity, and bit-identical to one
+    launch per layer (ARA_KERNEL=14) and to the dense kernels."""
+    blk = 16 if precision == "f64" else 32          # ELTs per column block
+    w = synth.get_config("tiny").with_(n_elts=4 * blk, catalog=20_000, rho=0.01, n_trials=1500, nmin=1, nmax=400)
+    off, ids, elts = make_inputs(w)
+    o = (blk - width) // 2                           # window inside its block
+    layers = tuple(synth.LayerSpec(u * blk + o, u * blk + o + width, 1e4 * (u + 1), 5e5 - 5e4 * u,
+                                   2e5 * u, 4e6 if u != 1 else INF) for u in range(n_win))
+    orc = run_oracle(off, ids, elts, w, layers, fp32=precision == "f32")
+    ylt, lossy, st, met = run_gpu(off, ids, elts, w, layers, precision=precision, return_periods=(2, 10, 100),
+                                  variant=15)
+    assert st["kernel_variant"] == 15 and st["n_kernel_launches"] == 1
+    assert_ylt_close(ylt, orc)
+    assert np.array_equal(lossy, orc["lossy"])
+    for v in (14, 5):
+        other, olossy, ost, _ = run_gpu(off, ids, elts, w, layers, precision=precision, variant=v)
+        assert ost["n_kernel_launches"] == n_win
+        assert np.array_equal(ylt, other) and np.array_equal(lossy, olossy)
+
+
 @pytest.mark.parametrize("variant", KERNEL_VARIANTS)
 def test_compacted_rounds_fifo_pressure(cuda, variant):
     """Sparse table, adversarial occupancy patterns for the compacted-rounds
