@@ -24,6 +24,7 @@
 //   * the trial sum is a fixed lane-strided + 5-step xor-shuffle tree;
 //   * validation of YET ids / offsets is fused (error bits, no extra pass).
 // This is a gather-and-reduce path: no tensor cores (not a contraction).
+#include <cstdlib>
 #include <cstring>
 
 #include "ara_internal.cuh"
@@ -1799,6 +1800,10 @@ cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
+    }
+    if (const char* v = getenv("ARA_CARVEOUT")) {   // A/B: shared-memory carveout preference (percent)
+        cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(v));
+        cudaGetLastError();
     }
     void* args[] = {(void*)&p};
     return cudaLaunchKernel(fn, dim3(g), dim3(kThreads), args, (size_t)smem, s);

@@ -5,8 +5,11 @@
 //                     L2 gather ceiling), ids hashed on the fly
 // Separate library (libara_mb.so); not on the product path.  Each call
 // allocates, times `iters` launches with CUDA events, and returns ms/launch.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -226,4 +229,121 @@ extern "C" double mb_tma_gather(uint64_t table_bytes, uint32_t row_bytes, uint64
     if (e != cudaSuccess) return -100 - (double)e;
     // report ms scaled to n_gathers rows
     return ms * (double)n_gathers / (double)(a.spw * 32 * (uint64_t)nsm * MB_WARPS);
+}
+
+// ---------------------------------------------------------------------------
+// Random 4-B lookups into a 256 KB bit table (the row-occupancy bitmap of a
+// 2M-event catalogue): (a) global memory (L1/L2 gather path, what the ARA
+// kernel does per event), (b) a CTA-local shared-memory table (ceiling), (c)
+// the table split over the shared memory of a thread-block cluster of K CTAs,
+// remote parts read through distributed shared memory.
+namespace {
+__global__ void lookup_global(const uint32_t* __restrict__ tab, uint32_t words, uint64_t n, uint32_t seed,
+                              uint32_t* out) {
+    uint32_t acc = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += 8ull * gridDim.x * blockDim.x) {
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t w = hash32((i + (uint64_t)k * gridDim.x * blockDim.x) * 0x9E3779B97F4A7C15ULL + seed) % words;
+            v[k] = __ldg(tab + w);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc ^= v[k];
+    }
+    if (acc == 0x12345678u) out[0] = acc;
+}
+
+__global__ void lookup_smem(uint32_t words, uint64_t n, uint32_t seed, uint32_t* out) {
+    extern __shared__ uint32_t st[];
+    for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) st[i] = hash32(i);
+    __syncthreads();
+    uint32_t acc = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += 8ull * gridDim.x * blockDim.x) {
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t w = hash32((i + (uint64_t)k * gridDim.x * blockDim.x) * 0x9E3779B97F4A7C15ULL + seed) % words;
+            v[k] = st[w];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc ^= v[k];
+    }
+    if (acc == 0x12345678u) out[0] = acc;
+}
+
+__global__ void lookup_dsmem(uint32_t words_per_cta, uint64_t n, uint32_t seed, uint32_t* out) {
+    extern __shared__ uint32_t st[];
+    cg::cluster_group cluster = cg::this_cluster();
+    const uint32_t K = cluster.num_blocks();
+    for (uint32_t i = threadIdx.x; i < words_per_cta; i += blockDim.x) st[i] = hash32(i + cluster.block_rank());
+    cluster.sync();
+    uint32_t acc = 0;
+    const uint32_t words = words_per_cta * K;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += 8ull * gridDim.x * blockDim.x) {
+        uint32_t v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const uint32_t w = hash32((i + (uint64_t)k * gridDim.x * blockDim.x) * 0x9E3779B97F4A7C15ULL + seed) % words;
+            const uint32_t* rp = cluster.map_shared_rank(st, w / words_per_cta);
+            v[k] = rp[w % words_per_cta];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc ^= v[k];
+    }
+    cluster.sync();   // no CTA leaves while others still read its table
+    if (acc == 0x12345678u) out[0] = acc;
+}
+}  // namespace
+
+extern "C" double mb_lookup(int mode, uint32_t table_bytes, int cluster, uint64_t n, int iters) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    uint32_t* out = nullptr;
+    uint32_t* tab = nullptr;
+    cudaMalloc(&out, 4);
+    const uint32_t words = table_bytes / 4;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    float ms = -1.f;
+    if (mode == 0) {
+        cudaMalloc(&tab, table_bytes);
+        cudaMemset(tab, 1, table_bytes);
+        lookup_global<<<nsm * 4, 512>>>(tab, words, n, 1, out);
+        cudaEventRecord(a);
+        for (int i = 0; i < iters; ++i) lookup_global<<<nsm * 4, 512>>>(tab, words, n, 2 + i, out);
+        cudaEventRecord(b);
+    } else if (mode == 1) {
+        cudaFuncSetAttribute(lookup_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)table_bytes);
+        lookup_smem<<<nsm, 1024, table_bytes>>>(words, n, 1, out);
+        cudaEventRecord(a);
+        for (int i = 0; i < iters; ++i) lookup_smem<<<nsm, 1024, table_bytes>>>(words, n, 2 + i, out);
+        cudaEventRecord(b);
+    } else {
+        const uint32_t per = table_bytes / cluster;
+        cudaFuncSetAttribute(lookup_dsmem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)per);
+        cudaFuncSetAttribute(lookup_dsmem, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((nsm / cluster) * cluster);
+        cfg.blockDim = dim3(1024);
+        cfg.dynamicSmemBytes = per;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = cluster;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, lookup_dsmem, per / 4, n, 1u, out);
+        cudaEventRecord(a);
+        for (int i = 0; i < iters; ++i) cudaLaunchKernelEx(&cfg, lookup_dsmem, per / 4, n, (uint32_t)(2 + i), out);
+        cudaEventRecord(b);
+    }
+    if (cudaEventSynchronize(b) == cudaSuccess) cudaEventElapsedTime(&ms, a, b);
+    if (cudaGetLastError() != cudaSuccess) ms = -1.f;
+    cudaFree(out);
+    cudaFree(tab);
+    return ms < 0 ? -1.0 : ms / iters;
 }
