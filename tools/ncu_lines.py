@@ -28,7 +28,12 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
-data = [r for r in rows[2:] if len(r) == len(hdr)]
+data = []
+for r in rows[2:]:   # the first kernel's rows only (a report may hold several launches)
+    if r and r[0] == "Address":
+        break
+    if len(r) == len(hdr):
+        data.append(r)
 ie, si = hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
 a0 = int(data[0][0], 16)
 ins, stall = defaultdict(float), defaultdict(float)
