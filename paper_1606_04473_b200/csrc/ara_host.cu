@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <cstdlib>
 #include <new>
@@ -298,6 +299,7 @@ extern "C" void ara_destroy(ara_ctx* ctx) {
     cudaFree(ctx->d_lossy);
     cudaFree(ctx->d_fold);
     cudaFree(ctx->d_occ4);
+    cudaFree(ctx->d_bm_union);
     cudaFree(ctx->d_sp_off);
     cudaFree(ctx->d_sp_ev);
     cudaFree(ctx->d_sp_ls);
@@ -1079,6 +1081,33 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     const uint32_t n_chunks_fold = (n_layers + nlc - 1) / nlc;
     const uint64_t fold_rows = (uint64_t)ctx->catalog + 1;
     CK(cudaEventRecord(ctx->ev[1], s));
+    // fold mode: per fold chunk, the union occupancy bitmap of its layers'
+    // column blocks (an event outside it has an all-+0 fold row), or null when
+    // some block is dense
+    std::vector<const uint32_t*> fold_bm(n_chunks_fold, nullptr);
+    if (fold && !ctx->no_skip) {
+        const uint32_t* bms = reinterpret_cast<const uint32_t*>(static_cast<const char*>(ctx->d_table) + geo.bm_off);
+        std::vector<std::vector<uint32_t>> blks(n_chunks_fold);
+        bool ok = true;
+        for (uint32_t l = 0; l < n_layers && ok; ++l) {
+            const uint32_t q0 = layers[l].elt_begin / eps, q1 = (layers[l].elt_end + eps - 1) / eps;
+            for (uint32_t b = q0 / spb; b <= (q1 - 1) / spb; ++b) {
+                if (b >= ctx->occ_rows.size() || 2ull * ctx->occ_rows[b] > (uint64_t)ctx->catalog + 1) ok = false;
+                auto& v = blks[l / nlc];
+                if (std::find(v.begin(), v.end(), b) == v.end()) v.push_back(b);
+            }
+        }
+        for (uint32_t fc = 0; fc < n_chunks_fold && ok; ++fc) {
+            if (blks[fc].size() == 1) { fold_bm[fc] = bms + (uint64_t)blks[fc][0] * geo.bm_words; continue; }
+            if (blks[fc].empty() || blks[fc].size() > 8) continue;
+            st = ensure(ctx, ctx->d_bm_union, ctx->bm_union_cap, (size_t)n_chunks_fold * geo.bm_words);
+            if (st != ARA_OK) return st;
+            uint32_t* u = ctx->d_bm_union + (uint64_t)fc * geo.bm_words;
+            CK(launch_bm_union(bms, geo.bm_words, blks[fc].data(), (uint32_t)blks[fc].size(), u, s));
+            fold_bm[fc] = u;
+        }
+        if (!ok) std::fill(fold_bm.begin(), fold_bm.end(), nullptr);
+    }
     if (fold) {
         // a0': fold the catalogue once per run (all layers), bit-identical per-event values
         st = ensure(ctx, ctx->d_fold, ctx->fold_cap, (size_t)n_chunks_fold * fold_rows * nlc);
@@ -1105,6 +1134,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 TrialParams p = base;
                 p.t_begin = chunks[c].first;
                 p.t_end = chunks[c].second;
+                p.bm = fold_bm[fc];
                 p.n_layers = (n_layers - fc * nlc) < nlc ? (n_layers - fc * nlc) : nlc;
                 p.ylt_row0 = fc * nlc;
                 p.portfolio_mode = fc == 0 ? 0 : 1;

@@ -127,6 +127,9 @@ cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const d
 // combined occupancy of up to 4 column blocks: 4 bits per event (bit u = block blk[u])
 cudaError_t launch_occ4(const uint32_t* bitmaps, uint64_t bm_words, const uint32_t* blk, uint32_t n_win,
                         uint32_t catalog, uint32_t* occ4, cudaStream_t s);
+// OR of up to 8 column blocks' occupancy bitmaps
+cudaError_t launch_bm_union(const uint32_t* bitmaps, uint64_t bm_words, const uint32_t* blk, uint32_t nb,
+                            uint32_t* out, cudaStream_t s);
 // zero exactly the rows the occupancy bitmaps mark, then the bitmaps and counters
 cudaError_t launch_clear_rows(void* d_table, const TableGeo& geo, uint32_t catalog, cudaStream_t s);
 cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int grid, int variant, cudaStream_t s);
@@ -240,6 +243,8 @@ struct ara_ctx {
     const double* d_last_full = nullptr;   // global YLT of the last run (metrics input)
     uint32_t* d_occ4 = nullptr;       // combined occupancy map of a multi-window launch
     size_t occ4_cap = 0;
+    uint32_t* d_bm_union = nullptr;   // fold mode: union occupancy of each fold chunk's blocks
+    size_t bm_union_cap = 0;
     int run_mode = 0;                  // ARA_RUN_DIRECT / ARA_RUN_FOLD
     double* d_fold = nullptr;          // fold mode: per-event occurrence-net losses
     size_t fold_cap = 0;

@@ -1551,6 +1551,9 @@ __global__ void __launch_bounds__(kThreads) trial_fold_kernel(const __grid_const
     const uint64_t base = __ldg(p.off);
     const double* fold = p.fold;
     uint32_t err = 0;
+    // (gating the fold-row loads with the occupancy bitmap measured slower here:
+    // 5.85 vs 3.98 ms -- the dependent bitmap load lengthens the load chain;
+    // the scan-based kernel below does gate)
     TrialSched sched;
     sched.init(p, gw, nw);
     uint64_t t = sched.next(p), tn = sched.next(p);
@@ -1622,6 +1625,206 @@ __global__ void __launch_bounds__(kThreads) trial_fold_kernel(const __grid_const
             store_trial(p, t, G, m);
         }
     }
+    peer_fence(p);
+    if (err) atomicOr(p.err, err);
+}
+
+// ---------------------------------------------------------------------------
+// Folded trial pass over the compacted-rounds scan (fold mode default).  The
+// same cross-trial scan as trial_kernel_cq (128-event steps, ids and
+// occupancy words by cp.async into per-warp rings) -- with the union
+// occupancy bitmap of the fold chunk's blocks, L1-resident because this
+// kernel keeps its shared memory small -- and, per event, the fold row
+// o(e)[layers] copied by cp.async only when the event's row is occupied
+// (an unoccupied event's fold row is exactly +0: zero-fill, no memory
+// request).  The fold rows of step s land in a ring slot FR-1 steps before
+// they are added, with trial_fold_kernel's lane mapping, per-lane order and
+// tree: identical YLT bits.
+template <int NL>
+struct FoldCqGeo {
+    using R = CqRings<2>;
+    static constexpr int FR = 3;                                  // fold-row ring slots (steps)
+    static constexpr int SLOT = 128 * NL * 8;                     // one step's fold rows
+    static constexpr int PER_WARP = R::BYTES + FR * SLOT;
+    static constexpr int BYTES = (kThreads / 32) * PER_WARP;
+};
+
+template <int NL>
+__global__ void __launch_bounds__(kThreads, 2) trial_fold_kernel_cq(const __grid_constant__ TrialParams p) {
+    using FG = FoldCqGeo<NL>;
+    using RG = typename FG::R;
+    constexpr int QD = RG::QD, DW = RG::DW, IR = RG::IR, WR = RG::WR, MR = RG::MR, IDB = RG::IDB;
+    constexpr int FR = FG::FR;
+    constexpr int WARPS = kThreads / 32;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+    unsigned char* wsm = smem + wib * FG::PER_WARP;
+    const uint32_t idr = (uint32_t)__cvta_generic_to_shared(wsm);   // id ring [IR][33 x 16 B]
+    const uint32_t ocr = idr + IR * IDB;                            // occupancy ring [WR][128]
+    CqStep* smeta = reinterpret_cast<CqStep*>(wsm + IR * IDB + WR * 512);
+    const uint32_t fr = idr + RG::BYTES;                            // fold rows [FR][4 sub-steps][NL][32]
+    const uint64_t nw = (uint64_t)gridDim.x * WARPS;
+    const uint64_t base = __ldg(p.off);
+    const uint32_t* bm = p.bm;
+    const double* fold = p.fold;
+    uint32_t err = 0;
+
+    uint32_t gseq = 0;
+    auto commit = [&]() { cp_commit(); return gseq++; };
+    auto wait_group = [&](uint32_t g) { cp_wait_upto(gseq - 1u - g); };
+    auto lds_u32 = [&](uint32_t a) {
+        uint32_t v;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+        return v;
+    };
+
+    uint64_t it_t = p.t_begin + (uint64_t)blockIdx.x * WARPS + wib;
+    uint64_t it_a = 0, nx_a = 0, nx_b = 0;
+    uint32_t it_n = 0, it_k0 = 0;
+    bool it_valid = it_t < p.t_end;
+    auto fetch_next_offsets = [&](uint64_t tn) {
+        if (tn < p.t_end) { nx_a = __ldg(p.off + tn); nx_b = __ldg(p.off + tn + 1); }
+    };
+    auto enter_trial = [&](uint64_t a, uint64_t b) {
+        if (b < a) { err |= ERRBIT_OFFSETS; b = a; }
+        it_a = a - base;
+        it_n = (uint32_t)(b - a);
+        it_k0 = 0;
+    };
+    if (it_valid) {
+        enter_trial(__ldg(p.off + it_t), __ldg(p.off + it_t + 1));
+        fetch_next_offsets(it_t + nw);
+    }
+    auto fetch_ids = [&](uint32_t x) {
+        CqStep md{~0ull, 0u, 0u, 0u, 0u};
+        if (it_valid) {
+            const uint32_t cnt = it_n - it_k0 < 128u ? it_n - it_k0 : 128u;
+            const uintptr_t ab = reinterpret_cast<uintptr_t>(p.ids + it_a + it_k0);
+            const uintptr_t al = ab & ~(uintptr_t)15;
+            const uintptr_t end = ab + 4u * cnt;
+            const uint32_t dst = idr + (x % IR) * IDB;
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const uint32_t c = lane + 32u * (uint32_t)r;
+                if (r == 0 || lane == 0) {
+                    const uintptr_t cs = al + 16u * c;
+                    const uint32_t nb = cs >= end ? 0u : (end - cs >= 16u ? 16u : (uint32_t)(end - cs));
+                    cp_async16(dst + 16u * c, reinterpret_cast<const void*>(nb ? cs : al), nb);
+                }
+            }
+            md = CqStep{it_t, it_n, it_k0, (uint32_t)(ab - al) / 4u, 0u};
+            it_k0 += 128u;
+            if (it_k0 >= it_n) {
+                it_t += nw;
+                it_valid = it_t < p.t_end;
+                if (it_valid) {
+                    enter_trial(nx_a, nx_b);
+                    fetch_next_offsets(it_t + nw);
+                }
+            }
+        }
+        if (lane == 0) smeta[x % MR] = md;
+    };
+    auto fetch_occupancy = [&](uint32_t x) {
+        const uint32_t sh = smeta[x % MR].sh;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t e = lds_u32(idr + (x % IR) * IDB + (sh + 32u * j + lane) * 4u);
+            e = e <= p.catalog ? e : 0u;
+            cp_async4(ocr + ((x % WR) * 128u + 32u * j + lane) * 4u, bm + (e >> 5), bm ? 4u : 0u);
+        }
+    };
+
+#pragma unroll 1
+    for (uint32_t x = 0; x < (uint32_t)QD; ++x) fetch_ids(x);
+    wait_group(commit());
+    __syncwarp();
+    uint32_t g_occ = 0;
+#pragma unroll 1
+    for (uint32_t x = 0; x < (uint32_t)DW; ++x) {
+        fetch_occupancy(x);
+        g_occ = commit();
+    }
+
+    double G[NL];
+    uint32_t m[NL];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) { G[l] = 0.0; m[l] = 0u; }
+    uint32_t gf[FR];   // commit group of each fold-row slot
+
+    // add step x's fold rows (landed) to the lanes' sums; finalise its trial
+    auto consume = [&](uint32_t x) {
+        uint32_t g = gf[0];
+#pragma unroll
+        for (int i = 1; i < FR; ++i) g = ((x % FR) == (uint32_t)i) ? gf[i] : g;
+        wait_group(g);
+        __syncwarp();
+        const CqStep md = smeta[x % MR];
+        const uint32_t src = fr + (x % FR) * FG::SLOT + lane * 8u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int l = 0; l < NL; ++l) {
+                double o;
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(o) : "r"(src + ((uint32_t)(j * NL + l) * 32u) * 8u)
+                             : "memory");
+                G[l] = __dadd_rn(G[l], o);
+                m[l] += (o > 0.0) ? 1u : 0u;
+            }
+        if (md.k0 + 128u >= md.n) {   // last step of trial md.t: a7 + a8
+#pragma unroll
+            for (int l = 0; l < NL; ++l) {
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) {
+                    G[l] = __dadd_rn(G[l], __shfl_xor_sync(0xffffffffu, G[l], off));
+                    m[l] += __shfl_xor_sync(0xffffffffu, m[l], off);
+                }
+            }
+            if (lane == 0) store_trial(p, md.t, G, m);
+#pragma unroll
+            for (int l = 0; l < NL; ++l) { G[l] = 0.0; m[l] = 0u; }
+        }
+    };
+
+    uint32_t sc = 0;
+#pragma unroll 1
+    for (;; ++sc) {
+        wait_group(g_occ);
+        __syncwarp();
+        const CqStep md = smeta[sc % MR];
+        if (md.t == ~0ull) break;
+        fetch_occupancy(sc + DW);
+        g_occ = commit();
+        fetch_ids(sc + QD);
+        commit();
+        // this step's fold rows: lanes with an occupied event copy o(e)[0..NL)
+        const uint32_t id_base = idr + (sc % IR) * IDB + (md.sh + lane) * 4u;
+        const uint32_t oc_base = ocr + ((sc % WR) * 128u + lane) * 4u;
+        const uint32_t n_here = md.n - md.k0;
+        const uint32_t dst = fr + (sc % FR) * FG::SLOT + lane * 8u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t e = lds_u32(id_base + 128u * j);
+            const uint32_t w = lds_u32(oc_base + 128u * j);
+            const bool live = 32u * (uint32_t)j + lane < n_here;
+            const bool bad = live && e - 1u >= p.catalog;
+            err |= bad ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
+            e = (live && !bad && (!bm || ((w >> (e & 31u)) & 1u))) ? e : 0u;
+            const double* row = fold + (uint64_t)e * p.fold_stride;
+#pragma unroll
+            for (int l = 0; l < NL; ++l)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst + ((uint32_t)(j * NL + l) * 32u) * 8u),
+                             "l"(row + l), "r"(e ? 8u : 0u)
+                             : "memory");
+        }
+        const uint32_t g = commit();
+#pragma unroll
+        for (int i = 0; i < FR; ++i) gf[i] = ((sc % FR) == (uint32_t)i) ? g : gf[i];
+        if (sc + 1 >= (uint32_t)FR) consume(sc + 1 - FR);
+        __syncwarp();
+    }
+    for (uint32_t x = sc + 1 >= (uint32_t)FR ? sc + 1 - FR : 0; x < sc; ++x) consume(x);
+    cp_wait<0>();
     peer_fence(p);
     if (err) atomicOr(p.err, err);
 }
@@ -1835,14 +2038,39 @@ cudaError_t launch_fold(const TrialParams& p, int fp32, uint32_t nsec, cudaStrea
 
 cudaError_t launch_trials_folded(const TrialParams& p, int grid_mult_x100, cudaStream_t s) {
     if (p.t_end <= p.t_begin) return cudaSuccess;
-    void* fn = p.fold_stride <= 1 ? (void*)trial_fold_kernel<1>
-               : p.fold_stride <= 2 ? (void*)trial_fold_kernel<2>
-               : p.fold_stride <= 4 ? (void*)trial_fold_kernel<4>
-                                    : (void*)trial_fold_kernel<8>;
+    // per-trial folded pass (default), or the scan-based one (ARA_FOLD_KERNEL=1, A/B:
+    // measured slower, 5.1 vs 4.0 ms on the paper config -- the scan costs more
+    // than the one-gather-per-event pass it replaces)
+    static int legacy = -1;
+    if (legacy < 0) {
+        const char* v = getenv("ARA_FOLD_KERNEL");
+        legacy = (v && atoi(v) == 1) ? 0 : 1;
+    }
+    void* fn;
+    int smem = 0;
+    if (!legacy) {
+        fn = p.fold_stride <= 1 ? (void*)trial_fold_kernel_cq<1>
+             : p.fold_stride <= 2 ? (void*)trial_fold_kernel_cq<2>
+             : p.fold_stride <= 4 ? (void*)trial_fold_kernel_cq<4>
+                                  : (void*)trial_fold_kernel_cq<8>;
+        smem = p.fold_stride <= 1 ? FoldCqGeo<1>::BYTES
+               : p.fold_stride <= 2 ? FoldCqGeo<2>::BYTES
+               : p.fold_stride <= 4 ? FoldCqGeo<4>::BYTES
+                                    : FoldCqGeo<8>::BYTES;
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+        }
+    } else {
+        fn = p.fold_stride <= 1 ? (void*)trial_fold_kernel<1>
+             : p.fold_stride <= 2 ? (void*)trial_fold_kernel<2>
+             : p.fold_stride <= 4 ? (void*)trial_fold_kernel<4>
+                                  : (void*)trial_fold_kernel<8>;
+    }
     int dev = 0, nsm = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, 0) != cudaSuccess || per_sm < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem) != cudaSuccess || per_sm < 1) {
         cudaGetLastError();
         per_sm = 1;
     }
@@ -1851,7 +2079,7 @@ cudaError_t launch_trials_folded(const TrialParams& p, int grid_mult_x100, cudaS
     if (grid > need) grid = need;
     if (grid < 1) grid = 1;
     void* args[] = {(void*)&p};
-    return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kThreads), args, 0, s);
+    return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(kThreads), args, (size_t)smem, s);
 }
 
 // Program rows (Alg. 1 l.1): Y_prog[q][t] = sum of the program's layer rows, in

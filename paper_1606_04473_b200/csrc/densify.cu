@@ -123,6 +123,30 @@ cudaError_t launch_occ4(const uint32_t* bitmaps, uint64_t bm_words, const uint32
     return cudaGetLastError();
 }
 
+// union of up to 8 column blocks' occupancy bitmaps (fold chunks of several layers)
+__global__ void __launch_bounds__(256) bm_union_kernel(const uint32_t* __restrict__ bitmaps, uint64_t bm_words,
+                                                       const uint4 blk_lo, const uint4 blk_hi, uint32_t nb,
+                                                       uint32_t* __restrict__ out) {
+    const uint32_t blk[8] = {blk_lo.x, blk_lo.y, blk_lo.z, blk_lo.w, blk_hi.x, blk_hi.y, blk_hi.z, blk_hi.w};
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < bm_words;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t w = 0;
+        for (uint32_t k = 0; k < nb; ++k) w |= bitmaps[(uint64_t)blk[k] * bm_words + i];
+        out[i] = w;
+    }
+}
+
+cudaError_t launch_bm_union(const uint32_t* bitmaps, uint64_t bm_words, const uint32_t* blk, uint32_t nb,
+                            uint32_t* out, cudaStream_t s) {
+    uint32_t b[8] = {};
+    for (uint32_t k = 0; k < nb && k < 8; ++k) b[k] = blk[k];
+    uint64_t blocks = (bm_words + 255) / 256;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    bm_union_kernel<<<(unsigned)blocks, 256, 0, s>>>(bitmaps, bm_words, make_uint4(b[0], b[1], b[2], b[3]),
+                                                     make_uint4(b[4], b[5], b[6], b[7]), nb < 8 ? nb : 8, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_clear_rows(void* d_table, const TableGeo& geo, uint32_t catalog, cudaStream_t s) {
     const uint64_t n = (uint64_t)geo.n_blocks * geo.bm_words;
     uint64_t blocks = (n + 255) / 256;

@@ -14,22 +14,31 @@ pytestmark = pytest.mark.gpu
 INF = math.inf
 
 
+@pytest.mark.parametrize("fold_kernel", ["scan", "per_trial"])
+@pytest.mark.parametrize("rho", [0.3, 0.02])
 @pytest.mark.parametrize("precision", ["f64", "f32"])
-def test_fold_equals_direct_tiny(cuda, precision):
-    w = synth.get_config("tiny")
+def test_fold_equals_direct_tiny(cuda, precision, rho, fold_kernel):
+    """rho = 0.02: the folded pass skips unoccupied events (union occupancy
+    bitmap); fold_kernel: the per-trial pass (default) or the scan-based one
+    (ARA_FOLD_KERNEL=1)."""
+    w = synth.get_config("tiny").with_(rho=rho)
     off, ids, elts = make_inputs(w)
+    env = {"ARA_FOLD_KERNEL": 1} if fold_kernel == "scan" else None
     a = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100))
-    b = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100), run_mode="fold")
+    b = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100), run_mode="fold",
+                env=env)
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert np.array_equal(a[3][1], b[3][1]) and np.array_equal(a[3][2], b[3][2])
     assert_ylt_close(b[0], run_oracle(off, ids, elts, w, w.layers, fp32=precision == "f32"))
 
 
+@pytest.mark.parametrize("rho", [0.3, 0.01])
 @pytest.mark.parametrize("n_layers", [1, 3, 5, 9, 17])
-def test_fold_many_layers_and_chunks(cuda, n_layers):
+def test_fold_many_layers_and_chunks(cuda, n_layers, rho):
     """Layer counts that exercise fold chunks of 1, 4, 8 layers and several
-    folded launches; windows unaligned and shared."""
-    w = synth.get_config("tiny").with_(n_elts=24, catalog=2000, rho=0.3, n_trials=600, nmin=0, nmax=260)
+    folded launches; windows unaligned and shared; rho = 0.01: sparse blocks,
+    union occupancy bitmaps over 1-2 blocks per fold chunk."""
+    w = synth.get_config("tiny").with_(n_elts=24, catalog=2000, rho=rho, n_trials=600, nmin=0, nmax=260)
     off, ids, elts = make_inputs(w)
     rng = np.random.default_rng(n_layers)
     layers = []
