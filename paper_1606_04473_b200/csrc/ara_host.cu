@@ -1403,7 +1403,8 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
         ld = ctx->T_local ? ctx->T_local : 1;
     }
     int nblk = (int)((T + 4095) / 4096);
-    const int maxblk = (2 * ctx->n_sm + (int)rows - 1) / (int)rows;
+    static const int blk_mult = [] { const char* v = getenv("ARA_METRICS_BLOCKS"); return v ? atoi(v) : 2; }();
+    const int maxblk = (blk_mult * ctx->n_sm + (int)rows - 1) / (int)rows;
     if (nblk > maxblk) nblk = maxblk;
     if (nblk < 1) nblk = 1;
     CK(metrics_alloc(ctx->ms, rows, n_rp, nblk > 2 * ctx->n_sm ? nblk : 2 * ctx->n_sm));   // + cooperative grid
