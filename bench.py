@@ -519,8 +519,10 @@ def main():
                              "step": ms,
                              "calls": {k: float(np.median([p[i] for p in part_ms]))
                                        for i, k in enumerate(("load_elts", "load_yet", "run", "metrics"))}},
-            # our kernels per step: densify + ARA launches (incl. fold/program kernels) + metrics (init, 8 passes, tail)
-            "gpu_launches": int(a.steps * (1 + np.mean(launches) + 10)),
+            # our kernels per timed step: load_elts = clear_rows (the table was densified
+            # before) + densify; ara_run = n_kernel_launches; ara_metrics = init + 8 radix
+            # passes + tail
+            "gpu_launches": int(a.steps * (2 + np.mean(launches) + 10)),
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
             "host": host_info(), "gen_seconds": gen_s,
         }

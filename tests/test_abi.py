@@ -115,3 +115,32 @@ def test_pack_ids_matches_bit_layout():
                 assert (as_int >> (int(i) * bits)) & ((1 << bits) - 1) == ids[i]
     with pytest.raises(ara.AraError):
         ara.ara_pack_ids(np.array([1 << 21], np.uint32), 21)
+
+
+def test_binding_structs_match_the_c_header(tmp_path):
+    """The ctypes mirrors of the ABI structs have the C header's size and field
+    offsets (a mismatch would silently corrupt arguments or stats)."""
+    import ctypes
+    import subprocess
+    from paper_1606_04473_b200 import ara
+    structs = {"ara_config": ara.ara_config, "ara_elt_terms": ara.ara_elt_terms, "ara_layer": ara.ara_layer,
+               "ara_layer_list": ara.ara_layer_list, "ara_run_stats": ara.ara_run_stats}
+    lines = ['#include <stddef.h>', '#include <stdio.h>', '#include "ara.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} size %zu\\n", sizeof({name}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{name} {f} %zu\\n", offsetof({name}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)], check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n"):
+        if line:
+            n, f, v = line.split()
+            got[(n, f)] = int(v)
+    for name, cls in structs.items():
+        assert got[(name, "size")] == ctypes.sizeof(cls), name
+        for f, _ in cls._fields_:
+            assert got[(name, f)] == getattr(cls, f).offset, (name, f)
