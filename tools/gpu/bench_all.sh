@@ -12,3 +12,9 @@ tail -3 gpurun_out/smoke.log; tail -3 gpurun_out/pytest_gpu.log
 for f in bench bench_f32 bench_ml bench_tower bench_fold; do python -c "
 import json;d=json.load(open('gpurun_out/$f.json'));r=d['roofline'];print('$f',round(d['ms_per_step'],3),round(d['value']/1e6,2),'Mtrials/s k',round(r['kernel_ms'],3),r['kernel'],'frac',round(r['frac'],3),'l2',r.get('l2_frac'),'e2e',round(d['e2e']['ms_per_step'],2) if d.get('e2e') else None)"; done
 head -c 600 gpurun_out/bench_ref.json
+B="python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e"
+timeout 600 $B > gpurun_out/plain.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu_launches.log 2>&1
+Q="python tools/prof_ara.py --steps 1"
+timeout 300 $Q > gpurun_out/plain_q.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:trial_kernel -c 1 -o gpurun_out/prof_default $Q > gpurun_out/ncu_full.log 2>&1
