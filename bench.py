@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--l2-persist", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every GPU runs its own paper-shaped YET shard (N x 1M trials in all, one "
+                         "global YLT, metrics over all of it); strong: the 1M trials split over the GPUs")
     ap.add_argument("--mode", default="direct", choices=["direct", "fold"],
                     help="direct = Alg. 3 per occurrence (headline); fold = catalogue-fold mode (SURVEY 8f F2)")
     return ap.parse_args()
@@ -249,10 +252,13 @@ def reference_arm(a, rank, world):
             res.append(r)
     tps = float(np.median([r["trials_per_s"] for r in res]))
     sample = f"first {res[0]['trials']} trials of the {w.name} workload per step, dense direct-access lookups"
+    # the same config as our arm (weak scaling: N x the workload's trials); the
+    # oracle's rate is measured on the bounded sample above
+    n_trials = w.n_trials * (world if a.scaling == "weak" else 1)
     line = {"impl": "reference", "metric": METRIC, "value": tps, "unit": "trials/s", "n_gpus": a.gpus,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * w.n_trials / tps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": a.precision,
-            "data": "synthetic", "config": {"workload": w.name, "n_trials": w.n_trials},
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * n_trials / tps,
+            "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": a.precision,
+            "data": "synthetic", "config": {"workload": w.name, "n_trials": n_trials},
             "lookups_per_sec": float(np.median([r["lookups_per_s"] for r in res])),
             "cpu_baseline": {"value": tps, "unit": "trials/s", "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": tps, "unit": "trials/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -297,6 +303,11 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     w = synth.get_config(a.config)
+    trials_per_gpu = w.n_trials
+    if a.scaling == "weak":   # N x the workload's trials; rank r holds trials [r T1, (r+1) T1)
+        w = w.with_(n_trials=w.n_trials * world)
+    else:
+        trials_per_gpu = (w.n_trials + world - 1) // world
     T = w.n_trials
     first, count = ara.ara_partition(T, world, rank)
     stream = torch.cuda.current_stream()
@@ -483,9 +494,10 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "trials/s", "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": a.scaling,
             "vs_baseline": None, "dtype": a.precision, "data": "synthetic",
-            "config": {"workload": w.name, "n_trials": T, "events_per_trial": [w.nmin, w.nmax],
+            "config": {"workload": w.name, "n_trials": T, "trials_per_gpu": trials_per_gpu,
+                       "events_per_trial": [w.nmin, w.nmax],
                        "n_events": n_events_global, "elts_per_layer": [Lr.elt_end - Lr.elt_begin for Lr in w.layers],
                        "catalog": w.catalog, "layers": L, "return_periods": len(R), "parallelism": f"trials/{world}",
                        "l2": "inputs larger than L2 (4 GB YET streamed once per step; 256 MB table)",

@@ -232,6 +232,7 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
     if (const char* v = getenv("ARA_PFN")) ctx->pf_sectors = atoi(v);
     if (const char* v = getenv("ARA_NO_SKIP")) ctx->no_skip = atoi(v) != 0;
     if (const char* v = getenv("ARA_NO_P2P")) ctx->use_p2p = atoi(v) == 0;
+    if (const char* v = getenv("ARA_METRICS_DIST")) ctx->metrics_dist = atoi(v);
     if (const char* v = getenv("ARA_BATCH")) ctx->batch = (uint32_t)atoi(v) ? (uint32_t)atoi(v) : 4u;
     auto bail = [&](ara_status st) {
         ara_destroy(ctx);
@@ -1356,6 +1357,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     ctx->last_layers = n_layers;
     ctx->last_rows = rows;
     ctx->d_last_full = d_full;
+    ctx->last_ld_local = ld;
     if (use_p2p) ctx->p2p_next ^= 1;
     if (stats) {
         const uint64_t nev = T_local ? ctx->h_small[2] - ctx->h_small[1] : 0;
@@ -1410,7 +1412,22 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
     CK(metrics_alloc(ctx->ms, rows, n_rp, nblk > 2 * ctx->n_sm ? nblk : 2 * ctx->n_sm));   // + cooperative grid
     cudaStream_t s = ctx->stream;
     CK(cudaEventRecord(ctx->ev[0], s));
-    CK(launch_metrics(d_y, T, ld, rows, n_rp, hk, ctx->ms, nblk, s));
+    // Distributed select (F4) on large global YLTs: every rank histograms only
+    // its own shard and the histograms are all-reduced, instead of every rank
+    // sweeping the whole global YLT (which grows with N under weak scaling).
+    const bool dist = ctx->world > 1 && (ctx->metrics_dist > 0 || (ctx->metrics_dist < 0 && T >= 3000000));
+    if (dist) {
+        int nerr = 0;
+        const uint64_t Tl = ctx->T_local;
+        int nb = (int)((Tl + 4095) / 4096);
+        if (nb > maxblk) nb = maxblk;
+        if (nb < 1) nb = 1;
+        CK(launch_metrics_dist(ctx->d_ylt_local, Tl, ctx->last_ld_local ? ctx->last_ld_local : 1, rows, n_rp, hk,
+                               ctx->ms, nb, ctx->comm, s, &nerr));
+        if (nerr) return fail(ctx, ARA_ERR_NCCL, "NCCL all-reduce in the distributed metrics failed");
+    } else {
+        CK(launch_metrics(d_y, T, ld, rows, n_rp, hk, ctx->ms, nblk, s));
+    }
     CK(cudaEventRecord(ctx->ev[1], s));
     std::vector<double> out((size_t)rows * n_rp * 2);
     CK(cudaMemcpyAsync(out.data(), ctx->ms.out, out.size() * sizeof(double), cudaMemcpyDeviceToHost, s));

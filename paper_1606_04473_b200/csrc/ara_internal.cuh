@@ -154,6 +154,8 @@ struct MetricsScratch {
     double* out = nullptr;          // [rows][n_rp][2] pml, tvar
     uint32_t* done = nullptr;       // block-completion counters
     uint32_t* coop_hist = nullptr;  // [3][rows * n_rp][256] rotating histograms (cooperative path)
+    double* dsum = nullptr;         // distributed select: tail sums / counts per (row, period)
+    uint64_t* dcnt = nullptr;
     size_t cap_rows_rp = 0;
     uint32_t cap_rows = 0;
     int nblk = 0;                   // capacity in blocks
@@ -162,6 +164,13 @@ cudaError_t metrics_alloc(MetricsScratch& m, uint32_t rows, uint32_t n_rp, int n
 void metrics_free(MetricsScratch& m);
 cudaError_t launch_metrics(const double* d_ylt, uint64_t T, uint64_t ld, uint32_t rows,
                            uint32_t n_rp, const uint64_t* h_k, MetricsScratch& m, int nblk, cudaStream_t s);
+// Distributed select: each rank histograms its own YLT shard
+// [rows][T_local] (row stride ld); the per-pass histograms and the tail sums are
+// all-reduced over `comm`, so every rank derives the same global PML/TVaR
+// without the global YLT.  *nccl_err is set when an NCCL call failed.
+cudaError_t launch_metrics_dist(const double* d_ylt, uint64_t T_local, uint64_t ld, uint32_t rows, uint32_t n_rp,
+                                const uint64_t* h_k, MetricsScratch& m, int nblk, ncclComm_t comm,
+                                cudaStream_t s, int* nccl_err);
 
 }  // namespace ara
 
@@ -241,6 +250,8 @@ struct ara_ctx {
     int p2p_next = 0;                 // buffer of the next run
     bool use_p2p = true;              // ARA_NO_P2P=1: assemble the YLT with ncclAllGather instead
     const double* d_last_full = nullptr;   // global YLT of the last run (metrics input)
+    uint64_t last_ld_local = 0;       // row stride of d_ylt_local in the last run
+    int metrics_dist = -1;            // ARA_METRICS_DIST: -1 auto (distributed when T >= 3M), 0 off, 1 on
     uint32_t* d_occ4 = nullptr;       // combined occupancy map of a multi-window launch
     size_t occ4_cap = 0;
     uint32_t* d_bm_union = nullptr;   // fold mode: union occupancy of each fold chunk's blocks

@@ -36,6 +36,9 @@ struct MParams {
     uint64_t* part_cnt;  // [rows][n_rp][nblk]
     double* out;         // [rows][n_rp][2]
     uint32_t* done;      // [rows]
+    double* dsum;        // distributed mode: this rank's tail sums [rows][n_rp] ...
+    uint64_t* dcnt;      // ... and counts (all-reduced across ranks, then finished)
+    int dist;            // 1: the YLT is this rank's shard; histograms and sums are all-reduced
     uint64_t k[ARA_MAX_RP];
 };
 
@@ -52,6 +55,62 @@ __global__ void init_kernel(const __grid_constant__ MParams P) {
     }
     for (uint32_t i = threadIdx.x; i < P.n_rp * 256u; i += blockDim.x) P.hist[(uint64_t)row * P.n_rp * 256 + i] = 0;
     if (threadIdx.x == 0) P.done[row] = 0;
+}
+
+// Pick the digit of every return period of `row` from the row's (complete)
+// global histograms: stage them in shared memory, one warp per return period
+// scans from the top digit down; update prefix / remaining rank / reps and
+// clear the histograms.  (The last block of a pass, or select_kernel.)
+__device__ void select_row(const MParams& P, uint32_t row, int shift, uint32_t* sh, uint64_t* s_prefix) {
+    const uint32_t n_rp = P.n_rp;
+    const uint32_t lane = threadIdx.x & 31u;
+    uint32_t* gh = P.hist + (uint64_t)row * n_rp * 256;
+    __shared__ uint32_t s_rep2[ARA_MAX_RP];
+    for (uint32_t i = threadIdx.x; i < n_rp; i += blockDim.x) s_rep2[i] = P.rep[row * n_rp + i];
+    __syncthreads();
+    const uint32_t* s_rep = s_rep2;
+    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) sh[i] = (s_rep[i >> 8] == (i >> 8)) ? __ldcg(gh + i) : 0u;
+    __syncthreads();
+    const uint32_t wid = threadIdx.x >> 5;
+    for (uint32_t r = wid; r < n_rp; r += blockDim.x >> 5) {
+        const uint32_t* h = sh + s_rep[r] * 256;
+        const uint64_t kr = P.krem[row * n_rp + r];
+        // lane l owns digits 255-8l .. 248-8l (descending)
+        uint32_t c[8];
+        uint64_t tot = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) { c[q] = h[255 - 8 * lane - q]; tot += c[q]; }
+        uint64_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += v;
+        }
+        const uint64_t excl = incl - tot;
+        const unsigned hit = __ballot_sync(0xffffffffu, excl < kr && kr <= incl);
+        const uint32_t src = (uint32_t)(__ffs(hit) - 1);
+        if (lane == src) {
+            uint64_t cum = excl;
+            uint32_t d = 255 - 8 * lane;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (kr <= cum + c[q]) { d = 255 - 8 * lane - q; break; }
+                cum += c[q];
+            }
+            const uint64_t pre = s_prefix[r] | ((uint64_t)d << shift);
+            P.prefix[row * n_rp + r] = pre;
+            P.krem[row * n_rp + r] = kr - cum;
+            s_prefix[r] = pre;
+        }
+    }
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < n_rp; r += blockDim.x) {
+        uint32_t rr = r;
+        for (uint32_t q = 0; q < r; ++q)
+            if (s_prefix[q] == s_prefix[r]) { rr = q; break; }
+        P.rep[row * n_rp + r] = rr;
+    }
+    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) gh[i] = 0;
 }
 
 __global__ void __launch_bounds__(256) radix_pass_kernel(const __grid_constant__ MParams P, int pass) {
@@ -119,6 +178,7 @@ __global__ void __launch_bounds__(256) radix_pass_kernel(const __grid_constant__
     uint32_t* gh = P.hist + (uint64_t)row * n_rp * 256;
     for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x)
         if (sh[i]) atomicAdd(&gh[i], sh[i]);
+    if (P.dist) return;   // the histograms are all-reduced across ranks, then select_kernel
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = (atomicAdd(&P.done[row], 1u) == P.nblk - 1) ? 1u : 0u;
@@ -126,52 +186,29 @@ __global__ void __launch_bounds__(256) radix_pass_kernel(const __grid_constant__
     if (!s_last) return;
     __threadfence();
 
-    // Last block of this row: stage the row's histograms in shared memory
-    // (coalesced), then one warp per return period finds the digit with a
-    // warp-wide scan from the top digit down.
-    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) sh[i] = (s_rep[i >> 8] == (i >> 8)) ? __ldcg(gh + i) : 0u;
-    __syncthreads();
-    const uint32_t wid = threadIdx.x >> 5;
-    for (uint32_t r = wid; r < n_rp; r += blockDim.x >> 5) {
-        const uint32_t* h = sh + s_rep[r] * 256;
-        const uint64_t kr = P.krem[row * n_rp + r];
-        // lane l owns digits 255-8l .. 248-8l (descending)
-        uint32_t c[8];
-        uint64_t tot = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) { c[q] = h[255 - 8 * lane - q]; tot += c[q]; }
-        uint64_t incl = tot;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= (uint32_t)o) incl += v;
-        }
-        const uint64_t excl = incl - tot;
-        const unsigned hit = __ballot_sync(0xffffffffu, excl < kr && kr <= incl);
-        const uint32_t src = (uint32_t)(__ffs(hit) - 1);
-        if (lane == src) {
-            uint64_t cum = excl;
-            uint32_t d = 255 - 8 * lane;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                if (kr <= cum + c[q]) { d = 255 - 8 * lane - q; break; }
-                cum += c[q];
-            }
-            const uint64_t pre = s_prefix[r] | ((uint64_t)d << shift);
-            P.prefix[row * n_rp + r] = pre;
-            P.krem[row * n_rp + r] = kr - cum;
-            s_prefix[r] = pre;
-        }
-    }
-    __syncthreads();
-    for (uint32_t r = threadIdx.x; r < n_rp; r += blockDim.x) {
-        uint32_t rr = r;
-        for (uint32_t q = 0; q < r; ++q)
-            if (s_prefix[q] == s_prefix[r]) { rr = q; break; }
-        P.rep[row * n_rp + r] = rr;
-    }
-    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) gh[i] = 0;
+    select_row(P, row, shift, sh, s_prefix);
     if (threadIdx.x == 0) P.done[row] = 0;
+}
+
+// distributed mode: one block per row picks the digits from the all-reduced histograms
+__global__ void __launch_bounds__(256) select_kernel(const __grid_constant__ MParams P, int pass) {
+    extern __shared__ uint32_t sh[];
+    __shared__ uint64_t s_prefix[ARA_MAX_RP];
+    const uint32_t row = blockIdx.x;
+    for (uint32_t i = threadIdx.x; i < P.n_rp; i += blockDim.x) s_prefix[i] = P.prefix[row * P.n_rp + i];
+    __syncthreads();
+    select_row(P, row, 56 - 8 * pass, sh, s_prefix);
+}
+
+// distributed mode: TVaR from the all-reduced tail sums and counts
+__global__ void finish_kernel(const __grid_constant__ MParams P, uint32_t rows) {
+    for (uint32_t q = threadIdx.x; q < rows * P.n_rp; q += blockDim.x) {
+        const double v = __longlong_as_double((long long)P.prefix[q]);
+        const uint64_t k = P.k[q % P.n_rp];
+        const double tail = __dadd_rn(P.dsum[q], __dmul_rn((double)(k - P.dcnt[q]), v));
+        P.out[(uint64_t)q * 2 + 0] = v;
+        P.out[(uint64_t)q * 2 + 1] = __ddiv_rn(tail, (double)k);
+    }
 }
 
 __global__ void __launch_bounds__(256) tail_kernel(const __grid_constant__ MParams P) {
@@ -256,10 +293,15 @@ __global__ void __launch_bounds__(256) tail_kernel(const __grid_constant__ MPara
             }
         }
         if (lane == 0) {
-            const uint64_t k = P.k[r];
-            const double tail = __dadd_rn(s, __dmul_rn((double)(k - c), v));
-            P.out[((uint64_t)row * n_rp + r) * 2 + 0] = v;
-            P.out[((uint64_t)row * n_rp + r) * 2 + 1] = __ddiv_rn(tail, (double)k);
+            if (P.dist) {   // this rank's share; finish_kernel completes it after the all-reduce
+                P.dsum[(uint64_t)row * n_rp + r] = s;
+                P.dcnt[(uint64_t)row * n_rp + r] = c;
+            } else {
+                const uint64_t k = P.k[r];
+                const double tail = __dadd_rn(s, __dmul_rn((double)(k - c), v));
+                P.out[((uint64_t)row * n_rp + r) * 2 + 0] = v;
+                P.out[((uint64_t)row * n_rp + r) * 2 + 1] = __ddiv_rn(tail, (double)k);
+            }
         }
     }
     if (threadIdx.x == 0) P.done[row] = 0;
@@ -485,6 +527,54 @@ __global__ void __launch_bounds__(256) metrics_coop_kernel(const __grid_constant
 
 }  // namespace
 
+cudaError_t launch_metrics_dist(const double* d_ylt, uint64_t T_local, uint64_t ld, uint32_t rows, uint32_t n_rp,
+                                const uint64_t* h_k, MetricsScratch& m, int nblk, ncclComm_t comm,
+                                cudaStream_t s, int* nccl_err) {
+    MParams P{};
+    P.ylt = d_ylt;
+    P.T = T_local;
+    P.ld = ld;
+    P.n_rp = n_rp;
+    P.nblk = (uint32_t)nblk;
+    P.hist = m.hist;
+    P.prefix = m.prefix;
+    P.krem = m.krem;
+    P.part_sum = m.part_sum;
+    P.part_cnt = m.part_cnt;
+    P.out = m.out;
+    P.done = m.done;
+    P.rep = m.done + rows;
+    P.dsum = m.dsum;
+    P.dcnt = m.dcnt;
+    P.dist = 1;
+    for (uint32_t i = 0; i < n_rp; ++i) P.k[i] = h_k[i];
+    const size_t smem = (size_t)n_rp * 256 * sizeof(uint32_t);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(radix_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    *nccl_err = 0;
+    init_kernel<<<rows, 256, 0, s>>>(P);
+    const size_t nh = (size_t)rows * n_rp * 256;
+    for (int pass = 0; pass < 8; ++pass) {
+        radix_pass_kernel<<<dim3(P.nblk, rows), 256, smem, s>>>(P, pass);
+        if (ncclAllReduce(P.hist, P.hist, nh, ncclUint32, ncclSum, comm, s) != ncclSuccess) { *nccl_err = 1; break; }
+        select_kernel<<<rows, 256, smem, s>>>(P, pass);
+    }
+    if (*nccl_err) return cudaGetLastError();
+    tail_kernel<<<dim3(P.nblk, rows), 256, 0, s>>>(P);
+    const size_t nq = (size_t)rows * n_rp;
+    if (ncclGroupStart() != ncclSuccess || ncclAllReduce(P.dsum, P.dsum, nq, ncclDouble, ncclSum, comm, s) != ncclSuccess ||
+        ncclAllReduce(P.dcnt, P.dcnt, nq, ncclUint64, ncclSum, comm, s) != ncclSuccess || ncclGroupEnd() != ncclSuccess) {
+        *nccl_err = 1;
+        return cudaGetLastError();
+    }
+    finish_kernel<<<1, 256, 0, s>>>(P, rows);
+    return cudaGetLastError();
+}
+
 cudaError_t metrics_alloc(MetricsScratch& m, uint32_t rows, uint32_t n_rp, int nblk) {
     const size_t need = (size_t)rows * n_rp;
     if (m.cap_rows_rp >= need && m.nblk >= nblk && m.cap_rows >= rows) return cudaSuccess;
@@ -499,6 +589,8 @@ cudaError_t metrics_alloc(MetricsScratch& m, uint32_t rows, uint32_t n_rp, int n
     if ((e = cudaMalloc(&m.out, rr * 2 * sizeof(double))) != cudaSuccess) return e;
     if ((e = cudaMalloc(&m.done, rows * sizeof(uint32_t) + rr * sizeof(uint32_t))) != cudaSuccess) return e;
     if ((e = cudaMalloc(&m.coop_hist, 3 * rr * 256 * sizeof(uint32_t))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&m.dsum, rr * sizeof(double))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&m.dcnt, rr * sizeof(uint64_t))) != cudaSuccess) return e;
     m.cap_rows_rp = need;
     m.cap_rows = rows;
     m.nblk = nblk;
@@ -513,6 +605,8 @@ void metrics_free(MetricsScratch& m) {
     cudaFree(m.out);
     cudaFree(m.done);
     cudaFree(m.coop_hist);
+    cudaFree(m.dsum);
+    cudaFree(m.dcnt);
     m = MetricsScratch{};
 }
 

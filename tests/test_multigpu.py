@@ -29,14 +29,22 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("name,n_trials,rho,p2p", [("tiny", 1000, None, True), ("tiny", 997, None, True),
-                                                   ("mini", 20_000, None, True), ("mini", 20_001, 0.01, True),
-                                                   ("tiny", 997, None, False), ("mini", 20_001, 0.01, False),
-                                                   ("multilayer", 4001, None, True)])
-def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials, rho, p2p):
+@pytest.mark.parametrize("name,n_trials,rho,p2p,mdist", [("tiny", 1000, None, True, False),
+                                                         ("tiny", 997, None, True, False),
+                                                         ("mini", 20_000, None, True, False),
+                                                         ("mini", 20_001, 0.01, True, False),
+                                                         ("tiny", 997, None, False, False),
+                                                         ("mini", 20_001, 0.01, False, False),
+                                                         ("multilayer", 4001, None, True, False),
+                                                         ("tiny", 997, None, True, True),
+                                                         ("mini", 20_001, 0.01, False, True)])
+def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials, rho, p2p, mdist):
     """p2p: the kernels store the YLT straight into every rank's global buffer
     over NVLink (fused assembly, the default); otherwise ncclAllGather
-    (ARA_NO_P2P=1).  Both must equal the 1-GPU run bit for bit."""
+    (ARA_NO_P2P=1).  Both must equal the 1-GPU run bit for bit.  mdist: the
+    metrics by distributed select (ARA_METRICS_DIST=1: each rank histograms
+    its shard, histograms and tail sums all-reduced) -- same PML bits, TVaR
+    within rounding of the summation order."""
     n = _ngpu()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
@@ -48,6 +56,7 @@ def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials, rho, p2p
     env = dict(os.environ)
     if not p2p:
         env["ARA_NO_P2P"] = "1"
+    env["ARA_METRICS_DIST"] = "1" if mdist else "0"
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     got = np.load(out)
