@@ -186,7 +186,7 @@ def load_peaks():
         return {}
 
 
-KERNEL_NAMES = {14: "ara::trial_kernel_cq (compacted rounds)", 12: "ara::trial_kernel_co (cooperative ring)",
+KERNEL_NAMES = {16: "ara::trial_kernel_cq (compacted rounds, 1-stage ring)", 14: "ara::trial_kernel_cq (compacted rounds)", 12: "ara::trial_kernel_co (cooperative ring)",
                 5: "ara::trial_kernel (register pipeline)", 0: "ara::trial_kernel (register pipeline)",
                 -2: "ara::fold_kernel+trial_fold_kernel"}
 

@@ -1005,7 +1005,8 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     // Fused YLT assembly: one launch group per chunk (no wide layers, no
     // programs, one fold chunk) with a kernel whose epilogue stores to peers.
     bool p2p_ok_kernel = ctx->kernel_variant < 0 || ctx->kernel_variant == 0 || ctx->kernel_variant == 5 ||
-                         ctx->kernel_variant == 12 || ctx->kernel_variant == 14 || ctx->kernel_variant == 15;
+                         ctx->kernel_variant == 12 || ctx->kernel_variant == 14 || ctx->kernel_variant == 15 ||
+                         ctx->kernel_variant == 16;
     bool single_group = (groups.size() == 1 || multiwin) && !groups[0].wide && n_programs == 0 &&
                         (!fold || (n_layers + nlc - 1) / nlc == 1) && world <= (uint32_t)kMaxPeers;
     bool use_p2p = false;
@@ -1223,7 +1224,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 // The other variants stay ARA_KERNEL-selectable for A/B runs.
                 int variant = ctx->kernel_variant;
                 if (variant == 15) variant = 14;   // multi-window only for multi-window runs (above)
-                if (variant < 0 && p.bm) variant = 14;
+                if (variant < 0 && p.bm) variant = 16;   // compacted rounds, 1-stage row ring
                 if (p.bm) {   // rows actually gathered: the occupied fraction of the block
                     const uint32_t blk = g.q0 / spb;
                     used_occupancy = (double)ctx->occ_rows[blk] / ((double)ctx->catalog + 1.0);

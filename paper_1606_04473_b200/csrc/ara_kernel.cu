@@ -884,7 +884,7 @@ struct CoGeo {
     static constexpr int RPI = 32 / LPR;               // rows per copy instruction
     static constexpr int STAGE = 32 * ROWB;            // one row per lane
     static constexpr int NS0 = (BUDGET_KB * 1024) / (WARPS * (STAGE + (int)sizeof(StepMeta)));
-    static constexpr int NS = NS0 > 16 ? 16 : (NS0 < 2 ? 2 : NS0);
+    static constexpr int NS = NS0 > 16 ? 16 : (NS0 < 1 ? 1 : NS0);   // 1: compacted rounds only
     static constexpr int BYTES = WARPS * NS * STAGE + WARPS * NS * (int)sizeof(StepMeta);
     // conflict-free chunk permutation of row r (8 consecutive rows of a
     // quarter-warp phase hit 8 distinct 16-B bank groups)
@@ -1928,11 +1928,13 @@ void* pick_nsec_cq(uint32_t nsec, int* smem) {
     return (void*)trial_kernel_cq<TV, 4, NLB, BUDGET_KB, MINB, 1>;
 }
 
-// two CTAs/SM: a 2-stage row ring (64 KB) plus the id/occupancy rings per CTA
+// two CTAs/SM: a 2-stage row ring (64 KB) plus the id/occupancy rings per CTA;
+// variant 16: a 1-stage row ring (more L1 left for the occupancy bitmap)
 template <typename TV>
 void* pick_cq(uint32_t nsec, int nl, int variant, int* smem) {
-    (void)variant;
-#define ARA_CQ_V(NLB) return pick_nsec_cq<TV, NLB, 64, 2>(nsec, smem);
+#define ARA_CQ_V(NLB)                                                         \
+    if (variant == 16) return pick_nsec_cq<TV, NLB, 40, 2>(nsec, smem);       \
+    return pick_nsec_cq<TV, NLB, 66, 2>(nsec, smem);
     if (nl <= 1) { ARA_CQ_V(1) }
     if (nl <= 2) { ARA_CQ_V(2) }
     ARA_CQ_V(4)
@@ -1942,10 +1944,10 @@ void* pick_cq(uint32_t nsec, int nl, int variant, int* smem) {
 // multi-window compacted rounds: up to 4 disjoint windows of equal width
 template <typename TV>
 void* pick_cqm(uint32_t nsec, int* smem) {
-    if (nsec <= 1) { *smem = CqGeo<TV, 1, 64, 2>::BYTES; return (void*)trial_kernel_cq<TV, 1, 4, 64, 2, 4>; }
-    if (nsec <= 2) { *smem = CqGeo<TV, 2, 64, 2>::BYTES; return (void*)trial_kernel_cq<TV, 2, 4, 64, 2, 4>; }
-    *smem = CqGeo<TV, 4, 64, 2>::BYTES;
-    return (void*)trial_kernel_cq<TV, 4, 4, 64, 2, 4>;
+    if (nsec <= 1) { *smem = CqGeo<TV, 1, 66, 2>::BYTES; return (void*)trial_kernel_cq<TV, 1, 4, 66, 2, 4>; }
+    if (nsec <= 2) { *smem = CqGeo<TV, 2, 66, 2>::BYTES; return (void*)trial_kernel_cq<TV, 2, 4, 66, 2, 4>; }
+    *smem = CqGeo<TV, 4, 66, 2>::BYTES;
+    return (void*)trial_kernel_cq<TV, 4, 4, 66, 2, 4>;
 }
 
 // variant: 0 = register-pipelined, 1 = shared-memory staged (cp.async ring),
@@ -1962,7 +1964,7 @@ void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
     if (variant == 1) return fp32 ? pick_sm<float>(nsec, nl, smem) : pick_sm<double>(nsec, nl, smem);
     if (variant >= 10 && variant <= 13 && nsec <= 4)
         return fp32 ? pick_co<float>(nsec, nl, variant, smem) : pick_co<double>(nsec, nl, variant, smem);
-    if (variant == 14 && nsec <= 4)
+    if ((variant == 14 || variant == 16) && nsec <= 4)
         return fp32 ? pick_cq<float>(nsec, nl, variant, smem) : pick_cq<double>(nsec, nl, variant, smem);
     if (variant == 15 && nsec <= 4) return fp32 ? pick_cqm<float>(nsec, smem) : pick_cqm<double>(nsec, smem);
     return fp32 ? pick<float>(nsec, nl, variant) : pick<double>(nsec, nl, variant);
