@@ -1,0 +1,52 @@
+"""Randomised GPU cross-checks: many small random workloads (catalogue sizes,
+trial lengths incl. empty and long trials, ELT densities from very sparse to
+dense, layer windows aligned / unaligned / towers / disjoint) -- the default
+kernels must match the oracle, and every kernel family must give the same YLT
+bits (they share the lane mapping and per-lane order)."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from parity_util import assert_ylt_close, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+INF = math.inf
+
+
+def _random_case(seed):
+    rng = np.random.default_rng(seed)
+    C = int(rng.choice([50, 700, 5000, 40_000]))
+    n_elts = int(rng.integers(1, 40))
+    rho = float(rng.choice([0.002, 0.01, 0.05, 0.3, 1.0]))
+    T = int(rng.integers(1, 600))
+    w = synth.get_config("tiny").with_(catalog=C, n_elts=n_elts, rho=rho, n_trials=T, nmin=0,
+                                       nmax=int(rng.choice([5, 130, 700])), seed=1000 + seed)
+    layers = []
+    for _ in range(int(rng.integers(1, 5))):
+        b = int(rng.integers(0, n_elts))
+        e = int(rng.integers(b + 1, min(n_elts, b + 17) + 1))
+        layers.append(synth.LayerSpec(b, e, float(rng.uniform(0, 8e4)),
+                                      float(rng.choice([INF, rng.uniform(1e5, 2e6)])),
+                                      float(rng.uniform(0, 1e6)), float(rng.choice([INF, rng.uniform(5e5, 5e6)]))))
+    d = rng.uniform(0, 3e4, n_elts)
+    li = np.where(rng.random(n_elts) < 0.3, INF, rng.uniform(5e4, 2e6, n_elts))
+    return w, tuple(layers), (d, li)
+
+
+@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_random_workloads(cuda, seed, precision):
+    w, layers, terms = _random_case(seed)
+    off, ids = synth.gen_yet(w)
+    elts = synth.gen_elts(w)
+    orc = run_oracle(off, ids, elts, w, layers, fp32=precision == "f32", terms=terms)
+    ylt, lossy, _, _ = run_gpu(off, ids, elts, w, layers, precision=precision, terms=terms)
+    assert_ylt_close(ylt, orc)
+    assert np.array_equal(lossy, orc["lossy"])
+    for v in (16, 12, 5):   # compacted rounds, cooperative ring, register pipeline
+        other, olossy, _, _ = run_gpu(off, ids, elts, w, layers, precision=precision, terms=terms, variant=v)
+        assert np.array_equal(ylt, other) and np.array_equal(lossy, olossy), v
+    fold, flossy, _, _ = run_gpu(off, ids, elts, w, layers, precision=precision, terms=terms, run_mode="fold")
+    assert np.array_equal(ylt, fold) and np.array_equal(lossy, flossy)
