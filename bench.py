@@ -66,6 +66,27 @@ def parse():
 
 
 # ------------------------------------------------------------------ helpers
+def bind_to_gpu_numa(local: int) -> int:
+    """Pin this rank to the CPUs nearest its GPU (NVML's ideal affinity), so the
+    pinned host buffers allocated afterwards are first-touched on the GPU's NUMA
+    node -- the host side of the paper's transfer bottleneck.  Returns
+    the number of CPUs the process may run on afterwards."""
+    try:
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        pr = torch.cuda.get_device_properties(local)
+        bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        pynvml.nvmlDeviceSetCpuAffinity(h)
+    except Exception:
+        pass
+    try:
+        return len(os.sched_getaffinity(0))
+    except OSError:
+        return os.cpu_count() or 1
+
+
 def host_info():
     cpu = "?"
     try:
@@ -299,6 +320,7 @@ def main():
     from paper_1606_04473_b200 import ara
 
     torch.cuda.set_device(local)
+    cpus_bound = bind_to_gpu_numa(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
@@ -536,7 +558,7 @@ def main():
             # passes + tail
             "gpu_launches": int(a.steps * (2 + np.mean(launches) + 10)),
             "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
-            "host": host_info(), "gen_seconds": gen_s,
+            "host": dict(host_info(), cpus_near_gpu=cpus_bound), "gen_seconds": gen_s,
         }
         emit(line)
     if world > 1:
