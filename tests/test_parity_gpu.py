@@ -326,9 +326,10 @@ def test_metrics_ties_extremes(cuda):
 
 
 # ------------------------------------------------------------------ errors
-def test_errors_are_reported_and_context_survives(cuda):
+@pytest.mark.parametrize("rho", [0.3, 0.02])   # 0.02: sparse table, the compacted-rounds kernel validates
+def test_errors_are_reported_and_context_survives(cuda, rho):
     ara = _ara()
-    w = synth.get_config("tiny")
+    w = synth.get_config("tiny").with_(rho=rho)
     off, ids, elts = make_inputs(w)
     eo, ev, ls = elts
     C = w.catalog
