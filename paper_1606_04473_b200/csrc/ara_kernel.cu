@@ -2043,6 +2043,8 @@ cudaError_t launch_trials_folded(const TrialParams& p, int grid_mult_x100, cudaS
     // per-trial folded pass (default), or the scan-based one (ARA_FOLD_KERNEL=1, A/B:
     // measured slower, 5.1 vs 4.0 ms on the paper config -- the scan costs more
     // than the one-gather-per-event pass it replaces)
+    // (a cross-trial register-pipelined pass with occupancy gating, 32 events
+    // per step, measured 5.25 ms -- slower too: more instructions per event)
     static int legacy = -1;
     if (legacy < 0) {
         const char* v = getenv("ARA_FOLD_KERNEL");
