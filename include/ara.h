@@ -223,7 +223,10 @@ ara_status ara_pack_ids(const uint32_t* ids, uint64_t n_ids, uint32_t bits, uint
  *   Y[n_layers][t] = sum_l Y[l][t] (portfolio, layer order)
  *   m[l][t] = #{e : o_e > 0}
  *   ylt   [(n_layers+1)][n_trials_global] f64, host or device, or NULL: the
- *         GLOBAL YLT (after the all-gather when world > 1), portfolio last.
+ *         GLOBAL YLT, portfolio last.  With world > 1 the YLT is assembled
+ *         across ranks (a9) either by the kernels themselves -- each
+ *         trial's entries stored into every rank's global buffer over NVLink
+ *         (CUDA IPC mappings made on the first run) -- or by ncclAllGather.
  *   lossy [n_layers][n_trials_local] u32, host or device, or NULL.
  *   stats nullable.
  * The YLT also stays resident on the device for ara_metrics.
@@ -257,10 +260,13 @@ ara_status ara_run_portfolio(ara_ctx* ctx, uint32_t n_programs, const uint32_t* 
  *   ara_run_portfolio (the YLT rows, in the same order)
  * computed on the device by radix select over the fp64 bit patterns plus a
  * masked tail sum.  Outputs are HOST pointers (k may be NULL).  device_ms
- * (nullable) receives the metrics kernels' event time.  Every rank computes
- * the same values; not collective.
+ * (nullable) receives the metrics kernels' event time.  Every rank obtains
+ * the same values.  COLLECTIVE when world > 1: on large global YLTs (>= 3M
+ * trials) each rank selects over its own shard and the per-pass histograms
+ * and tail sums are all-reduced (the distributed select); NCCL failures are
+ * reported as ARA_ERR_NCCL.
  * Errors: STATE (no run yet), INVALID_ARG (n_rp 0 or > ARA_MAX_RP, NULL),
- * DOMAIN (R outside [1, T]), CUDA. */
+ * DOMAIN (R outside [1, T]), CUDA, NCCL. */
 ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* return_periods,
                        uint64_t* k, double* pml, double* tvar, double* device_ms);
 
