@@ -166,7 +166,7 @@ class ClockSampler:
 
 
 def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str = "direct",
-                      occupancy: float = 1.0) -> int:
+                      occupancy: float = 1.0, packed: bool = False) -> int:
     """DESIGN.md section 6 "Algorithmic bytes": the north star's count, YET
     bytes streamed + 32 B per gathered ELT sector.  Direct mode, per launch
     (layers sharing one row window share a launch): per event 4 B of id, plus
@@ -176,7 +176,9 @@ def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str
     YLT row.  Fold mode: the fold pass reads
     every catalogue row window once and writes 8 B per (event id, layer); the
     trial pass reads 4 B of id + one fold row (8 B x layers, padded to a power
-    of two) per event."""
+    of two) per event.  Packed rows (kernels 17-19): an occupied event's
+    non-zero losses are one 32-B packed slot, so the occupied fraction costs
+    one sector per event instead of the window's sectors."""
     eps = 4 if precision == "f64" else 8
     windows = []
     for L in w.layers:
@@ -196,7 +198,7 @@ def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str
                    + per_trial)
     per_event = 0.0
     for (a, b), _ in windows:
-        per_event += 4 + (32 if occupancy < 1.0 else 0) + occupancy * 32 * (b - a)
+        per_event += 4 + (32 if occupancy < 1.0 else 0) + occupancy * 32 * (1 if packed else b - a)
     return int(n_events * per_event + per_trial)
 
 
@@ -207,7 +209,9 @@ def load_peaks():
         return {}
 
 
-KERNEL_NAMES = {16: "ara::trial_kernel_cq (compacted rounds, 1-stage ring)", 14: "ara::trial_kernel_cq (compacted rounds)", 12: "ara::trial_kernel_co (cooperative ring)",
+KERNEL_NAMES = {17: "ara::trial_kernel_cq (compacted rounds over packed rows)",
+                18: "ara::trial_kernel_cq (packed rows, 2-stage ring)", 19: "ara::trial_kernel_cq (packed rows, 4-stage ring)",
+                16: "ara::trial_kernel_cq (compacted rounds, 1-stage ring)", 14: "ara::trial_kernel_cq (compacted rounds)", 12: "ara::trial_kernel_co (cooperative ring)",
                 5: "ara::trial_kernel (register pipeline)", 0: "ara::trial_kernel (register pipeline)",
                 -2: "ara::fold_kernel+trial_fold_kernel"}
 
@@ -435,7 +439,8 @@ def main():
 
     # roofline of the dominant kernel (the ARA trial kernel) on this rank
     k_ms = float(np.mean(kern_ms))
-    alg = algorithmic_bytes(w, ev_local, count, a.precision, a.mode, occupancy=used.get("occupancy", 1.0))
+    alg = algorithmic_bytes(w, ev_local, count, a.precision, a.mode, occupancy=used.get("occupancy", 1.0),
+                            packed=used.get("variant") in (17, 18, 19))
     peaks = load_peaks()
     peak = peaks.get("hbm_gbs")
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"

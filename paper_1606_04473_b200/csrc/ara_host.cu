@@ -409,7 +409,7 @@ ara_status densify_local(ara_ctx* ctx, uint32_t n_elts, uint64_t nrec, const Spa
     // a table whose non-zero rows are all marked in its bitmaps (a previous
     // densify) is cleared row by row; otherwise the whole allocation is zeroed
     if (ctx->table_clean) CK(launch_clear_rows(ctx->d_table, ctx->geo, ctx->catalog, ctx->stream));
-    else CK(cudaMemsetAsync(ctx->d_table, 0, ctx->table_bytes, ctx->stream));
+    else CK(cudaMemsetAsync(ctx->d_table, 0, ctx->geo.pk_off, ctx->stream));   // packed slots: written before read
     ctx->table_clean = false;
     CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(uint32_t), ctx->stream));
     CK(launch_densify(sp.off, sp.ev, sp.ls, n_elts, nrec, ctx->catalog, ctx->d_table, ctx->geo, fp32, ctx->d_err,
@@ -426,6 +426,7 @@ ara_status densify_local(ara_ctx* ctx, uint32_t n_elts, uint64_t nrec, const Spa
     if (small) std::memcpy(ctx->occ_rows.data(), h_occ, nb * sizeof(uint32_t));
     else CK(cudaMemcpy(ctx->occ_rows.data(), d_occ, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost));
     ctx->table_clean = true;   // every stored element's row is marked (even for rejected ELTs)
+    if (!ctx->no_skip) CK(launch_pack_rows(ctx->d_table, ctx->geo, ctx->catalog, fp32, ctx->stream));
     return device_errors(ctx, (uint32_t)(ctx->h_small[0] & 0xffffffffu));
 }
 
@@ -1006,7 +1007,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     // programs, one fold chunk) with a kernel whose epilogue stores to peers.
     bool p2p_ok_kernel = ctx->kernel_variant < 0 || ctx->kernel_variant == 0 || ctx->kernel_variant == 5 ||
                          ctx->kernel_variant == 12 || ctx->kernel_variant == 14 || ctx->kernel_variant == 15 ||
-                         ctx->kernel_variant == 16;
+                         (ctx->kernel_variant >= 16 && ctx->kernel_variant <= 19);
     bool single_group = (groups.size() == 1 || multiwin) && !groups[0].wide && n_programs == 0 &&
                         (!fold || (n_layers + nlc - 1) / nlc == 1) && world <= (uint32_t)kMaxPeers;
     bool use_p2p = false;
@@ -1060,6 +1061,12 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                    ? reinterpret_cast<const uint32_t*>(static_cast<const char*>(ctx->d_table) + geo.bm_off) +
                          (uint64_t)(g.q0 / spb) * geo.bm_words
                    : nullptr;
+        // packed rows of the block (built by load_elts for sparse blocks)
+        p.pk = p.bm ? static_cast<const void*>(static_cast<const char*>(ctx->d_table) + geo.pk_off +
+                                               (size_t)(g.q0 / spb) * ((size_t)ctx->catalog + 1) * kPackBytes)
+                    : nullptr;
+        p.pk_col0 = (g.q0 % spb) * eps;
+        p.pk_wmask = g.nsec * eps >= 32 ? 0xffffffffu : (1u << (g.nsec * eps)) - 1u;
         for (uint32_t q = 0; q < g.nl; ++q) {
             const LayerI& L = layers[g.l0 + q];
             for (uint32_t w = 0; w < (uint32_t)kMaxWin; ++w) {
@@ -1224,7 +1231,8 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 // The other variants stay ARA_KERNEL-selectable for A/B runs.
                 int variant = ctx->kernel_variant;
                 if (variant == 15) variant = 14;   // multi-window only for multi-window runs (above)
-                if (variant < 0 && p.bm) variant = 16;   // compacted rounds, 1-stage row ring
+                if (variant < 0 && p.bm) variant = 17;   // compacted rounds over the packed rows
+                if (variant >= 17 && variant <= 19 && !p.pk) variant = 16;
                 if (p.bm) {   // rows actually gathered: the occupied fraction of the block
                     const uint32_t blk = g.q0 / spb;
                     used_occupancy = (double)ctx->occ_rows[blk] / ((double)ctx->catalog + 1.0);

@@ -31,6 +31,7 @@ constexpr int kMaxFoldL = 8;         // layers per folded trial launch (fold mod
 constexpr int kMaxWin = kMaxSec * kSectorBytes / 4;   // 64 columns (fp32) per window
 constexpr int kThreads = 256;        // 8 warps per CTA
 constexpr int kTablePadBytes = kMaxSec * kSectorBytes;  // over-read slack after the last row
+constexpr int kPackBytes = 32;       // packed row: u32 mask, u32 event id, 24 B of values
 constexpr int kMaxPeers = 8;         // ranks whose global YLT a kernel epilogue writes over NVLink
 
 // Direct-access table geometry: ELT columns are cut
@@ -48,7 +49,8 @@ struct TableGeo {
     uint64_t bm_words = 0;       // row-occupancy bitmap words per block (ceil((C+1)/32), padded)
     size_t bm_off = 0;           // byte offset of the bitmaps in the allocation
     size_t occ_off = 0;          // byte offset of the per-block occupied-row counters (u32)
-    size_t bytes = 0;            // allocation incl. pad and bitmaps
+    size_t pk_off = 0;           // byte offset of the packed-row slots (kPackBytes per event per block)
+    size_t bytes = 0;            // allocation incl. pad, bitmaps and packed slots
 };
 inline TableGeo table_geometry(uint32_t n_elts, uint32_t catalog, int fp32) {
     TableGeo g;
@@ -66,7 +68,11 @@ inline TableGeo table_geometry(uint32_t n_elts, uint32_t catalog, int fp32) {
     g.bm_words = (((uint64_t)catalog + 1 + 31) / 32 + 63) / 64 * 64;
     g.bm_off = ((size_t)g.n_blocks * g.block_elems * g.esz + kTablePadBytes + 255) / 256 * 256;
     g.occ_off = g.bm_off + (size_t)g.n_blocks * g.bm_words * 4;
-    g.bytes = g.occ_off + ((size_t)g.n_blocks * 4 + 255) / 256 * 256;
+    // Packed rows of the sparse blocks (one 32-B sector per event, written for
+    // the occupied rows only, never zero-filled): the row's non-zero mask, its
+    // event id and its first non-zero values in column order (PackedRow below).
+    g.pk_off = g.occ_off + ((size_t)g.n_blocks * 4 + 255) / 256 * 256;
+    g.bytes = g.pk_off + (size_t)g.n_blocks * ((size_t)catalog + 1) * kPackBytes;
     return g;
 }
 
@@ -115,6 +121,12 @@ struct TrialParams {
     // offset of layer u's window (event 0); bm then points at the combined
     // 4-bit-per-event occupancy map of the windows' column blocks
     uint64_t win0[kMaxLB];
+    // packed rows of the window's (sparse) column block, or null: slot e holds
+    // row e's non-zero mask over the block's columns, e, and its first
+    // 24 / esz non-zero values in column order; the window is block columns
+    // pk_col0 .. (pk_wmask's bits), i.e. window element j = block column pk_col0 + j
+    const void* pk;
+    uint32_t pk_col0, pk_wmask;
     uint64_t peer_ld;           // = T_global
     uint64_t peer_t0;           // global index of local trial 0 (this rank's first trial)
 };
@@ -130,6 +142,8 @@ cudaError_t launch_occ4(const uint32_t* bitmaps, uint64_t bm_words, const uint32
 // OR of up to 8 column blocks' occupancy bitmaps
 cudaError_t launch_bm_union(const uint32_t* bitmaps, uint64_t bm_words, const uint32_t* blk, uint32_t nb,
                             uint32_t* out, cudaStream_t s);
+// packed rows (TrialParams::pk) of every sparse column block (<= half its rows occupied)
+cudaError_t launch_pack_rows(void* d_table, const TableGeo& geo, uint32_t catalog, int fp32, cudaStream_t s);
 // zero exactly the rows the occupancy bitmaps mark, then the bitmaps and counters
 cudaError_t launch_clear_rows(void* d_table, const TableGeo& geo, uint32_t catalog, cudaStream_t s);
 cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int grid, int variant, cudaStream_t s);

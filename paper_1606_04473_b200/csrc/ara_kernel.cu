@@ -253,6 +253,63 @@ __device__ __forceinline__ void event_compute_sparse(const TrialParams& p, const
     }
 }
 
+// event_compute over a staged packed row (TrialParams::pk): the slot's mask
+// names the block's non-zero columns, so the window's non-zeros are visited in
+// ascending column order -- the order (and the values) event_compute_sparse
+// visits, so l_e is bit-identical.  The v-th non-zero of the row sits in the
+// slot when v < 24 / esz, else it is read from the dense table (rows with more
+// non-zeros than the slot holds: ~1e-4 of the occupied rows at rho = 0.01).
+template <typename TV, int NLB>
+__device__ __forceinline__ void event_compute_packed(const TrialParams& p, const double2 (*s_term)[kMaxWin],
+                                                     uint32_t src, uint32_t swz, double (&G)[NLB],
+                                                     uint32_t (&m)[NLB]) {
+    constexpr int CAP = (kPackBytes - 8) / (int)sizeof(TV);
+    constexpr bool SM = true;   // lanes look up different columns: shared memory, not the constant bank
+    uint32_t mask, e;
+    asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(mask), "=r"(e) : "r"(src + (swz << 4)) : "memory");
+    const uint32_t nz = (mask >> p.pk_col0) & p.pk_wmask;
+    // one pass over the window's non-zeros (ascending column), every layer of
+    // the launch accumulating its own l_e in that order
+    double le[NLB];
+#pragma unroll
+    for (int l = 0; l < NLB; ++l) le[l] = 0.0;
+    uint32_t mm = nz;
+    while (mm) {
+        const uint32_t j = (uint32_t)(__ffs(mm) - 1);
+        mm &= mm - 1u;
+        const uint32_t b = j + p.pk_col0;
+        const uint32_t v = __popc(mask & ((1u << b) - 1u));   // rank of column b among the row's non-zeros
+        double x;
+        if (v < (uint32_t)CAP) {
+            const uint32_t o = 8u + v * (uint32_t)sizeof(TV);
+            const uint32_t a = src + (((o >> 4) ^ swz) << 4) + (o & 15u);
+            if (sizeof(TV) == 8) {
+                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a) : "memory");
+            } else {
+                float xf;
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xf) : "r"(a) : "memory");
+                x = (double)xf;
+            }
+        } else {
+            x = (double)__ldg(static_cast<const TV*>(p.table) + p.sec_off[0] + (uint64_t)e * p.row_stride + j);
+        }
+#pragma unroll
+        for (int l = 0; l < NLB; ++l) {
+            if (l == 0 || l < (int)p.n_layers) {   // a launch has >= 1 layer
+                const double2 tc = SM ? lds_term(&s_term[l][j]) : p.term[l][j];
+                le[l] = __dadd_rn(le[l], terms(x, tc.x, tc.y));
+            }
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < NLB; ++l) {
+        if (l >= (int)p.n_layers) break;
+        const double o = terms(le[l], p.lw[l].occ_r, p.lw[l].occ_l);
+        G[l] = __dadd_rn(G[l], o);
+        m[l] += (o > 0.0) ? 1u : 0u;
+    }
+}
+
 // The same for a multi-window launch: the staged row belongs to the window of
 // layer u (one layer per window); only that layer's accumulators change.
 template <typename TV, int NSEC, int NLB>
@@ -1144,8 +1201,13 @@ __device__ __forceinline__ void cp_wait_upto(uint32_t n) {
     }
 }
 
-template <typename TV, int NSEC, int NLB, int BUDGET_KB, int MINB, int NWIN>
+template <typename TV, int NSEC, int NLB, int BUDGET_KB, int MINB, int NWIN, bool PK = false, bool OL = false>
 __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_constant__ TrialParams p) {
+    // PK: the rounds gather packed rows (one 32-B slot per event, p.pk; NSEC == 1)
+    // OL: a step's occupancy words are plain L1-cached loads into registers,
+    //     issued one step ahead, instead of cp.async copies into the ring
+    static_assert(!PK || (NSEC == 1 && NWIN == 1), "packed rounds: one sector per event, one window");
+    static_assert(!OL || NWIN == 1, "register occupancy words: one window");
     // NWIN == 1: one row window (layers 0..n_layers-1 share it: towers);
     // NWIN > 1: p.n_layers disjoint windows, one layer each, scanned together
     // (one id stream, one combined 4-bit occupancy word per event, one FIFO
@@ -1157,7 +1219,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
     constexpr int CH = Geo::CH, LPR = Geo::LPR, RPI = Geo::RPI;
     constexpr int QD = RG::QD, DW = RG::DW, IR = RG::IR, WR = RG::WR, MR = RG::MR, IDB = RG::IDB;
     constexpr int QC = NWIN > 1 ? 2 : 4;   // per-lane FIFO of occupied events (per window)
-    constexpr bool SM = TermsInSmem<TV, NSEC, NLB>::value;
+    constexpr bool SM = PK || TermsInSmem<TV, NSEC, NLB>::value;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double2 s_term[SM ? NLB : 1][kMaxWin];
     const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
@@ -1178,9 +1240,10 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
     const uint32_t* bm = p.bm;
     uint32_t err = 0;
     const uint32_t c_chunk = lane % LPR, c_row = lane / LPR;
-    const uint32_t row_bytes = (uint32_t)(p.row_stride * sizeof(TV));
-    const char* c_src = reinterpret_cast<const char*>(p.table) +
-                        (p.sec_off[c_chunk >> 1] + (c_chunk & 1) * (16 / sizeof(TV))) * sizeof(TV);
+    const uint32_t row_bytes = PK ? (uint32_t)kPackBytes : (uint32_t)(p.row_stride * sizeof(TV));
+    const char* c_src = PK ? static_cast<const char*>(p.pk) + c_chunk * 16u
+                           : reinterpret_cast<const char*>(p.table) +
+                                 (p.sec_off[c_chunk >> 1] + (c_chunk & 1) * (16 / sizeof(TV))) * sizeof(TV);
     uint32_t c_dst[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) c_dst[h] = c_row * Geo::ROWB + ((c_chunk ^ Geo::swz((uint32_t)h * RPI + c_row)) << 4);
@@ -1234,7 +1297,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
                     cp_async16(dst + 16u * c, reinterpret_cast<const void*>(nb ? cs : al), nb);
                 }
             }
-            md = CqStep{it_t, it_n, it_k0, (uint32_t)(ab - al) / 4u, 0u};
+            md = CqStep{it_t, it_n, it_k0, (uint32_t)(ab - al) / 4u, gseq};   // pad: the ids' commit group
             it_k0 += 128u;
             if (it_k0 >= it_n) {
                 it_t += nw;
@@ -1258,19 +1321,36 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         }
     };
 
+    // OL: step x's occupancy words into registers (its ids have landed)
+    auto load_occupancy = [&](uint32_t x, uint32_t (&o)[4]) {
+        const uint32_t sh = smeta[x % MR].sh;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint32_t e = lds_u32(idr + (x % IR) * IDB + (sh + 32u * j + lane) * 4u);
+            e = e <= p.catalog ? e : 0u;   // not validated yet
+            o[j] = bm ? __ldg(bm + (e >> 5)) : 0u;
+        }
+    };
+
     // prologue: ids of steps 0..QD-1 (one group), then occupancy of steps 0..DW-1
 #pragma unroll 1
     for (uint32_t x = 0; x < (uint32_t)QD; ++x) fetch_ids(x);
     wait_group(commit());
     __syncwarp();
     uint32_t g_occ = 0;   // commit group of the occupancy words of the next step to scan
+    uint32_t onx[4] = {0u, 0u, 0u, 0u};   // OL: occupancy words of the next step to scan
+    if (OL) {
+        load_occupancy(0, onx);
+    } else {
 #pragma unroll 1
-    for (uint32_t x = 0; x < (uint32_t)DW; ++x) {
-        fetch_occupancy(x);
-        g_occ = commit();
+        for (uint32_t x = 0; x < (uint32_t)DW; ++x) {
+            fetch_occupancy(x);
+            g_occ = commit();
+        }
     }
 
-    // ---- per-lane FIFOs of occupied events, one per window (entries at and beyond fc are 0)
+    // ---- per-lane FIFOs of occupied events, one per window (NWIN == 1:
+    // right-aligned; NWIN > 1: left-aligned, entries at and beyond fc are 0)
     uint32_t f[NWIN][QC], fc[NWIN];
 #pragma unroll
     for (int u = 0; u < NWIN; ++u) {
@@ -1294,7 +1374,8 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         wait_group(g);
         __syncwarp();   // other lanes' copies of my row are complete and visible
         const StepMeta rm = rmeta[slot];
-        if (NWIN == 1) event_compute_sparse<TV, NSEC, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m);
+        if (PK) event_compute_packed<TV, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m);
+        else if (NWIN == 1) event_compute_sparse<TV, NSEC, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m);
         else event_compute_sparse_win<TV, NSEC, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m, rm.k0);
         __syncwarp();   // every lane's reads of the slot precede the copies refilling it
         ++head;
@@ -1323,10 +1404,15 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
 #pragma unroll
         for (int w = 0; w < NWIN; ++w) {
             if ((uint32_t)w != u) continue;
-            ce = f[w][0];
+            if (NWIN == 1) {   // right-aligned FIFO: the head is f[QC - fc]
 #pragma unroll
-            for (int i = 0; i + 1 < QC; ++i) f[w][i] = f[w][i + 1];
-            f[w][QC - 1] = 0u;
+                for (int i = 0; i < QC; ++i) ce = (fc[0] == (uint32_t)(QC - i)) ? f[0][i] : ce;
+            } else {
+                ce = f[w][0];
+#pragma unroll
+                for (int i = 0; i + 1 < QC; ++i) f[w][i] = f[w][i + 1];
+                f[w][QC - 1] = 0u;
+            }
             fc[w] -= fc[w] ? 1u : 0u;
         }
         const char* src = c_src;
@@ -1352,16 +1438,30 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
     // body small enough for the instruction cache.
 #pragma unroll 1
     for (uint32_t sc = 0;; ++sc) {
-        // step sc's occupancy words (and, older, its ids) have landed
-        wait_group(g_occ);
-        __syncwarp();
+        uint32_t ocur[4];
+        if (OL) {
+            // ids of step sc+1 (and, older, sc's) have landed; its occupancy
+            // loads are issued now and consumed by the next step
+            wait_group(smeta[(sc + 1) % MR].pad);
+            __syncwarp();
+#pragma unroll
+            for (int j = 0; j < 4; ++j) ocur[j] = onx[j];
+        } else {
+            // step sc's occupancy words (and, older, its ids) have landed
+            wait_group(g_occ);
+            __syncwarp();
+        }
         const CqStep md = smeta[sc % MR];
         if (md.t == ~0ull) break;
         // refill first: occupancy of step sc+DW (its ids landed: QD >= 2 DW + 1),
         // then ids of step sc+QD; separate groups, so the next scan waits for
         // the occupancy words only
-        fetch_occupancy(sc + DW);
-        g_occ = commit();
+        if (OL) {
+            load_occupancy(sc + 1, onx);
+        } else {
+            fetch_occupancy(sc + DW);
+            g_occ = commit();
+        }
         fetch_ids(sc + QD);
         commit();
         const bool trial_end = md.k0 + 128u >= md.n;
@@ -1372,16 +1472,22 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
 #pragma unroll 1
         for (uint32_t j = 0; j < 4u; ++j) {
             uint32_t e = lds_u32(id_base + 128u * j);
-            const uint32_t w = lds_u32(oc_base + 128u * j);
+            const uint32_t w = OL ? (j == 0u ? ocur[0] : j == 1u ? ocur[1] : j == 2u ? ocur[2] : ocur[3])
+                                  : lds_u32(oc_base + 128u * j);
             const bool live = 32u * j + lane < n_here;
             const bool bad = live && e - 1u >= p.catalog;            // id 0 or > C (A14)
             err |= bad ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
             if (NWIN == 1) {
                 e = (live && !bad && (!bm || ((w >> (e & 31u)) & 1u))) ? e : 0u;
-                // append (entries at and beyond fc are 0, so f[fc] is free); branch-free
+                // append: the FIFO is right-aligned (its fc entries are
+                // f[QC - fc] .. f[QC - 1], oldest first), so an append shifts
+                // it left by one -- predicated moves, no index compares
                 const bool add = e != 0u;
+                if (add) {
 #pragma unroll
-                for (int i = 0; i < QC; ++i) f[0][i] = (add && fc[0] == (uint32_t)i) ? e : f[0][i];
+                    for (int i = 0; i + 1 < QC; ++i) f[0][i] = f[0][i + 1];
+                    f[0][QC - 1] = e;
+                }
                 fc[0] += add ? 1u : 0u;
             } else {
                 const uint32_t bits = (live && !bad) ? (bm ? (w >> ((e & 7u) * 4u)) & 15u : 15u) : 0u;
@@ -1928,11 +2034,22 @@ void* pick_nsec_cq(uint32_t nsec, int* smem) {
     return (void*)trial_kernel_cq<TV, 4, NLB, BUDGET_KB, MINB, 1>;
 }
 
+// packed rounds (17): one 32-B slot per event; the row ring (BUDGET_KB) holds
+// NS 1-KB stages per warp
+template <typename TV, int NLB, int B, bool OL>
+void* pick_pk(int* smem) {
+    *smem = CqGeo<TV, 1, B, 2>::BYTES;
+    return (void*)trial_kernel_cq<TV, 1, NLB, B, 2, 1, true, OL>;
+}
+
 // two CTAs/SM: a 2-stage row ring (64 KB) plus the id/occupancy rings per CTA;
 // variant 16: a 1-stage row ring (more L1 left for the occupancy bitmap)
 template <typename TV>
 void* pick_cq(uint32_t nsec, int nl, int variant, int* smem) {
 #define ARA_CQ_V(NLB)                                                         \
+    if (variant == 17) return pick_pk<TV, NLB, 10, false>(smem);              \
+    if (variant == 18) return pick_pk<TV, NLB, 10, true>(smem);               \
+    if (variant == 19) return pick_pk<TV, NLB, 40, false>(smem);              \
     if (variant == 16) return pick_nsec_cq<TV, NLB, 40, 2>(nsec, smem);       \
     return pick_nsec_cq<TV, NLB, 66, 2>(nsec, smem);
     if (nl <= 1) { ARA_CQ_V(1) }
@@ -1955,7 +2072,10 @@ void* pick_cqm(uint32_t nsec, int* smem) {
 // 8 = TMA gather4 ring (needs p.tmap; windows of <= 4 sectors in one block),
 // 10-13 = cooperative cp.async ring (whole rows per instruction) at 1/2/3 CTAs/SM,
 // 14 = compacted rounds over the cooperative ring (skips zero rows' arithmetic),
-// 15 = the same over up to 4 disjoint layer windows in one launch (host-selected).
+// 15 = the same over up to 4 disjoint layer windows in one launch (host-selected),
+// 16 = 14 with a 1-stage row ring, 17 = compacted rounds over packed rows (p.pk),
+// 18 = 17 with the occupancy words by L1-cached loads into registers,
+// 19 = 17 with a 4-stage row ring.
 void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
     *smem = 0;
     if (variant == 8 && nsec <= 4)
@@ -1964,7 +2084,7 @@ void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
     if (variant == 1) return fp32 ? pick_sm<float>(nsec, nl, smem) : pick_sm<double>(nsec, nl, smem);
     if (variant >= 10 && variant <= 13 && nsec <= 4)
         return fp32 ? pick_co<float>(nsec, nl, variant, smem) : pick_co<double>(nsec, nl, variant, smem);
-    if ((variant == 14 || variant == 16) && nsec <= 4)
+    if (((variant >= 16 && variant <= 19) || variant == 14) && nsec <= 4)
         return fp32 ? pick_cq<float>(nsec, nl, variant, smem) : pick_cq<double>(nsec, nl, variant, smem);
     if (variant == 15 && nsec <= 4) return fp32 ? pick_cqm<float>(nsec, smem) : pick_cqm<double>(nsec, smem);
     return fp32 ? pick<float>(nsec, nl, variant) : pick<double>(nsec, nl, variant);
@@ -1973,9 +2093,9 @@ void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
 }  // namespace
 
 int trial_kernel_grid(int fp32, uint32_t max_nsec, int n_layers, int variant) {
-    static int cache[16][2][kMaxSec + 2][kMaxLB + 1] = {};
+    static int cache[32][2][kMaxSec + 2][kMaxLB + 1] = {};
     const uint32_t ns = max_nsec > (uint32_t)kMaxSec ? kMaxSec + 1 : max_nsec;
-    int& c = cache[variant & 15][fp32 ? 1 : 0][ns][n_layers];
+    int& c = cache[variant & 31][fp32 ? 1 : 0][ns][n_layers];
     if (c) return c;
     int dev = 0, nsm = 148, per_sm = 1, smem = 0;
     cudaGetDevice(&dev);

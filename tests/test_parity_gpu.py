@@ -446,3 +446,36 @@ def test_portfolio_programs_and_explicit_elt_lists(cuda, run_mode):
     for r in range(L + P + 1):
         kk, p_o, _ = oracle.metrics(ylt[r], (2, 10, 100))
         assert np.array_equal(p_o, pml[r]) and np.array_equal(kk, k)
+
+
+@pytest.mark.parametrize("variant", (-1, 14, 16, 17, 18, 19))
+@pytest.mark.parametrize("precision", ("f64", "f32"))
+def test_packed_rows_overflow_and_offset_windows(cuda, variant, precision):
+    """Packed rows (variant 17-19): a sparse block whose first 400 rows are
+    non-zero in EVERY ELT, so those rows hold more non-zeros than a packed slot
+    (3 fp64 / 6 fp32 values) and the rest are read from the dense table; layers
+    whose window starts inside the block (the slot mask is shifted), a window
+    over the block's tail, and one spanning two fp64 blocks (no bitmap).  Must
+    match the oracle and be bit-identical to the unskipped run."""
+    rng = np.random.default_rng(17)
+    w = synth.get_config("tiny").with_(catalog=20000, n_elts=20, n_trials=600, nmin=1, nmax=250)
+    off, ids = synth.gen_yet(w)
+    eo, ev, ls = [0], [], []
+    for j in range(w.n_elts):
+        tail = rng.choice(np.arange(401, w.catalog + 1), 200, replace=False)
+        e = np.unique(np.concatenate([np.arange(1, 401), tail])).astype(np.uint32)
+        ev.append(e)
+        ls.append(np.floor(rng.lognormal(np.log(5e4), 1.5, len(e))))
+        eo.append(eo[-1] + len(e))
+    elts = (np.array(eo, dtype=np.uint64), np.concatenate(ev), np.concatenate(ls))
+    d = rng.uniform(0, 2e4, w.n_elts)
+    li = np.where(rng.random(w.n_elts) < 0.3, INF, rng.uniform(1e5, 2e6, w.n_elts))
+    layers = (synth.LayerSpec(0, 16, 2.5e4, 7.5e5, 1.2e6, 8e6), synth.LayerSpec(4, 12, 1e4, 4e5, 6.5e5, 4e6),
+              synth.LayerSpec(16, 20, 0.0, INF, 1e5, INF), synth.LayerSpec(0, 20, 2.5e5, 5e5, 4e5, 3.5e6))
+    orc = run_oracle(off, ids, elts, w, layers, fp32=precision == "f32", terms=(d, li))
+    ylt, lossy, st, _ = run_gpu(off, ids, elts, w, layers, precision=precision, terms=(d, li), variant=variant)
+    assert_ylt_close(ylt, orc)
+    assert np.array_equal(lossy, orc["lossy"])
+    ylt2, lossy2, _, _ = run_gpu(off, ids, elts, w, layers, precision=precision, terms=(d, li), variant=variant,
+                                 env={"ARA_NO_SKIP": 1})
+    assert np.array_equal(ylt, ylt2) and np.array_equal(lossy, lossy2)
