@@ -18,7 +18,8 @@ from typing import Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libara.so")
+# ARA_LIB_PATH: another build of the same library (A/B timing of two builds on one box)
+LIB_PATH = os.environ.get("ARA_LIB_PATH") or os.path.join(_HERE, "libara.so")
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()); "
                       "there is no CPU fallback")

@@ -1469,27 +1469,62 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         const uint32_t id_base = idr + (sc % IR) * IDB + (md.sh + lane) * 4u;
         const uint32_t oc_base = ocr + ((sc % WR) * 128u + lane) * 4u;
         const uint32_t n_here = md.n - md.k0;   // events of the trial from this step on
+        if constexpr (NWIN == 1) {
+            // (1) the step's 4 sub-steps tested at once (independent loads and
+            // compares: instruction-level parallelism); ev[j] = event
+            // k0 + 32 j + lane if its row is occupied, else 0
+            uint32_t ev[4], na = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const uint32_t e = lds_u32(id_base + 128u * j);
+                const uint32_t w = OL ? ocur[j] : lds_u32(oc_base + 128u * j);
+                const bool live = 32u * j + lane < n_here;
+                const bool bad = live && e - 1u >= p.catalog;            // id 0 or > C (A14)
+                err |= bad ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
+                ev[j] = (live && !bad && (!bm || ((w >> (e & 31u)) & 1u))) ? e : 0u;
+                na += ev[j] ? 1u : 0u;
+            }
+            // (2) rounds are emitted until every lane's FIFO has room for the
+            // step's appends, (3) the appends (right-aligned FIFO: an append
+            // shifts it left by one -- predicated moves), (4) at the end of
+            // the trial, rounds until every FIFO is empty, the last one
+            // finalising the trial.  The FIFO keeps each lane's events in
+            // increasing k, so the emission points do not change any sum.
+            bool appended = false;
+#pragma unroll 1
+            for (;;) {
+                uint32_t last = 0;
+                if (!appended) {
+                    if (!__any_sync(0xffffffffu, fc[0] + na > (uint32_t)QC)) {
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            if (ev[j]) {
+#pragma unroll
+                                for (int i = 0; i + 1 < QC; ++i) f[0][i] = f[0][i + 1];
+                                f[0][QC - 1] = ev[j];
+                            }
+                        }
+                        fc[0] += na;
+                        appended = true;
+                        if (!trial_end) break;
+                        continue;
+                    }
+                } else {
+                    last = __any_sync(0xffffffffu, fc[0] > 1u) ? 0u : 1u;
+                }
+                if (tail - head == (uint32_t)NS) consume();
+                emit(md.t, last, 0u);
+                if (last) break;
+            }
+        } else {
 #pragma unroll 1
         for (uint32_t j = 0; j < 4u; ++j) {
             uint32_t e = lds_u32(id_base + 128u * j);
-            const uint32_t w = OL ? (j == 0u ? ocur[0] : j == 1u ? ocur[1] : j == 2u ? ocur[2] : ocur[3])
-                                  : lds_u32(oc_base + 128u * j);
+            const uint32_t w = lds_u32(oc_base + 128u * j);
             const bool live = 32u * j + lane < n_here;
             const bool bad = live && e - 1u >= p.catalog;            // id 0 or > C (A14)
             err |= bad ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
-            if (NWIN == 1) {
-                e = (live && !bad && (!bm || ((w >> (e & 31u)) & 1u))) ? e : 0u;
-                // append: the FIFO is right-aligned (its fc entries are
-                // f[QC - fc] .. f[QC - 1], oldest first), so an append shifts
-                // it left by one -- predicated moves, no index compares
-                const bool add = e != 0u;
-                if (add) {
-#pragma unroll
-                    for (int i = 0; i + 1 < QC; ++i) f[0][i] = f[0][i + 1];
-                    f[0][QC - 1] = e;
-                }
-                fc[0] += add ? 1u : 0u;
-            } else {
+            {
                 const uint32_t bits = (live && !bad) ? (bm ? (w >> ((e & 7u) * 4u)) & 15u : 15u) : 0u;
 #pragma unroll
                 for (int u = 0; u < NWIN; ++u) {
@@ -1507,26 +1542,20 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
             for (int u = 0; u < NWIN; ++u) fullmask |= __any_sync(0xffffffffu, fc[u] == (uint32_t)QC) ? 1u << u : 0u;
             if (fullmask || flush) {
                 for (;;) {
-                    uint32_t u = 0, last = 0;
-                    if (NWIN == 1) {
-                        if (!fullmask && !flush) break;
-                        last = (flush && !__any_sync(0xffffffffu, fc[0] > 1u)) ? 1u : 0u;
-                    } else {
-                        // the first window with a full FIFO (or, flushing, any entry)
-                        uint32_t pend = 0;
+                    // the first window with a full FIFO (or, flushing, any entry)
+                    uint32_t pend = 0;
 #pragma unroll
-                        for (int w = 0; w < NWIN; ++w)
-                            pend |= __any_sync(0xffffffffu, flush ? fc[w] > 0u : fc[w] == (uint32_t)QC) ? 1u << w : 0u;
-                        if (!pend && !flush) break;
-                        u = pend ? (uint32_t)(__ffs(pend) - 1) : (uint32_t)NWIN;   // NWIN: the marker
-                        last = pend ? 0u : 1u;
-                    }
+                    for (int w = 0; w < NWIN; ++w)
+                        pend |= __any_sync(0xffffffffu, flush ? fc[w] > 0u : fc[w] == (uint32_t)QC) ? 1u << w : 0u;
+                    if (!pend && !flush) break;
+                    const uint32_t u = pend ? (uint32_t)(__ffs(pend) - 1) : (uint32_t)NWIN;   // NWIN: the marker
+                    const uint32_t last = pend ? 0u : 1u;
                     if (tail - head == (uint32_t)NS) consume();
                     emit(md.t, last, u);
-                    if (NWIN == 1 ? (!flush || last) : last) break;
-                    fullmask = 0;   // (multi-window) re-evaluated from the FIFOs above
+                    if (last) break;
                 }
             }
+        }
         }
         __syncwarp();   // reads of this step's slots precede their refills
     }
