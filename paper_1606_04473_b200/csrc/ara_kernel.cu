@@ -268,6 +268,9 @@ __device__ __forceinline__ void event_compute_packed(const TrialParams& p, const
     uint32_t mask, e;
     asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(mask), "=r"(e) : "r"(src + (swz << 4)) : "memory");
     const uint32_t nz = (mask >> p.pk_col0) & p.pk_wmask;
+    // the slot holds all of the row's non-zeros (the common case): no
+    // dense-table reads in the loop below
+    const bool full = __popc(mask) <= CAP;
     // one pass over the window's non-zeros (ascending column), every layer of
     // the launch accumulating its own l_e in that order
     double le[NLB];
@@ -280,7 +283,7 @@ __device__ __forceinline__ void event_compute_packed(const TrialParams& p, const
         const uint32_t b = j + p.pk_col0;
         const uint32_t v = __popc(mask & ((1u << b) - 1u));   // rank of column b among the row's non-zeros
         double x;
-        if (v < (uint32_t)CAP) {
+        if (full || v < (uint32_t)CAP) {
             const uint32_t o = 8u + v * (uint32_t)sizeof(TV);
             const uint32_t a = src + (((o >> 4) ^ swz) << 4) + (o & 15u);
             if (sizeof(TV) == 8) {
@@ -1310,14 +1313,19 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         }
         if (lane == 0) smeta[x % MR] = md;
     };
-    // copy the occupancy words of step x's events (its ids have landed)
+    // copy the occupancy words of step x's events (its ids have landed); the
+    // lane's 4 ids stay in nid for the scan of step x (NWIN == 1: the words
+    // land lane-major, [lane][j], so the scan reads its 4 with one load)
+    uint32_t nid[4] = {0u, 0u, 0u, 0u};
     auto fetch_occupancy = [&](uint32_t x) {
         const uint32_t sh = smeta[x % MR].sh;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             uint32_t e = lds_u32(idr + (x % IR) * IDB + (sh + 32u * j + lane) * 4u);
+            nid[j] = e;
             e = e <= p.catalog ? e : 0u;   // not validated yet
-            cp_async4(ocr + ((x % WR) * 128u + 32u * j + lane) * 4u, bm + (e >> (NWIN > 1 ? 3 : 5)), bm ? 4u : 0u);
+            const uint32_t slot = NWIN == 1 ? lane * 4u + (uint32_t)j : 32u * j + lane;
+            cp_async4(ocr + ((x % WR) * 128u + slot) * 4u, bm + (e >> (NWIN > 1 ? 3 : 5)), bm ? 4u : 0u);
         }
     };
 
@@ -1327,6 +1335,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             uint32_t e = lds_u32(idr + (x % IR) * IDB + (sh + 32u * j + lane) * 4u);
+            nid[j] = e;
             e = e <= p.catalog ? e : 0u;   // not validated yet
             o[j] = bm ? __ldg(bm + (e >> 5)) : 0u;
         }
@@ -1453,6 +1462,9 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         }
         const CqStep md = smeta[sc % MR];
         if (md.t == ~0ull) break;
+        uint32_t cid[4];   // this step's ids (lane's events k0 + 32 j + lane)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cid[j] = nid[j];
         // refill first: occupancy of step sc+DW (its ids landed: QD >= 2 DW + 1),
         // then ids of step sc+QD; separate groups, so the next scan waits for
         // the occupancy words only
@@ -1474,10 +1486,13 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
             // compares: instruction-level parallelism); ev[j] = event
             // k0 + 32 j + lane if its row is occupied, else 0
             uint32_t ev[4], na = 0;
+            uint4 w4 = make_uint4(0u, 0u, 0u, 0u);
+            if (!OL) w4 = lds_v4(ocr + (sc % WR) * 512u + lane * 16u);
+            const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const uint32_t e = lds_u32(id_base + 128u * j);
-                const uint32_t w = OL ? ocur[j] : lds_u32(oc_base + 128u * j);
+                const uint32_t e = cid[j];
+                const uint32_t w = OL ? ocur[j] : wv[j];
                 const bool live = 32u * j + lane < n_here;
                 const bool bad = live && e - 1u >= p.catalog;            // id 0 or > C (A14)
                 err |= bad ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
