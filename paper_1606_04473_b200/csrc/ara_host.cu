@@ -1007,7 +1007,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     // programs, one fold chunk) with a kernel whose epilogue stores to peers.
     bool p2p_ok_kernel = ctx->kernel_variant < 0 || ctx->kernel_variant == 0 || ctx->kernel_variant == 5 ||
                          ctx->kernel_variant == 12 || ctx->kernel_variant == 14 || ctx->kernel_variant == 15 ||
-                         (ctx->kernel_variant >= 16 && ctx->kernel_variant <= 19);
+                         (ctx->kernel_variant >= 16 && ctx->kernel_variant <= 20);
     bool single_group = (groups.size() == 1 || multiwin) && !groups[0].wide && n_programs == 0 &&
                         (!fold || (n_layers + nlc - 1) / nlc == 1) && world <= (uint32_t)kMaxPeers;
     bool use_p2p = false;
@@ -1232,7 +1232,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 int variant = ctx->kernel_variant;
                 if (variant == 15) variant = 14;   // multi-window only for multi-window runs (above)
                 if (variant < 0 && p.bm) variant = 17;   // compacted rounds over the packed rows
-                if (variant >= 17 && variant <= 19 && !p.pk) variant = 16;
+                if (variant >= 17 && variant <= 20 && !p.pk) variant = 16;
                 if (p.bm) {   // rows actually gathered: the occupied fraction of the block
                     const uint32_t blk = g.q0 / spb;
                     used_occupancy = (double)ctx->occ_rows[blk] / ((double)ctx->catalog + 1.0);

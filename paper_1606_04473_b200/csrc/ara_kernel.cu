@@ -1173,21 +1173,21 @@ struct CqStep {
     uint32_t sh, pad;      // position of event k0 in the step's id slot
 };
 
-template <int MINB_>
+template <int MINB_, int SE_ = 128>
 struct CqRings {
     static constexpr int QD = 3;        // ids are copied QD steps ahead
     static constexpr int DW = 1;        // occupancy words DW steps ahead (QD >= 2 DW + 1)
-    static constexpr int IR = QD + 1;   // id ring slots (33 x 16 B)
-    static constexpr int WR = DW + 1;   // occupancy ring slots (128 x u32)
+    static constexpr int IR = QD + 1;   // id ring slots (SE/4 + 1 chunks of 16 B)
+    static constexpr int WR = DW + 1;   // occupancy ring slots (SE x u32)
     static constexpr int MR = 8;        // step-meta ring slots (> QD)
-    static constexpr int IDB = 33 * 16;
-    static constexpr int BYTES = IR * IDB + WR * 512 + MR * (int)sizeof(CqStep);   // per warp
+    static constexpr int IDB = (SE_ / 4 + 1) * 16;
+    static constexpr int BYTES = IR * IDB + WR * SE_ * 4 + MR * (int)sizeof(CqStep);   // per warp
 };
 
-template <typename TV, int NSEC, int BUDGET_KB, int MINB>
+template <typename TV, int NSEC, int BUDGET_KB, int MINB, int SE = 128>
 struct CqGeo {
     using Ring = CoGeo<TV, NSEC, BUDGET_KB>;
-    using R = CqRings<MINB>;
+    using R = CqRings<MINB, SE>;
     static constexpr int BYTES = Ring::WARPS * Ring::NS * Ring::STAGE + Ring::WARPS * Ring::NS * (int)sizeof(StepMeta) +
                                  Ring::WARPS * R::BYTES;
 };
@@ -1204,20 +1204,25 @@ __device__ __forceinline__ void cp_wait_upto(uint32_t n) {
     }
 }
 
-template <typename TV, int NSEC, int NLB, int BUDGET_KB, int MINB, int NWIN, bool PK = false, bool OL = false>
+template <typename TV, int NSEC, int NLB, int BUDGET_KB, int MINB, int NWIN, bool PK = false, bool OL = false,
+          int SE = 128>
 __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_constant__ TrialParams p) {
     // PK: the rounds gather packed rows (one 32-B slot per event, p.pk; NSEC == 1)
     // OL: a step's occupancy words are plain L1-cached loads into registers,
     //     issued one step ahead, instead of cp.async copies into the ring
     static_assert(!PK || (NSEC == 1 && NWIN == 1), "packed rounds: one sector per event, one window");
     static_assert(!OL || NWIN == 1, "register occupancy words: one window");
+    // SE: events per scan step (SUB = SE / 32 sub-steps, scanned 4 at a time)
+    static_assert(SE == 128 || (SE == 256 && NWIN == 1 && !OL), "256-event steps: one window, cp.async words");
+    constexpr int SUB = SE / 32;
+    constexpr int NCH = SE / 4 + 1;   // 16-B id chunks spanning a step's ids
     // NWIN == 1: one row window (layers 0..n_layers-1 share it: towers);
     // NWIN > 1: p.n_layers disjoint windows, one layer each, scanned together
     // (one id stream, one combined 4-bit occupancy word per event, one FIFO
     // per window; the last round of a trial is an empty finalising marker)
     static_assert(NWIN == 1 || NWIN == NLB, "one layer per window");
     using Geo = CoGeo<TV, NSEC, BUDGET_KB>;
-    using RG = typename CqGeo<TV, NSEC, BUDGET_KB, MINB>::R;
+    using RG = typename CqGeo<TV, NSEC, BUDGET_KB, MINB, SE>::R;
     constexpr int NS = Geo::NS;
     constexpr int CH = Geo::CH, LPR = Geo::LPR, RPI = Geo::RPI;
     constexpr int QD = RG::QD, DW = RG::DW, IR = RG::IR, WR = RG::WR, MR = RG::MR, IDB = RG::IDB;
@@ -1231,7 +1236,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
     unsigned char* wsm = smem + Geo::WARPS * NS * (Geo::STAGE + (int)sizeof(StepMeta)) + wib * RG::BYTES;
     const uint32_t idr = (uint32_t)__cvta_generic_to_shared(wsm);   // id ring [IR][33 x 16 B]
     const uint32_t ocr = idr + IR * IDB;                            // occupancy ring [WR][128]
-    CqStep* smeta = reinterpret_cast<CqStep*>(wsm + IR * IDB + WR * 512);
+    CqStep* smeta = reinterpret_cast<CqStep*>(wsm + IR * IDB + WR * SE * 4);
     if (SM) {
         for (int i = threadIdx.x; i < NLB * kMaxWin; i += kThreads)
             s_term[i / kMaxWin][i % kMaxWin] = p.term[i / kMaxWin][i % kMaxWin];
@@ -1286,22 +1291,22 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
     auto fetch_ids = [&](uint32_t x) {
         CqStep md{~0ull, 0u, 0u, 0u, 0u};
         if (it_valid) {
-            const uint32_t cnt = it_n - it_k0 < 128u ? it_n - it_k0 : 128u;
+            const uint32_t cnt = it_n - it_k0 < (uint32_t)SE ? it_n - it_k0 : (uint32_t)SE;
             const uintptr_t ab = reinterpret_cast<uintptr_t>(p.ids + it_a + it_k0);
             const uintptr_t al = ab & ~(uintptr_t)15;
             const uintptr_t end = ab + 4u * cnt;
             const uint32_t dst = idr + (x % IR) * IDB;
 #pragma unroll
-            for (int r = 0; r < 2; ++r) {
+            for (int r = 0; r < (NCH + 31) / 32; ++r) {
                 const uint32_t c = lane + 32u * (uint32_t)r;
-                if (r == 0 || lane == 0) {
+                if (32 * (r + 1) <= NCH || c < (uint32_t)NCH) {
                     const uintptr_t cs = al + 16u * c;
                     const uint32_t nb = cs >= end ? 0u : (end - cs >= 16u ? 16u : (uint32_t)(end - cs));
                     cp_async16(dst + 16u * c, reinterpret_cast<const void*>(nb ? cs : al), nb);
                 }
             }
             md = CqStep{it_t, it_n, it_k0, (uint32_t)(ab - al) / 4u, gseq};   // pad: the ids' commit group
-            it_k0 += 128u;
+            it_k0 += (uint32_t)SE;
             if (it_k0 >= it_n) {
                 it_t += nw;
                 it_valid = it_t < p.t_end;
@@ -1316,16 +1321,18 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
     // copy the occupancy words of step x's events (its ids have landed); the
     // lane's 4 ids stay in nid for the scan of step x (NWIN == 1: the words
     // land lane-major, [lane][j], so the scan reads its 4 with one load)
-    uint32_t nid[4] = {0u, 0u, 0u, 0u};
+    uint32_t nid[SUB];
+#pragma unroll
+    for (int j = 0; j < SUB; ++j) nid[j] = 0u;
     auto fetch_occupancy = [&](uint32_t x) {
         const uint32_t sh = smeta[x % MR].sh;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < SUB; ++j) {
             uint32_t e = lds_u32(idr + (x % IR) * IDB + (sh + 32u * j + lane) * 4u);
             nid[j] = e;
             e = e <= p.catalog ? e : 0u;   // not validated yet
-            const uint32_t slot = NWIN == 1 ? lane * 4u + (uint32_t)j : 32u * j + lane;
-            cp_async4(ocr + ((x % WR) * 128u + slot) * 4u, bm + (e >> (NWIN > 1 ? 3 : 5)), bm ? 4u : 0u);
+            const uint32_t slot = NWIN == 1 ? lane * (uint32_t)SUB + (uint32_t)j : 32u * j + lane;
+            cp_async4(ocr + ((x % WR) * (uint32_t)SE + slot) * 4u, bm + (e >> (NWIN > 1 ? 3 : 5)), bm ? 4u : 0u);
         }
     };
 
@@ -1462,9 +1469,9 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         }
         const CqStep md = smeta[sc % MR];
         if (md.t == ~0ull) break;
-        uint32_t cid[4];   // this step's ids (lane's events k0 + 32 j + lane)
+        uint32_t cid[SUB];   // this step's ids (lane's events k0 + 32 j + lane)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) cid[j] = nid[j];
+        for (int j = 0; j < SUB; ++j) cid[j] = nid[j];
         // refill first: occupancy of step sc+DW (its ids landed: QD >= 2 DW + 1),
         // then ids of step sc+QD; separate groups, so the next scan waits for
         // the occupancy words only
@@ -1476,33 +1483,47 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         }
         fetch_ids(sc + QD);
         commit();
-        const bool trial_end = md.k0 + 128u >= md.n;
+        const bool trial_end = md.k0 + (uint32_t)SE >= md.n;
 #pragma unroll 1
         const uint32_t id_base = idr + (sc % IR) * IDB + (md.sh + lane) * 4u;
         const uint32_t oc_base = ocr + ((sc % WR) * 128u + lane) * 4u;
         const uint32_t n_here = md.n - md.k0;   // events of the trial from this step on
         if constexpr (NWIN == 1) {
-            // (1) the step's 4 sub-steps tested at once (independent loads and
-            // compares: instruction-level parallelism); ev[j] = event
-            // k0 + 32 j + lane if its row is occupied, else 0
+            uint32_t wv[SUB];
+            if (OL) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) wv[j] = ocur[j];
+            } else {
+#pragma unroll
+                for (int q = 0; q < SUB / 4; ++q) {
+                    const uint4 w4 = lds_v4(ocr + ((sc % WR) * (uint32_t)SE + lane * (uint32_t)SUB + 4u * q) * 4u);
+                    wv[4 * q] = w4.x; wv[4 * q + 1] = w4.y; wv[4 * q + 2] = w4.z; wv[4 * q + 3] = w4.w;
+                }
+            }
+#pragma unroll 1
+            for (uint32_t h = 0; h < (uint32_t)(SUB / 4); ++h) {
+            // (1) 4 sub-steps tested at once (independent loads and compares:
+            // instruction-level parallelism); ev[j] = event k0 + 128 h + 32 j
+            // + lane if its row is occupied, else 0
             uint32_t ev[4], na = 0;
-            uint4 w4 = make_uint4(0u, 0u, 0u, 0u);
-            if (!OL) w4 = lds_v4(ocr + (sc % WR) * 512u + lane * 16u);
-            const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const uint32_t e = cid[j];
-                const uint32_t w = OL ? ocur[j] : wv[j];
-                const bool live = 32u * j + lane < n_here;
+                const uint32_t w = wv[j];
+                const bool live = 128u * h + 32u * j + lane < n_here;
                 const bool bad = live && e - 1u >= p.catalog;            // id 0 or > C (A14)
                 err |= bad ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
                 ev[j] = (live && !bad && (!bm || ((w >> (e & 31u)) & 1u))) ? e : 0u;
                 na += ev[j] ? 1u : 0u;
             }
+            // the next 4 sub-steps move down (constant register indices)
+#pragma unroll
+            for (int j = 0; j + 4 < SUB; ++j) { cid[j] = cid[j + 4]; wv[j] = wv[j + 4]; }
+            const bool flush = trial_end && h + 1u == (uint32_t)(SUB / 4);
             // (2) rounds are emitted until every lane's FIFO has room for the
-            // step's appends, (3) the appends (right-aligned FIFO: an append
-            // shifts it left by one -- predicated moves), (4) at the end of
-            // the trial, rounds until every FIFO is empty, the last one
+            // appends, (3) the appends (right-aligned FIFO: an append shifts
+            // it left by one -- predicated moves), (4) at the end of the
+            // trial, rounds until every FIFO is empty, the last one
             // finalising the trial.  The FIFO keeps each lane's events in
             // increasing k, so the emission points do not change any sum.
             bool appended = false;
@@ -1521,7 +1542,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
                         }
                         fc[0] += na;
                         appended = true;
-                        if (!trial_end) break;
+                        if (!flush) break;
                         continue;
                     }
                 } else {
@@ -1530,6 +1551,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
                 if (tail - head == (uint32_t)NS) consume();
                 emit(md.t, last, 0u);
                 if (last) break;
+            }
             }
         } else {
 #pragma unroll 1
@@ -2080,10 +2102,10 @@ void* pick_nsec_cq(uint32_t nsec, int* smem) {
 
 // packed rounds (17): one 32-B slot per event; the row ring (BUDGET_KB) holds
 // NS 1-KB stages per warp
-template <typename TV, int NLB, int B, bool OL>
+template <typename TV, int NLB, int B, bool OL, int SE = 128>
 void* pick_pk(int* smem) {
-    *smem = CqGeo<TV, 1, B, 2>::BYTES;
-    return (void*)trial_kernel_cq<TV, 1, NLB, B, 2, 1, true, OL>;
+    *smem = CqGeo<TV, 1, B, 2, SE>::BYTES;
+    return (void*)trial_kernel_cq<TV, 1, NLB, B, 2, 1, true, OL, SE>;
 }
 
 // two CTAs/SM: a 2-stage row ring (64 KB) plus the id/occupancy rings per CTA;
@@ -2094,6 +2116,7 @@ void* pick_cq(uint32_t nsec, int nl, int variant, int* smem) {
     if (variant == 17) return pick_pk<TV, NLB, 10, false>(smem);              \
     if (variant == 18) return pick_pk<TV, NLB, 10, true>(smem);               \
     if (variant == 19) return pick_pk<TV, NLB, 40, false>(smem);              \
+    if (variant == 20) return pick_pk<TV, NLB, 10, false, 256>(smem);         \
     if (variant == 16) return pick_nsec_cq<TV, NLB, 40, 2>(nsec, smem);       \
     return pick_nsec_cq<TV, NLB, 66, 2>(nsec, smem);
     if (nl <= 1) { ARA_CQ_V(1) }
@@ -2119,7 +2142,7 @@ void* pick_cqm(uint32_t nsec, int* smem) {
 // 15 = the same over up to 4 disjoint layer windows in one launch (host-selected),
 // 16 = 14 with a 1-stage row ring, 17 = compacted rounds over packed rows (p.pk),
 // 18 = 17 with the occupancy words by L1-cached loads into registers,
-// 19 = 17 with a 4-stage row ring.
+// 19 = 17 with a 4-stage row ring, 20 = 17 with 256-event scan steps.
 void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
     *smem = 0;
     if (variant == 8 && nsec <= 4)
@@ -2128,7 +2151,7 @@ void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
     if (variant == 1) return fp32 ? pick_sm<float>(nsec, nl, smem) : pick_sm<double>(nsec, nl, smem);
     if (variant >= 10 && variant <= 13 && nsec <= 4)
         return fp32 ? pick_co<float>(nsec, nl, variant, smem) : pick_co<double>(nsec, nl, variant, smem);
-    if (((variant >= 16 && variant <= 19) || variant == 14) && nsec <= 4)
+    if (((variant >= 16 && variant <= 20) || variant == 14) && nsec <= 4)
         return fp32 ? pick_cq<float>(nsec, nl, variant, smem) : pick_cq<double>(nsec, nl, variant, smem);
     if (variant == 15 && nsec <= 4) return fp32 ? pick_cqm<float>(nsec, smem) : pick_cqm<double>(nsec, smem);
     return fp32 ? pick<float>(nsec, nl, variant) : pick<double>(nsec, nl, variant);
@@ -2172,6 +2195,12 @@ cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int
     }
     if (const char* v = getenv("ARA_CARVEOUT")) {   // A/B: shared-memory carveout preference (percent)
         cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(v));
+        cudaGetLastError();
+    } else if (variant == 17) {
+        // the smallest shared-memory configuration that holds the 2 CTAs/SM
+        // (2 x 37 KB -> the 100 KB split): the rest of the 256 KB is L1 for
+        // the occupancy bitmap (measured 5.94 vs 5.98 ms at the driver's 132 KB)
+        cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 34);
         cudaGetLastError();
     }
     void* args[] = {(void*)&p};
