@@ -267,41 +267,56 @@ __device__ __forceinline__ void event_compute_packed(const TrialParams& p, const
     constexpr bool SM = true;   // lanes look up different columns: shared memory, not the constant bank
     uint32_t mask, e;
     asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(mask), "=r"(e) : "r"(src + (swz << 4)) : "memory");
-    const uint32_t nz = (mask >> p.pk_col0) & p.pk_wmask;
-    // the slot holds all of the row's non-zeros (the common case): no
-    // dense-table reads in the loop below
-    const bool full = __popc(mask) <= CAP;
     // one pass over the window's non-zeros (ascending column), every layer of
     // the launch accumulating its own l_e in that order
     double le[NLB];
 #pragma unroll
     for (int l = 0; l < NLB; ++l) le[l] = 0.0;
-    uint32_t mm = nz;
-    while (mm) {
-        const uint32_t j = (uint32_t)(__ffs(mm) - 1);
-        mm &= mm - 1u;
-        const uint32_t b = j + p.pk_col0;
-        const uint32_t v = __popc(mask & ((1u << b) - 1u));   // rank of column b among the row's non-zeros
-        double x;
-        if (full || v < (uint32_t)CAP) {
-            const uint32_t o = 8u + v * (uint32_t)sizeof(TV);
-            const uint32_t a = src + (((o >> 4) ^ swz) << 4) + (o & 15u);
-            if (sizeof(TV) == 8) {
-                asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a) : "memory");
-            } else {
-                float xf;
-                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xf) : "r"(a) : "memory");
-                x = (double)xf;
-            }
-        } else {
-            x = (double)__ldg(static_cast<const TV*>(p.table) + p.sec_off[0] + (uint64_t)e * p.row_stride + j);
-        }
+    auto add = [&](double x, uint32_t j) {
 #pragma unroll
         for (int l = 0; l < NLB; ++l) {
             if (l == 0 || l < (int)p.n_layers) {   // a launch has >= 1 layer
                 const double2 tc = SM ? lds_term(&s_term[l][j]) : p.term[l][j];
                 le[l] = __dadd_rn(le[l], terms(x, tc.x, tc.y));
             }
+        }
+    };
+    auto lds_val = [&](uint32_t o) {   // value at byte o of the staged slot
+        const uint32_t a = src + (((o >> 4) ^ swz) << 4) + (o & 15u);
+        double x;
+        if (sizeof(TV) == 8) {
+            asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a) : "memory");
+        } else {
+            float xf;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(xf) : "r"(a) : "memory");
+            x = (double)xf;
+        }
+        return x;
+    };
+    if (__popc(mask) <= CAP) {
+        // the slot holds all of the row's non-zeros (the common case): walk
+        // them in column order, the v-th at byte 8 + v * esz
+        uint32_t mm = mask, o = 8u;
+        while (mm) {
+            const uint32_t b = (uint32_t)(__ffs(mm) - 1);
+            mm &= mm - 1u;
+            const uint32_t j = b - p.pk_col0;   // window element (wraps when b < col0)
+            if (j < 32u && ((p.pk_wmask >> j) & 1u)) add(lds_val(o), j);
+            o += (uint32_t)sizeof(TV);
+        }
+    } else {
+        // more non-zeros than the slot holds: the first CAP from the slot,
+        // the rest from the dense table
+        uint32_t mm = (mask >> p.pk_col0) & p.pk_wmask;
+        while (mm) {
+            const uint32_t j = (uint32_t)(__ffs(mm) - 1);
+            mm &= mm - 1u;
+            const uint32_t v = __popc(mask & ((1u << (j + p.pk_col0)) - 1u));   // rank among the row's non-zeros
+            const double x = v < (uint32_t)CAP
+                                 ? lds_val(8u + v * (uint32_t)sizeof(TV))
+                                 : (double)__ldg(static_cast<const TV*>(p.table) + p.sec_off[0] +
+                                                 (uint64_t)e * p.row_stride + j);
+            add(x, j);
         }
     }
 #pragma unroll
@@ -1293,19 +1308,18 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         if (it_valid) {
             const uint32_t cnt = it_n - it_k0 < (uint32_t)SE ? it_n - it_k0 : (uint32_t)SE;
             const uintptr_t ab = reinterpret_cast<uintptr_t>(p.ids + it_a + it_k0);
-            const uintptr_t al = ab & ~(uintptr_t)15;
-            const uintptr_t end = ab + 4u * cnt;
+            const char* al = reinterpret_cast<const char*>(ab & ~(uintptr_t)15);
+            const uint32_t rem = (uint32_t)(ab & 15u) + 4u * cnt;   // bytes from al to the step's last id
             const uint32_t dst = idr + (x % IR) * IDB;
 #pragma unroll
             for (int r = 0; r < (NCH + 31) / 32; ++r) {
-                const uint32_t c = lane + 32u * (uint32_t)r;
-                if (32 * (r + 1) <= NCH || c < (uint32_t)NCH) {
-                    const uintptr_t cs = al + 16u * c;
-                    const uint32_t nb = cs >= end ? 0u : (end - cs >= 16u ? 16u : (uint32_t)(end - cs));
-                    cp_async16(dst + 16u * c, reinterpret_cast<const void*>(nb ? cs : al), nb);
+                const uint32_t off = 16u * (lane + 32u * (uint32_t)r);
+                if (32 * (r + 1) <= NCH || off < 16u * (uint32_t)NCH) {
+                    const uint32_t nb = off >= rem ? 0u : (rem - off >= 16u ? 16u : rem - off);
+                    cp_async16(dst + off, al + (nb ? off : 0u), nb);
                 }
             }
-            md = CqStep{it_t, it_n, it_k0, (uint32_t)(ab - al) / 4u, gseq};   // pad: the ids' commit group
+            md = CqStep{it_t, it_n, it_k0, (uint32_t)(ab & 15u) / 4u, gseq};   // pad: the ids' commit group
             it_k0 += (uint32_t)SE;
             if (it_k0 >= it_n) {
                 it_t += nw;
@@ -1484,7 +1498,6 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         fetch_ids(sc + QD);
         commit();
         const bool trial_end = md.k0 + (uint32_t)SE >= md.n;
-#pragma unroll 1
         const uint32_t id_base = idr + (sc % IR) * IDB + (md.sh + lane) * 4u;
         const uint32_t oc_base = ocr + ((sc % WR) * 128u + lane) * 4u;
         const uint32_t n_here = md.n - md.k0;   // events of the trial from this step on
