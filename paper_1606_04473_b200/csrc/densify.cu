@@ -85,29 +85,37 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const unsigned char* __r
                                                         const uint32_t* __restrict__ occ, uint32_t n_blocks,
                                                         uint32_t catalog, uint32_t epb,
                                                         uint64_t block_bytes, unsigned char* __restrict__ pk) {
+    // one thread per row: the bitmap word is a warp broadcast, an occupied
+    // row is read with independent 16-B loads
     constexpr int CAP = (kPackBytes - 8) / (int)sizeof(TV);
+    constexpr int EPC = 16 / (int)sizeof(TV);   // elements per 16-B chunk
     using UT = typename std::conditional<sizeof(TV) == 8, unsigned long long, uint32_t>::type;
+    const uint32_t nchunk = epb * (uint32_t)sizeof(TV) / 16u;   // 2 .. 8 (rows are 32-B multiples)
     for (uint32_t b = blockIdx.y; b < n_blocks; b += gridDim.y) {
-    if (2ull * occ[b] > (uint64_t)catalog + 1) continue;   // dense block: not packed (host rule, ara_run)
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < bm_words; i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t w = bm[b * bm_words + i];
-        while (w) {
-            const uint32_t bit = __ffs(w) - 1;
-            w &= w - 1;
-            const uint64_t e = i * 32 + bit;
-            if (e > catalog) break;
-            const UT* row = reinterpret_cast<const UT*>(tab + b * block_bytes + e * epb * sizeof(TV));
+        if (2ull * occ[b] > (uint64_t)catalog + 1) continue;   // dense block: not packed (host rule, ara_run)
+        for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e <= catalog;
+             e += (uint64_t)gridDim.x * blockDim.x) {
+            if (!((__ldg(bm + b * bm_words + (e >> 5)) >> (e & 31u)) & 1u)) continue;
+            const uint4* row = reinterpret_cast<const uint4*>(tab + b * block_bytes + e * epb * sizeof(TV));
+            uint4 ch[kBlockBytes / 16];
+#pragma unroll
+            for (int q = 0; q < kBlockBytes / 16; ++q) ch[q] = (uint32_t)q < nchunk ? __ldg(row + q) : make_uint4(0, 0, 0, 0);
             uint32_t mask = 0, n = 0;
             UT v[CAP];
 #pragma unroll
             for (int k = 0; k < CAP; ++k) v[k] = 0;
-            for (uint32_t c = 0; c < epb; ++c) {
-                const UT x = row[c];
-                if (x == 0) continue;
-                mask |= 1u << c;
 #pragma unroll
-                for (int k = 0; k < CAP; ++k) v[k] = (n == (uint32_t)k) ? x : v[k];
-                ++n;
+            for (int q = 0; q < kBlockBytes / 16; ++q) {
+                UT x[EPC];
+                memcpy(x, &ch[q], 16);
+#pragma unroll
+                for (int h = 0; h < EPC; ++h) {
+                    if (x[h] == 0) continue;
+                    mask |= 1u << (q * EPC + h);
+#pragma unroll
+                    for (int k = 0; k < CAP; ++k) v[k] = (n == (uint32_t)k) ? x[h] : v[k];
+                    ++n;
+                }
             }
             uint32_t out[kPackBytes / 4];
             out[0] = mask;
@@ -117,7 +125,6 @@ __global__ void __launch_bounds__(256) pack_rows_kernel(const unsigned char* __r
             dst[0] = make_uint4(out[0], out[1], out[2], out[3]);
             dst[1] = make_uint4(out[4], out[5], out[6], out[7]);
         }
-    }
     }
 }
 
@@ -141,9 +148,8 @@ cudaError_t launch_pack_rows(void* d_table, const TableGeo& geo, uint32_t catalo
     unsigned char* t = static_cast<unsigned char*>(d_table);
     const uint32_t* bm = reinterpret_cast<const uint32_t*>(t + geo.bm_off);
     const uint32_t* occ = reinterpret_cast<const uint32_t*>(t + geo.occ_off);
-    const uint64_t words = ((uint64_t)catalog + 1 + 31) / 32;
-    uint64_t bx = (words + 255) / 256;
-    if (bx > 148 * 4) bx = 148 * 4;
+    uint64_t bx = ((uint64_t)catalog + 1 + 255) / 256;   // one thread per row (latency-bound row reads)
+    if (bx > 65535) bx = 65535;
     const dim3 grid((unsigned)bx, geo.n_blocks < 65535u ? geo.n_blocks : 65535u);
     const uint64_t block_bytes = geo.block_elems * geo.esz;
     if (fp32)
