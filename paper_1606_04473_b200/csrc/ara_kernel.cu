@@ -1241,7 +1241,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
     constexpr int NS = Geo::NS;
     constexpr int CH = Geo::CH, LPR = Geo::LPR, RPI = Geo::RPI;
     constexpr int QD = RG::QD, DW = RG::DW, IR = RG::IR, WR = RG::WR, MR = RG::MR, IDB = RG::IDB;
-    constexpr int QC = NWIN > 1 ? 2 : 4;   // per-lane FIFO of occupied events (per window)
+    constexpr int QC = NWIN > 1 ? 2 : 6;   // per-lane FIFO of occupied events (per window)
     constexpr bool SM = PK || TermsInSmem<TV, NSEC, NLB>::value;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ double2 s_term[SM ? NLB : 1][kMaxWin];
