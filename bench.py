@@ -176,7 +176,7 @@ def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str
     YLT row.  Fold mode: the fold pass reads
     every catalogue row window once and writes 8 B per (event id, layer); the
     trial pass reads 4 B of id + one fold row (8 B x layers, padded to a power
-    of two) per event.  Packed rows (kernels 17-19): an occupied event's
+    of two) per event.  Packed rows (kernels 17-21): an occupied event's
     non-zero losses are one 32-B packed slot, so the occupied fraction costs
     one sector per event instead of the window's sectors."""
     eps = 4 if precision == "f64" else 8
@@ -209,7 +209,9 @@ def load_peaks():
         return {}
 
 
-KERNEL_NAMES = {17: "ara::trial_kernel_cq (compacted rounds over packed rows)",
+KERNEL_NAMES = {21: "ara::trial_kernel_cq (compacted rounds over packed rows, packed across trials)",
+                20: "ara::trial_kernel_cq (packed rows, 256-event steps)",
+                17: "ara::trial_kernel_cq (compacted rounds over packed rows)",
                 18: "ara::trial_kernel_cq (packed rows, 2-stage ring)", 19: "ara::trial_kernel_cq (packed rows, 4-stage ring)",
                 16: "ara::trial_kernel_cq (compacted rounds, 1-stage ring)", 14: "ara::trial_kernel_cq (compacted rounds)", 12: "ara::trial_kernel_co (cooperative ring)",
                 5: "ara::trial_kernel (register pipeline)", 0: "ara::trial_kernel (register pipeline)",
@@ -440,7 +442,7 @@ def main():
     # roofline of the dominant kernel (the ARA trial kernel) on this rank
     k_ms = float(np.mean(kern_ms))
     alg = algorithmic_bytes(w, ev_local, count, a.precision, a.mode, occupancy=used.get("occupancy", 1.0),
-                            packed=used.get("variant") in (17, 18, 19))
+                            packed=used.get("variant") in (17, 18, 19, 20, 21))
     peaks = load_peaks()
     peak = peaks.get("hbm_gbs")
     peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"

@@ -120,9 +120,9 @@ typedef struct {
     double total_ms;         /* whole ara_run on the stream, first enqueue to completion */
     uint64_t h2d_bytes;      /* bytes copied host->device inside this run */
     uint32_t n_kernel_launches;
-    int32_t kernel_variant;  /* trial kernel of the last direct launch: 14 compacted rounds (sparse
-                                tables), 12 cooperative cp.async ring, 5/0 register pipeline, ...
-                                (ARA_KERNEL numbering); -2 = fold mode, -1 = none */
+    int32_t kernel_variant;  /* trial kernel of the last direct launch: 21 compacted rounds over packed
+                                rows, packed across trials (sparse tables), 12 cooperative cp.async ring, 5/0 register
+                                pipeline, ... (ARA_KERNEL numbering); -2 = fold mode, -1 = none */
     double occupancy;        /* fraction of row windows the last direct launch gathers: the occupied-row
                                 fraction of its column block when zero rows are skipped, else 1.0 */
 } ara_run_stats;
@@ -163,6 +163,10 @@ const char* ara_last_error(const ara_ctx* ctx);
  *   (an ELT is a map: no duplicates).
  *   terms [n_elts] or NULL (identity: deductible 0, limit +inf).
  * Arrays may be host or device memory; they are not referenced after return.
+ * Besides the table, the call builds a row-occupancy bitmap per 128-B column
+ * block and, for blocks with at most half of their rows occupied, a packed
+ * copy of every occupied row (one 32-B sector: non-zero mask, event id, first
+ * non-zero losses), which the default sparse kernel gathers instead of the row.
  * COLLECTIVE when world > 1: rank 0's arrays are authoritative; rank 0
  * validates them and broadcasts the sparse records over NVLink (ncclBroadcast),
  * then every rank densifies its own copy of the table.  Other ranks may pass

@@ -1007,7 +1007,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     // programs, one fold chunk) with a kernel whose epilogue stores to peers.
     bool p2p_ok_kernel = ctx->kernel_variant < 0 || ctx->kernel_variant == 0 || ctx->kernel_variant == 5 ||
                          ctx->kernel_variant == 12 || ctx->kernel_variant == 14 || ctx->kernel_variant == 15 ||
-                         (ctx->kernel_variant >= 16 && ctx->kernel_variant <= 20);
+                         (ctx->kernel_variant >= 16 && ctx->kernel_variant <= 21);
     bool single_group = (groups.size() == 1 || multiwin) && !groups[0].wide && n_programs == 0 &&
                         (!fold || (n_layers + nlc - 1) / nlc == 1) && world <= (uint32_t)kMaxPeers;
     bool use_p2p = false;
@@ -1224,15 +1224,15 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
             } else {
                 setup_window(g, p);
                 // Kernel choice (measured, profiles/r01_kernel_variants.md): windows over a
-                // sparse column block (occupancy bitmap set) use the compacted-rounds kernel
-                // (14); dense fp64 windows of <= 4 sectors the cooperative cp.async ring at
+                // sparse column block (occupancy bitmap set) use the compacted-rounds kernel over
+                // packed rows with rounds packed across trials (21); dense fp64 windows of <= 4 sectors the cooperative cp.async ring at
                 // 3 CTAs/SM (12); dense fp32 windows the register-pipelined LDG kernel at
                 // 3 CTAs/SM (5) for single layers, 2 CTAs/SM (0) for shared-window towers.
                 // The other variants stay ARA_KERNEL-selectable for A/B runs.
                 int variant = ctx->kernel_variant;
                 if (variant == 15) variant = 14;   // multi-window only for multi-window runs (above)
-                if (variant < 0 && p.bm) variant = 17;   // compacted rounds over the packed rows
-                if (variant >= 17 && variant <= 20 && !p.pk) variant = 16;
+                if (variant < 0 && p.bm) variant = 21;   // compacted rounds over the packed rows, across trials
+                if (variant >= 17 && variant <= 21 && !p.pk) variant = 16;
                 if (p.bm) {   // rows actually gathered: the occupied fraction of the block
                     const uint32_t blk = g.q0 / spb;
                     used_occupancy = (double)ctx->occ_rows[blk] / ((double)ctx->catalog + 1.0);

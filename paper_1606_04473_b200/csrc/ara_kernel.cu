@@ -262,7 +262,10 @@ __device__ __forceinline__ void event_compute_sparse(const TrialParams& p, const
 template <typename TV, int NLB>
 __device__ __forceinline__ void event_compute_packed(const TrialParams& p, const double2 (*s_term)[kMaxWin],
                                                      uint32_t src, uint32_t swz, double (&G)[NLB],
-                                                     uint32_t (&m)[NLB]) {
+                                                     uint32_t (&m)[NLB], double (&Gn)[NLB], uint32_t (&mn)[NLB],
+                                                     bool nxt) {
+    // nxt: the event belongs to the trial after the one G accumulates (rounds
+    // packed across a trial boundary): it is added to Gn / mn instead
     constexpr int CAP = (kPackBytes - 8) / (int)sizeof(TV);
     constexpr bool SM = true;   // lanes look up different columns: shared memory, not the constant bank
     uint32_t mask, e;
@@ -323,8 +326,13 @@ __device__ __forceinline__ void event_compute_packed(const TrialParams& p, const
     for (int l = 0; l < NLB; ++l) {
         if (l >= (int)p.n_layers) break;
         const double o = terms(le[l], p.lw[l].occ_r, p.lw[l].occ_l);
-        G[l] = __dadd_rn(G[l], o);
-        m[l] += (o > 0.0) ? 1u : 0u;
+        if (nxt) {
+            Gn[l] = __dadd_rn(Gn[l], o);
+            mn[l] += (o > 0.0) ? 1u : 0u;
+        } else {
+            G[l] = __dadd_rn(G[l], o);
+            m[l] += (o > 0.0) ? 1u : 0u;
+        }
     }
 }
 
@@ -1220,13 +1228,19 @@ __device__ __forceinline__ void cp_wait_upto(uint32_t n) {
 }
 
 template <typename TV, int NSEC, int NLB, int BUDGET_KB, int MINB, int NWIN, bool PK = false, bool OL = false,
-          int SE = 128>
+          int SE = 128, bool XT = false>
 __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_constant__ TrialParams p) {
     // PK: the rounds gather packed rows (one 32-B slot per event, p.pk; NSEC == 1)
     // OL: a step's occupancy words are plain L1-cached loads into registers,
     //     issued one step ahead, instead of cp.async copies into the ring
     static_assert(!PK || (NSEC == 1 && NWIN == 1), "packed rounds: one sector per event, one window");
     static_assert(!OL || NWIN == 1, "register occupancy words: one window");
+    // XT: rounds packed across trial boundaries -- a trial whose scan has
+    // ended stays "pending" while the next trial's events enter the FIFOs
+    // (tagged), so its last rounds also carry the next trial's events; each
+    // lane adds a tagged event to a second accumulator, and the pending
+    // trial is finalised with the round that pops its last event
+    static_assert(!XT || PK, "cross-trial rounds: packed rows");
     // SE: events per scan step (SUB = SE / 32 sub-steps, scanned 4 at a time)
     static_assert(SE == 128 || (SE == 256 && NWIN == 1 && !OL), "256-event steps: one window, cp.async words");
     constexpr int SUB = SE / 32;
@@ -1389,10 +1403,13 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         for (int i = 0; i < QC; ++i) f[u][i] = 0u;
     }
 
-    double G[NLB];
-    uint32_t m[NLB];
+    double G[NLB], Gn[NLB];
+    uint32_t m[NLB], mn[NLB];
 #pragma unroll
-    for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
+    for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; Gn[l] = 0.0; mn[l] = 0u; }
+    uint32_t ft = 0;          // XT: tag bits of the FIFO entries (bit i <-> f[0][i]): 1 = event of the
+                              //     open trial while another trial is pending
+    uint64_t pend = ~0ull;    // XT: the pending trial, or none
     uint32_t head = 0, tail = 0;   // ring slots: next to consume / next to fill (warp-uniform)
     uint32_t rg[NS];               // commit group of each ring slot's rows
 
@@ -1404,7 +1421,8 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         wait_group(g);
         __syncwarp();   // other lanes' copies of my row are complete and visible
         const StepMeta rm = rmeta[slot];
-        if (PK) event_compute_packed<TV, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m);
+        if (PK) event_compute_packed<TV, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m, Gn, mn,
+                                              XT && ((rm.k0 >> lane) & 1u));
         else if (NWIN == 1) event_compute_sparse<TV, NSEC, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m);
         else event_compute_sparse_win<TV, NSEC, NLB>(p, s_term, my_row + slot * Geo::STAGE, my_swz, G, m, rm.k0);
         __syncwarp();   // every lane's reads of the slot precede the copies refilling it
@@ -1423,8 +1441,51 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
                 store_trial(p, t, G, m);
             }
 #pragma unroll
-            for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
+            for (int l = 0; l < NLB; ++l) {   // XT: the next trial's partial sums move up
+                G[l] = XT ? Gn[l] : 0.0;
+                m[l] = XT ? mn[l] : 0u;
+                Gn[l] = 0.0;
+                mn[l] = 0u;
+            }
         }
+    };
+    // XT: emit a round (pop: every lane pops its FIFO head; !pop: an empty
+    // marker round); the round that leaves the pending trial without entries
+    // finalises it.  StepMeta: {finalised trial, last, tag mask of the lanes'
+    // events}
+    auto emit_xt = [&](bool pop) {
+        uint32_t ce = 0, tg = 0;
+        if (pop) {
+#pragma unroll
+            for (int i = 0; i < QC; ++i) ce = (fc[0] == (uint32_t)(QC - i)) ? f[0][i] : ce;
+            tg = fc[0] ? (ft >> (QC - fc[0])) & 1u : 0u;
+            fc[0] -= fc[0] ? 1u : 0u;
+        }
+        const uint32_t tagmask = __ballot_sync(0xffffffffu, tg != 0u);
+        uint32_t last = 0;
+        uint64_t tf = 0;
+        if (pend != ~0ull) {
+            const uint32_t valid = fc[0] ? (((1u << fc[0]) - 1u) << (QC - fc[0])) : 0u;
+            if (!__any_sync(0xffffffffu, (~ft & valid) != 0u)) {   // no pending-trial entry left
+                last = 1u;
+                tf = pend;
+                pend = ~0ull;
+                ft = 0u;   // the remaining entries belong to the open trial, now untagged
+            }
+        }
+        const uint32_t slot = tail % NS;
+        const uint32_t dst = ring + slot * Geo::STAGE;
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            const uint32_t e = __shfl_sync(0xffffffffu, ce, (uint32_t)i * RPI + c_row);
+            cp_async16(dst + (uint32_t)i * RPI * Geo::ROWB + c_dst[i & 1], c_src + (uint64_t)e * row_bytes,
+                       e ? 16u : 0u);
+        }
+        if (lane == 0) rmeta[slot] = StepMeta{tf, last, tagmask};
+        const uint32_t g = commit();
+#pragma unroll
+        for (int i = 0; i < NS; ++i) rg[i] = (slot == (uint32_t)i) ? g : rg[i];
+        ++tail;
     };
     // emit a round of window u: every lane pops that FIFO's head (0 = nothing:
     // zero-fill); u == NWIN: the empty finalising marker (multi-window)
@@ -1540,6 +1601,42 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
             // finalising the trial.  The FIFO keeps each lane's events in
             // increasing k, so the emission points do not change any sum.
             bool appended = false;
+            if constexpr (XT) {
+                // flush: finalise the pending trial (rounds until its entries
+                // are gone), then the open trial becomes pending -- finalised
+                // at once by an empty marker round if it left no entries
+                bool made_pending = false;
+#pragma unroll 1
+                for (;;) {
+                    bool pop = true;
+                    if (!appended) {
+                        if (!__any_sync(0xffffffffu, fc[0] + na > (uint32_t)QC)) {
+                            const uint32_t tag = pend != ~0ull ? 1u : 0u;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                if (ev[j]) {
+#pragma unroll
+                                    for (int i = 0; i + 1 < QC; ++i) f[0][i] = f[0][i + 1];
+                                    f[0][QC - 1] = ev[j];
+                                    ft = (ft >> 1) | (tag << (QC - 1));
+                                }
+                            }
+                            fc[0] += na;
+                            appended = true;
+                            if (!flush) break;
+                            continue;
+                        }
+                    } else if (pend == ~0ull) {
+                        if (made_pending) break;
+                        pend = md.t;
+                        made_pending = true;
+                        if (__any_sync(0xffffffffu, fc[0] > 0u)) break;
+                        pop = false;   // no entries: the marker round finalises it
+                    }
+                    if (tail - head == (uint32_t)NS) consume();
+                    emit_xt(pop);
+                }
+            } else {
 #pragma unroll 1
             for (;;) {
                 uint32_t last = 0;
@@ -1564,6 +1661,7 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
                 if (tail - head == (uint32_t)NS) consume();
                 emit(md.t, last, 0u);
                 if (last) break;
+            }
             }
             }
         } else {
@@ -1608,6 +1706,13 @@ __global__ void __launch_bounds__(kThreads, MINB) trial_kernel_cq(const __grid_c
         }
         }
         __syncwarp();   // reads of this step's slots precede their refills
+    }
+    if constexpr (XT) {   // the last pending trial
+#pragma unroll 1
+        while (pend != ~0ull) {
+            if (tail - head == (uint32_t)NS) consume();
+            emit_xt(true);
+        }
     }
     while (head != tail) consume();
     cp_wait<0>();
@@ -2115,10 +2220,10 @@ void* pick_nsec_cq(uint32_t nsec, int* smem) {
 
 // packed rounds (17): one 32-B slot per event; the row ring (BUDGET_KB) holds
 // NS 1-KB stages per warp
-template <typename TV, int NLB, int B, bool OL, int SE = 128>
+template <typename TV, int NLB, int B, bool OL, int SE = 128, bool XT = false>
 void* pick_pk(int* smem) {
     *smem = CqGeo<TV, 1, B, 2, SE>::BYTES;
-    return (void*)trial_kernel_cq<TV, 1, NLB, B, 2, 1, true, OL, SE>;
+    return (void*)trial_kernel_cq<TV, 1, NLB, B, 2, 1, true, OL, SE, XT>;
 }
 
 // two CTAs/SM: a 2-stage row ring (64 KB) plus the id/occupancy rings per CTA;
@@ -2130,6 +2235,7 @@ void* pick_cq(uint32_t nsec, int nl, int variant, int* smem) {
     if (variant == 18) return pick_pk<TV, NLB, 10, true>(smem);               \
     if (variant == 19) return pick_pk<TV, NLB, 40, false>(smem);              \
     if (variant == 20) return pick_pk<TV, NLB, 10, false, 256>(smem);         \
+    if (variant == 21) return pick_pk<TV, NLB, 10, false, 128, true>(smem);   \
     if (variant == 16) return pick_nsec_cq<TV, NLB, 40, 2>(nsec, smem);       \
     return pick_nsec_cq<TV, NLB, 66, 2>(nsec, smem);
     if (nl <= 1) { ARA_CQ_V(1) }
@@ -2155,7 +2261,8 @@ void* pick_cqm(uint32_t nsec, int* smem) {
 // 15 = the same over up to 4 disjoint layer windows in one launch (host-selected),
 // 16 = 14 with a 1-stage row ring, 17 = compacted rounds over packed rows (p.pk),
 // 18 = 17 with the occupancy words by L1-cached loads into registers,
-// 19 = 17 with a 4-stage row ring, 20 = 17 with 256-event scan steps.
+// 19 = 17 with a 4-stage row ring, 20 = 17 with 256-event scan steps,
+// 21 = 17 with rounds packed across trial boundaries.
 void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
     *smem = 0;
     if (variant == 8 && nsec <= 4)
@@ -2164,7 +2271,7 @@ void* pick_kernel(int fp32, uint32_t nsec, int nl, int variant, int* smem) {
     if (variant == 1) return fp32 ? pick_sm<float>(nsec, nl, smem) : pick_sm<double>(nsec, nl, smem);
     if (variant >= 10 && variant <= 13 && nsec <= 4)
         return fp32 ? pick_co<float>(nsec, nl, variant, smem) : pick_co<double>(nsec, nl, variant, smem);
-    if (((variant >= 16 && variant <= 20) || variant == 14) && nsec <= 4)
+    if (((variant >= 16 && variant <= 21) || variant == 14) && nsec <= 4)
         return fp32 ? pick_cq<float>(nsec, nl, variant, smem) : pick_cq<double>(nsec, nl, variant, smem);
     if (variant == 15 && nsec <= 4) return fp32 ? pick_cqm<float>(nsec, smem) : pick_cqm<double>(nsec, smem);
     return fp32 ? pick<float>(nsec, nl, variant) : pick<double>(nsec, nl, variant);
@@ -2209,7 +2316,7 @@ cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int
     if (const char* v = getenv("ARA_CARVEOUT")) {   // A/B: shared-memory carveout preference (percent)
         cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, atoi(v));
         cudaGetLastError();
-    } else if (variant == 17) {
+    } else if (variant == 17 || variant == 21) {
         // the smallest shared-memory configuration that holds the 2 CTAs/SM
         // (2 x 37 KB -> the 100 KB split): the rest of the 256 KB is L1 for
         // the occupancy bitmap (measured 5.94 vs 5.98 ms at the driver's 132 KB)

@@ -448,7 +448,7 @@ def test_portfolio_programs_and_explicit_elt_lists(cuda, run_mode):
         assert np.array_equal(p_o, pml[r]) and np.array_equal(kk, k)
 
 
-@pytest.mark.parametrize("variant", (-1, 14, 16, 17, 18, 19, 20))
+@pytest.mark.parametrize("variant", (-1, 14, 16, 17, 18, 19, 20, 21))
 @pytest.mark.parametrize("precision", ("f64", "f32"))
 def test_packed_rows_overflow_and_offset_windows(cuda, variant, precision):
     """Packed rows (variant 17-19): a sparse block whose first 400 rows are

@@ -45,7 +45,7 @@ def test_random_workloads(cuda, seed, precision):
     ylt, lossy, _, _ = run_gpu(off, ids, elts, w, layers, precision=precision, terms=terms)
     assert_ylt_close(ylt, orc)
     assert np.array_equal(lossy, orc["lossy"])
-    for v in (17, 16, 12, 5):   # packed rounds, compacted rounds, cooperative ring, register pipeline
+    for v in (17, 21, 16, 12, 5):   # packed rounds (+ cross-trial), compacted rounds, cooperative ring, register pipeline
         other, olossy, _, _ = run_gpu(off, ids, elts, w, layers, precision=precision, terms=terms, variant=v)
         assert np.array_equal(ylt, other) and np.array_equal(lossy, olossy), v
     fold, flossy, _, _ = run_gpu(off, ids, elts, w, layers, precision=precision, terms=terms, run_mode="fold")
