@@ -212,7 +212,7 @@ def load_peaks():
 KERNEL_NAMES = {21: "ara::trial_kernel_cq (compacted rounds over packed rows, packed across trials)",
                 20: "ara::trial_kernel_cq (packed rows, 256-event steps)",
                 17: "ara::trial_kernel_cq (compacted rounds over packed rows)",
-                18: "ara::trial_kernel_cq (packed rows, 2-stage ring)", 19: "ara::trial_kernel_cq (packed rows, 4-stage ring)",
+                18: "ara::trial_kernel_cq (packed rows, L1-cached occupancy loads)", 19: "ara::trial_kernel_cq (packed rows, 4-stage ring)",
                 16: "ara::trial_kernel_cq (compacted rounds, 1-stage ring)", 14: "ara::trial_kernel_cq (compacted rounds)", 12: "ara::trial_kernel_co (cooperative ring)",
                 5: "ara::trial_kernel (register pipeline)", 0: "ara::trial_kernel (register pipeline)",
                 -2: "ara::fold_kernel+trial_fold_kernel"}
