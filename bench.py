@@ -100,8 +100,8 @@ def host_info():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons, sampled every 100 ms from before the
-    warm-up to after the timed region; mark() brackets the timed window and
+    """SM clocks + throttle reasons (NVML every 10 ms, else nvidia-smi every
+    100 ms), sampled from before the warm-up to after the timed region; mark() brackets the timed window and
     stop() summarises the samples inside it (all samples if the window was
     shorter than two sampling periods)."""
 
@@ -117,6 +117,36 @@ class ClockSampler:
         self.win = [None, None]
 
     def start(self):
+        # NVML polled every 10 ms (a timed region of ~10 steps lasts only
+        # ~60 ms); nvidia-smi at its 100-ms floor when NVML is unavailable
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+            bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+            self._stop_evt = threading.Event()
+
+            def poll():
+                mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                while not self._stop_evt.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        act = ["Active" if r & b else "Not Active" for b in bits.values()]
+                        self.lines.append((time.time(), ",".join(["t", str(self.gpu), str(sm), str(mx), "0", hex(r)] + act)))
+                    except pynvml.NVMLError:
+                        pass
+                    time.sleep(0.01)
+
+            self.proc = "nvml"
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.proc = None
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
                                           "-lms", "100", "-i", str(self.gpu)],
@@ -136,13 +166,18 @@ class ClockSampler:
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        self.t.join(timeout=2)
+        if self.proc == "nvml":
+            time.sleep(0.03)
+            self._stop_evt.set()
+            self.t.join(timeout=2)
+        else:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
         rows = []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ts, ln in self.lines:
@@ -156,7 +191,8 @@ class ClockSampler:
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
         a, b = self.win
-        inside = [r for r in rows if a is not None and b is not None and a - 0.15 <= r[0] <= b + 0.15]
+        slack = 0.015 if self.proc == "nvml" else 0.15
+        inside = [r for r in rows if a is not None and b is not None and a - slack <= r[0] <= b + slack]
         sel = inside if len(inside) >= 2 else rows
         sm = [r[1] for r in sel]
         load = [x for x in sm if x > 0.5 * max(sm)] or sm
