@@ -479,3 +479,37 @@ def test_packed_rows_overflow_and_offset_windows(cuda, variant, precision):
     ylt2, lossy2, _, _ = run_gpu(off, ids, elts, w, layers, precision=precision, terms=(d, li), variant=variant,
                                  env={"ARA_NO_SKIP": 1})
     assert np.array_equal(ylt, ylt2) and np.array_equal(lossy, lossy2)
+
+
+@pytest.mark.parametrize("variant", (21, 17))
+@pytest.mark.parametrize("rho", (0.01, 0.1, 0.3))
+def test_cross_trial_rounds_short_and_empty_trials(cuda, variant, rho):
+    """Rounds packed across trial boundaries (variant 21): many short, empty
+    and long trials back to back, so trials are pending across several
+    following trials' scans, finalised by marker rounds (trials without
+    occupied events) and forced flushes (a short trial ending while another
+    is pending).  Bit-identical to the per-trial-flush kernel (16) and to the
+    unskipped path, and within tolerance of the oracle."""
+    rng = np.random.default_rng(21)
+    w = synth.get_config("tiny").with_(catalog=4000, rho=rho, n_trials=8)
+    _, _, elts = make_inputs(w)
+    occupied = np.unique(elts[1])
+    lens = rng.choice([0, 1, 2, 3, 5, 31, 32, 33, 127, 128, 129, 700], size=1500)
+    trials = []
+    for i, n in enumerate(lens):
+        if i % 7 == 3:
+            trials.append(rng.choice(occupied, n))             # every event occupied
+        else:
+            trials.append(rng.integers(1, w.catalog + 1, n))   # random
+    off = np.zeros(len(trials) + 1, dtype=np.uint64)
+    off[1:] = np.cumsum([len(t) for t in trials])
+    ids = np.concatenate(trials).astype(np.uint32)
+    w = w.with_(n_trials=len(trials))
+    orc = run_oracle(off, ids, elts, w, w.layers)
+    ylt, lossy, st, _ = run_gpu(off, ids, elts, w, w.layers, variant=variant)
+    assert_ylt_close(ylt, orc)
+    assert np.array_equal(lossy, orc["lossy"])
+    ylt16, lossy16, _, _ = run_gpu(off, ids, elts, w, w.layers, variant=16)
+    assert np.array_equal(ylt, ylt16) and np.array_equal(lossy, lossy16)
+    ylt0, lossy0, _, _ = run_gpu(off, ids, elts, w, w.layers, variant=variant, env={"ARA_NO_SKIP": 1})
+    assert np.array_equal(ylt, ylt0) and np.array_equal(lossy, lossy0)
