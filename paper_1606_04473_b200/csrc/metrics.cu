@@ -213,8 +213,10 @@ __global__ void finish_kernel(const __grid_constant__ MParams P, uint32_t rows) 
 
 __global__ void __launch_bounds__(256) tail_kernel(const __grid_constant__ MParams P) {
     // RC return periods per sweep over the row (each accumulator is the same
-    // per-thread sequential sum over the same keys as a one-period sweep)
-    constexpr int RC = 8;
+    // per-thread sequential sum over the same keys as a one-period sweep).
+    // RC = 10 covers the paper's 10 return periods in one sweep (40 KB of
+    // static shared memory for the block reductions).
+    constexpr int RC = 10;
     __shared__ double s_sum[RC][256];
     __shared__ uint64_t s_cnt[RC][256];
     __shared__ uint32_t s_last;
