@@ -10,7 +10,8 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall 
              -Iinclude -I$(NCCL_DIR)/include --expt-relaxed-constexpr -Xptxas -v --fmad=false
 PKG       := paper_1606_04473_b200
 CSRC      := $(PKG)/csrc
-CU_SRCS   := $(CSRC)/ara_host.cu $(CSRC)/ara_kernel.cu $(CSRC)/densify.cu $(CSRC)/metrics.cu
+CU_SRCS   := $(CSRC)/ara_host.cu $(CSRC)/kernel_sparse.cu $(CSRC)/kernel_dense.cu $(CSRC)/kernel_fold.cu \
+             $(CSRC)/densify.cu $(CSRC)/metrics.cu
 CU_OBJS   := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
 
 all: oracle/liboracle.so synth/libsynth.so $(PKG)/libara.so $(PKG)/libara_mb.so
@@ -21,7 +22,7 @@ oracle/liboracle.so: oracle/oracle.c oracle/oracle.h
 synth/libsynth.so: synth/synth.c synth/synth.h
 	$(CC) -O2 -pthread -fPIC -shared -std=gnu99 -Wall -o $@ synth/synth.c -lm -lpthread
 
-build/%.o: $(CSRC)/%.cu $(CSRC)/ara_internal.cuh include/ara.h
+build/%.o: $(CSRC)/%.cu $(CSRC)/ara_internal.cuh $(CSRC)/ara_device.cuh include/ara.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -dc -o $@ $< 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 

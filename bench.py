@@ -51,8 +51,9 @@ def parse():
     ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
     ap.add_argument("--e2e-mode", default="chunked", choices=["chunked", "all"])
     ap.add_argument("--chunk-trials", type=int, default=65536)
-    ap.add_argument("--e2e-format", default="packed", choices=["packed", "u32"],
-                    help="host YET format for the e2e leg: bit-packed ids (F3, the library's transfer format) or u32")
+    ap.add_argument("--e2e-format", default="both", choices=["both", "u32"],
+                    help="e2e legs: u32 host ids (the headline, plain ara_load_yet) and, with 'both', also the "
+                         "bit-packed transfer format (F3, ara_load_yet_packed) as e2e_packed")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -202,19 +203,19 @@ class ClockSampler:
 
 
 def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str = "direct",
-                      occupancy: float = 1.0, packed: bool = False) -> int:
-    """DESIGN.md section 6 "Algorithmic bytes": the north star's count, YET
-    bytes streamed + 32 B per gathered ELT sector.  Direct mode, per launch
-    (layers sharing one row window share a launch): per event 4 B of id, plus
-    -- when zero rows are skipped (occupancy < 1) -- the sector holding the
-    event's row-occupancy bit, plus the 32-B sectors of the launch's row window
-    for the occupied fraction of events; per trial 8 B of offsets + 8 B per
-    YLT row.  Fold mode: the fold pass reads
-    every catalogue row window once and writes 8 B per (event id, layer); the
-    trial pass reads 4 B of id + one fold row (8 B x layers, padded to a power
-    of two) per event.  Packed rows (kernels 17-21): an occupied event's
-    non-zero losses are one 32-B packed slot, so the occupied fraction costs
-    one sector per event instead of the window's sectors."""
+                      occupancy: float = 1.0, packed: bool = False) -> dict:
+    """DESIGN.md section 6 "Algorithmic bytes", the north star's count: YET
+    bytes streamed + 32 B per ELT sector the kernel actually gathers, per
+    launch (layers sharing one row window share a launch).  Direct mode: per
+    event 4 B of id; per gathered event the row window's 32-B sectors -- or,
+    with packed rows (the sparse kernel), one 32-B slot for the occupied
+    fraction of events only (an unoccupied row is never read); per trial 8 B
+    of offsets + 8 B per YLT row.  The occupancy probes (one bit per event,
+    a 250 KB bitmap held in shared memory / L1 / L2, never DRAM-streamed) are
+    NOT HBM bytes: they are returned separately as index_bytes (one 4-B word
+    per probe).  Fold mode: the fold pass reads every catalogue row window
+    once and writes 8 B per (event id, layer); the trial pass reads 4 B of id
+    + one fold row (8 B x layers, padded to a power of two) per event."""
     eps = 4 if precision == "f64" else 8
     windows = []
     for L in w.layers:
@@ -230,12 +231,19 @@ def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str
         nlc = 1
         while nlc < nl and nlc < 8:
             nlc *= 2
-        return int((w.catalog + 1) * (32 * sec + 8 * nl) + n_events * (4 + 8 * nlc) * ((nl + nlc - 1) // nlc)
-                   + per_trial)
-    per_event = 0.0
+        hbm = int((w.catalog + 1) * (32 * sec + 8 * nl) + n_events * (4 + 8 * nlc) * ((nl + nlc - 1) // nlc)
+                  + per_trial)
+        return {"hbm": hbm, "index": 0, "yet": 4 * n_events * ((nl + nlc - 1) // nlc), "elt": hbm - per_trial}
+    yet = elt = index = 0.0
     for (a, b), _ in windows:
-        per_event += 4 + (32 if occupancy < 1.0 else 0) + occupancy * 32 * (1 if packed else b - a)
-    return int(n_events * per_event + per_trial)
+        yet += 4.0 * n_events
+        if packed:
+            elt += occupancy * 32.0 * n_events
+            index += 4.0 * n_events
+        else:
+            elt += 32.0 * (b - a) * n_events
+    return {"hbm": int(yet + elt + per_trial), "index": int(index), "yet": int(yet), "elt": int(elt),
+            "per_trial": int(per_trial)}
 
 
 def load_peaks():
@@ -245,11 +253,8 @@ def load_peaks():
         return {}
 
 
-KERNEL_NAMES = {21: "ara::trial_kernel_cq (compacted rounds over packed rows, packed across trials)",
-                20: "ara::trial_kernel_cq (packed rows, 256-event steps)",
-                17: "ara::trial_kernel_cq (compacted rounds over packed rows)",
-                18: "ara::trial_kernel_cq (packed rows, L1-cached occupancy loads)", 19: "ara::trial_kernel_cq (packed rows, 4-stage ring)",
-                16: "ara::trial_kernel_cq (compacted rounds, 1-stage ring)", 14: "ara::trial_kernel_cq (compacted rounds)", 12: "ara::trial_kernel_co (cooperative ring)",
+KERNEL_NAMES = {30: "ara::trial_kernel_bc (ballot-compacted rounds over packed rows)",
+                12: "ara::trial_kernel_co (cooperative ring)",
                 5: "ara::trial_kernel (register pipeline)", 0: "ara::trial_kernel (register pipeline)",
                 -2: "ara::fold_kernel+trial_fold_kernel"}
 
@@ -259,23 +264,31 @@ def kernel_name(variant):
     return KERNEL_NAMES.get(int(variant), f"ara::trial_kernel (ARA_KERNEL={variant})")
 
 
+L2_PEAK_SOURCE = "profiles/r01_microbench.json"
+
+
 def l2_gather_peak():
-    """Measured L2 gather ceiling (GB/s): random 32-B gathers from an L2-resident table."""
+    """Builder-measured L2 gather ceiling (GB/s): random 32-B gathers from an
+    L2-resident 16 MB table (tools/microbench.py); not a MEASURED_PEAKS.json
+    figure, so every use names the file."""
     try:
-        return json.load(open(os.path.join(ROOT, "profiles", "r01_microbench.json")))["gather_16MB_32B_gbs"]
+        return json.load(open(os.path.join(ROOT, L2_PEAK_SOURCE)))["gather_16MB_32B_gbs"]
     except (OSError, ValueError, KeyError):
         return None
 
 
-def load_traffic(w, precision, variant):
-    """DRAM bytes (and L2 sectors) per launch of the ARA kernel from the
-    committed ncu --set full capture of the same kernel variant, or None."""
+def load_traffic(w, precision, variant, n_trials_launch):
+    """DRAM bytes and L2->SM sectors per launch of the ARA kernel from the
+    committed ncu --set full capture of the same kernel variant AT THE SAME
+    LAUNCH SIZE (trials per launch), or None."""
     p = os.path.join(ROOT, "profiles", "ara_kernel_traffic.json")
     try:
         d = json.load(open(p)).get(f"{w.name}/{precision}", {})
     except (OSError, ValueError):
         return None
-    return d if d.get("variant") == variant else None
+    if d.get("variant") != variant or d.get("n_trials_per_launch") != n_trials_launch:
+        return None
+    return d
 
 
 # ------------------------------------------------------------------ oracle (cpu baseline / reference arm)
@@ -318,8 +331,12 @@ def reference_arm(a, rank, world):
     # the same config as our arm (weak scaling: N x the workload's trials); the
     # oracle's rate is measured on the bounded sample above
     n_trials = w.n_trials * (world if a.scaling == "weak" else 1)
+    # ms_per_step is the MEASURED time of one step (one bounded sample); the
+    # time the oracle would need for the whole workload is a projection
     line = {"impl": "reference", "metric": METRIC, "value": tps, "unit": "trials/s", "n_gpus": a.gpus,
-            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * n_trials / tps,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * float(np.median([r["seconds"] for r in res])),
+            "ms_per_step_projected_full_workload": 1e3 * n_trials / tps,
+            "trials_per_step": int(np.median([r["trials"] for r in res])),
             "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": a.precision,
             "data": "synthetic", "config": {"workload": w.name, "n_trials": n_trials},
             "lookups_per_sec": float(np.median([r["lookups_per_s"] for r in res])),
@@ -477,27 +494,35 @@ def main():
 
     # roofline of the dominant kernel (the ARA trial kernel) on this rank
     k_ms = float(np.mean(kern_ms))
-    alg = algorithmic_bytes(w, ev_local, count, a.precision, a.mode, occupancy=used.get("occupancy", 1.0),
-                            packed=used.get("variant") in (17, 18, 19, 20, 21))
+    algb = algorithmic_bytes(w, ev_local, count, a.precision, a.mode, occupancy=used.get("occupancy", 1.0),
+                             packed=used.get("variant") == 30)
+    alg = algb["hbm"]
     peaks = load_peaks()
     peak = peaks.get("hbm_gbs")
-    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (measured copy, burst)"
     if not peak:
         peak, peak_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
     achieved = alg / (k_ms / 1e3) / 1e9
-    trec = load_traffic(w, a.precision, used.get("variant")) if a.mode == "direct" else None
+    trec = load_traffic(w, a.precision, used.get("variant"), count) if a.mode == "direct" else None
     traffic = trec.get("dram_bytes_per_launch") if trec else None
+    l2pk = l2_gather_peak()
     ctx.close()
 
     # ---- end-to-end arm: host buffers through the C-ABI
     e2e = None
-    if not a.no_e2e:
+    def e2e_leg(fmt):
+        """The step through the C-ABI with pinned HOST buffers: ELT records + YET
+        (u32 ids, or the F3 packed transfer format) copied in chunks overlapped
+        with the kernel, YLT + metrics read back, all inside the timed region."""
         ylt_pin = torch.empty((L + 1) * T, dtype=torch.float64, pin_memory=True)
         ids_view = ids_pin[:n_ev]
         bits = ara.bits_for_catalog(w.catalog)
-        if a.e2e_format == "packed":   # host YET stored in the packed transfer format (setup, untimed)
+        pack_ms = None
+        if fmt == "packed":   # host YET stored in the packed transfer format (setup, untimed; timed once below)
             packed_pin = torch.empty(ara.ara_packed_words(n_ev, bits), dtype=torch.int32, pin_memory=True)
+            tp = time.perf_counter()
             ara.ara_pack_ids(ids_pin.numpy().view(np.uint32)[:n_ev], bits, packed_pin)
+            pack_ms = 1e3 * (time.perf_counter() - tp)
             ids_bytes = packed_pin.numel() * 4
         else:
             ids_bytes = n_ev * 4
@@ -505,14 +530,13 @@ def main():
                            nccl_id=new_nccl_id(), load_mode=a.e2e_mode, chunk_trials=a.chunk_trials,
                            l2_persist=a.l2_persist, run_mode=a.mode)
         h2d_ms = []
-
         wall = []
 
         def estep():
             t0 = time.perf_counter()
             ectx.load_elts(eo_pin, ev_pin, ls_pin, terms, n_elts=w.n_elts)
             t1 = time.perf_counter()
-            if a.e2e_format == "packed":
+            if fmt == "packed":
                 ectx.load_yet_packed(T, first, off_pin, packed_pin, bits)
             else:
                 ectx.load_yet(T, first, off_pin, ids_view)
@@ -531,21 +555,31 @@ def main():
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(a.steps):
-            s2 = estep()
+            estep()
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
         ems = max_over_ranks(e0.elapsed_time(e1)) / a.steps
         h2d = n_off * 8 + ids_bytes + (eo_pin.numel() * 8 + ev_pin.numel() * 4 + ls_pin.numel() * 8 if rank == 0 else 0)
         d2h = (L + 1) * T * 8 + 2 * (L + 1) * len(R) * 8 + 8
-        e2e = {"value": T / (ems / 1e3), "unit": "trials/s", "ms_per_step": ems, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": d2h, "mode": a.e2e_mode, "chunk_trials": a.chunk_trials,
-               "yet_format": a.e2e_format + (str(bits) if a.e2e_format == "packed" else ""),
-               "h2d_gbs": (ids_bytes + n_off * 8) / (float(np.mean(h2d_ms[-a.steps:])) / 1e3) / 1e9
-               if a.e2e_mode == "chunked" and np.mean(h2d_ms) > 0 else None,
-               "wall_ms": {k: 1e3 * float(np.median([x[i] for x in wall[-a.steps:]]))
-                           for i, k in enumerate(("load_elts", "load_yet", "run", "metrics"))}}
         ectx.close()
+        return {"value": T / (ems / 1e3), "unit": "trials/s", "ms_per_step": ems, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "mode": a.e2e_mode, "chunk_trials": a.chunk_trials,
+                "yet_format": fmt + (str(bits) if fmt == "packed" else ""),
+                "host_pack_ms_untimed": pack_ms,
+                "h2d_gbs": (ids_bytes + n_off * 8) / (float(np.mean(h2d_ms[-a.steps:])) / 1e3) / 1e9
+                if a.e2e_mode == "chunked" and np.mean(h2d_ms) > 0 else None,
+                "wall_ms": {k: 1e3 * float(np.median([x[i] for x in wall[-a.steps:]]))
+                            for i, k in enumerate(("load_elts", "load_yet", "run", "metrics"))}}
+
+    # ---- end-to-end arm: host buffers through the C-ABI.  The headline e2e is
+    # the plain u32 contract of ara_load_yet; e2e_packed is the same step with
+    # the host YET held in the 21-bit transfer format (F3)
+    e2e = e2e_packed = None
+    if not a.no_e2e:
+        e2e = e2e_leg("u32")
+        if a.e2e_format == "both":
+            e2e_packed = e2e_leg("packed")
 
     # ---- CPU baseline (oracle) on rank 0 at N = 1 only
     cpu = None
@@ -566,41 +600,45 @@ def main():
                        "n_events": n_events_global, "elts_per_layer": [Lr.elt_end - Lr.elt_begin for Lr in w.layers],
                        "catalog": w.catalog, "layers": L, "return_periods": len(R), "parallelism": f"trials/{world}",
                        "l2": "inputs larger than L2 (4 GB YET streamed once per step; 256 MB table)",
-                       "l2_persist": a.l2_persist, "mode": a.mode},
+                       "l2_persist": a.l2_persist, "mode": a.mode, "rho": w.rho,
+                       "occupied_fraction": used.get("occupancy")},
             "lookups_per_sec": lookups / (ms / 1e3),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic if a.mode == "direct" else None,
+                         "frac": achieved / peak, "traffic": traffic,
                          "kernel": kernel_name(used.get("variant", -1)),
-                         "table_occupancy": used.get("occupancy"),
-                         "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg, "peak_source": peak_src,
-                         # algorithmic bytes count every gathered row, including the ones L2
-                         # serves, so frac can exceed 1; the DRAM-level figure is traffic / time
-                         "dram_achieved": (traffic / (k_ms * 1e6)) if (traffic and a.mode == "direct") else None,
-                         "dram_frac": (traffic / (k_ms * 1e6) / peak) if (traffic and a.mode == "direct") else None,
+                         "kernel_ms": k_ms, "algorithmic_bytes_per_launch": alg,
+                         "algorithmic_bytes": {"yet": algb["yet"], "elt_sectors": algb["elt"],
+                                               "offsets_ylt": algb.get("per_trial", 0)},
+                         # one 4-B bitmap word per event: shared memory / L1 / L2, never HBM-streamed
+                         "index_bytes": algb["index"], "peak_source": peak_src,
+                         # from the committed ncu capture of the same kernel at the same launch
+                         # size (profiles/ara_kernel_traffic.json), else null
+                         "dram_achieved": (traffic / (k_ms * 1e6)) if traffic else None,
+                         "dram_frac": (traffic / (k_ms * 1e6) / peak) if traffic else None,
                          "l2_hit_rate_pct": trec.get("l2_hit_rate_pct") if trec else None,
                          "l2_sector_bytes": (32 * trec["l2_sectors_per_launch"]) if trec else None,
-                         # L2 -> SM sector traffic against the measured L2 gather ceiling
-                         # (profiles/r01_microbench.json: random 32-B gathers, L2-resident table)
-                         "l2_frac": (32 * trec["l2_sectors_per_launch"] / (k_ms * 1e6) / l2_gather_peak())
-                         if (trec and l2_gather_peak()) else None,
+                         "l2_peak_gbs": l2pk, "l2_peak_source": L2_PEAK_SOURCE + " (builder microbenchmark: "
+                                                                  "random 32-B gathers, L2-resident 16 MB table)",
+                         "l2_frac": (32 * trec["l2_sectors_per_launch"] / (k_ms * 1e6) / l2pk)
+                         if (trec and l2pk) else None,
                          "traffic_source": trec.get("source") if trec else None,
-                         # SURVEY 8(d) F_roof: the binding hardware roof is the larger of the DRAM
-                         # time (ncu DRAM bytes / HBM peak) and the L2 time (ncu L2 sector bytes /
-                         # measured L2 gather ceiling); hierarchical_frac = that time / kernel time
-                         "hierarchical_frac": (max(traffic / peak, 32 * trec["l2_sectors_per_launch"] / l2_gather_peak())
-                                               / 1e6 / k_ms) if (trec and l2_gather_peak()) else None,
-                         "note": ("algorithmic bytes = YET bytes + 32 B per gathered ELT sector (north star); "
-                                  "most gathered sectors are L2 hits (l2_hit_rate_pct), so achieved can exceed "
-                                  "the HBM peak; hierarchical_frac is the fraction of the binding roof")},
+                         # SURVEY 8(d) F_roof: the larger of the DRAM time (ncu DRAM bytes / HBM
+                         # peak) and the L2 time (ncu L2 sector bytes / L2 gather ceiling), over
+                         # the kernel time
+                         "hierarchical_frac": (max(traffic / peak, 32 * trec["l2_sectors_per_launch"] / l2pk)
+                                               / 1e6 / k_ms) if (trec and l2pk) else None,
+                         "note": ("frac = north-star bytes (YET ids + the 32-B ELT sectors actually gathered "
+                                  "+ offsets/YLT) / kernel time / HBM peak; occupancy probes are index_bytes, "
+                                  "not HBM bytes")},
             "breakdown_ms": {"ara_kernel": k_ms, "allgather": float(np.mean(ag_ms)), "metrics": float(np.mean(met_ms)),
                              "step": ms,
                              "calls": {k: float(np.median([p[i] for p in part_ms]))
                                        for i, k in enumerate(("load_elts", "load_yet", "run", "metrics"))}},
             # our kernels per timed step: load_elts = clear_rows (the table was densified
-            # before) + densify; ara_run = n_kernel_launches; ara_metrics = init + 8 radix
-            # passes + tail
-            "gpu_launches": int(a.steps * (2 + np.mean(launches) + 10)),
-            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
+            # before) + densify + pack_rows; ara_run = n_kernel_launches; ara_metrics =
+            # init + 8 radix passes + tail
+            "gpu_launches": int(a.steps * (3 + np.mean(launches) + 10)),
+            "e2e": e2e, "e2e_packed": e2e_packed, "cpu_baseline": cpu, "clocks": clk,
             "host": dict(host_info(), cpus_near_gpu=cpus_bound), "gen_seconds": gen_s,
         }
         emit(line)

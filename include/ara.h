@@ -31,8 +31,20 @@
  * Numerics: fp64 arithmetic, round-to-nearest, no FMA contraction on the
  * term path.  Per event the ELT losses are summed sequentially in the layer's
  * ELT order (so the lossy-occurrence counts are bit-exact against the paper's
- * sequential Alg. 3); per trial the occurrence-net losses are summed in a
- * fixed lane-strided + warp-tree order (deterministic, partition-invariant).
+ * sequential Alg. 3); per trial the occurrence-net losses are summed in an
+ * order fixed by the trial's own events -- lane-strided + warp tree in the
+ * dense kernels, the trial's occupied events dealt round-robin to the lanes +
+ * warp tree in the sparse kernel -- so results are deterministic and
+ * independent of sharding, chunking and alignment, and within the A21 bound
+ * (|dY| <= 1e-9 * sum of the trial's event losses) of the sequential sum.
+ *
+ * Deviations from the SURVEY.md 8(b) sketch (deliberate):
+ * lossy-occurrence counts are an ara_run OUTPUT ARGUMENT (host or device
+ * buffer, like the YLT) rather than a pointer inside ara_run_stats, so the
+ * stats struct is plain data; ara_metrics returns the ranks k[] (host, may be
+ * NULL) and the metrics kernels' device time instead of a `ranks` argument
+ * after the outputs.  ara_load_yet_packed, ara_set_elt_terms and
+ * ara_run_portfolio are additions (F3, P:197 re-pricing, F4).
  */
 #ifndef ARA_H
 #define ARA_H
@@ -75,7 +87,8 @@ typedef enum {
 typedef enum {
     ARA_RUN_DIRECT = 0,   /* per occurrence: gather the layer's row window and apply every term (Alg. 3 as written) */
     ARA_RUN_FOLD = 1      /* per run: fold the catalogue once (o(e) for every event id, P:373 per-occurrence
-                             independence), then gather one value per occurrence; bit-identical YLT */
+                             independence), then gather one value per occurrence; YLT bit-identical to the
+                             dense direct kernels (same lane order), within A21 of the sparse one */
 } ara_run_mode;
 
 typedef struct {
@@ -120,9 +133,10 @@ typedef struct {
     double total_ms;         /* whole ara_run on the stream, first enqueue to completion */
     uint64_t h2d_bytes;      /* bytes copied host->device inside this run */
     uint32_t n_kernel_launches;
-    int32_t kernel_variant;  /* trial kernel of the last direct launch: 21 compacted rounds over packed
-                                rows, packed across trials (sparse tables), 12 cooperative cp.async ring, 5/0 register
-                                pipeline, ... (ARA_KERNEL numbering); -2 = fold mode, -1 = none */
+    int32_t kernel_variant;  /* trial kernel of the last direct launch (ARA_KERNEL numbering): 30 ballot-
+                                compacted rounds over packed rows (sparse column blocks), 12 cooperative
+                                cp.async ring (dense fp64), 5 / 0 register pipeline (dense fp32, wide
+                                windows); -2 = fold mode, -1 = none */
     double occupancy;        /* fraction of row windows the last direct launch gathers: the occupied-row
                                 fraction of its column block when zero rows are skipped, else 1.0 */
 } ara_run_stats;
@@ -190,7 +204,10 @@ ara_status ara_set_elt_terms(ara_ctx* ctx, uint32_t n_elts, const ara_elt_terms*
  * HOST pointers: ALL_AT_ONCE copies them into library-owned HBM before
  * returning; CHUNKED keeps the pointers (they must stay valid, ideally pinned,
  * until the last ara_run that uses them) and streams them inside ara_run.
- * DEVICE pointers are borrowed without a copy and must stay valid likewise.
+ * DEVICE pointers are borrowed without a copy and must stay valid likewise;
+ * the sparse kernel streams them with 16-B aligned bulk copies, which may read
+ * up to 12 bytes before the first and after the last id inside the same
+ * 16-B-aligned block (never across a page boundary).
  * Offsets monotonicity and id ranges are validated inside the ARA kernel and
  * reported by ara_run (OUT_OF_RANGE).  Local call (not collective); ara_run
  * checks that the ranks' ranges tile [0, n_trials_global).

@@ -85,47 +85,6 @@ float ev_ms(cudaEvent_t a, cudaEvent_t b) {
     return ms;
 }
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_tiled() {
-    static EncodeTiledFn fn = nullptr;
-    static bool tried = false;
-    if (!tried) {
-        tried = true;
-        void* f = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = (EncodeTiledFn)f;
-        cudaGetLastError();
-    }
-    return fn;
-}
-
-// TMA map of one column block as a 2D tensor [C+1 rows][epb cols]; the box is
-// one row of `box_sec` sectors, swizzled so each lane's row read is
-// bank-conflict free (see trial_kernel_tma).
-bool make_block_map(const ara_ctx* ctx, uint32_t blk, uint32_t box_sec, CUtensorMap* map) {
-    EncodeTiledFn enc = encode_tiled();
-    if (!enc) return false;
-    const TableGeo& g = ctx->geo;
-    const uint32_t eps = kSectorBytes / g.esz;
-    cuuint64_t dims[2] = {g.epb, (cuuint64_t)ctx->catalog + 1};
-    cuuint64_t strides[1] = {(cuuint64_t)g.epb * g.esz};
-    cuuint32_t box[2] = {box_sec * eps, 1};
-    cuuint32_t est[2] = {1, 1};
-    const uint32_t rowb = box_sec * kSectorBytes;
-    CUtensorMapSwizzle sw = rowb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                            : rowb == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                         : CU_TENSOR_MAP_SWIZZLE_32B;
-    void* base = static_cast<char*>(ctx->d_table) + (size_t)blk * g.block_elems * g.esz;
-    return enc(map, g.esz == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, base, dims,
-               strides, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 void release_yet(ara_ctx* ctx) {
     if (ctx->h_registered) {
         cudaHostUnregister(ctx->h_registered);
@@ -229,11 +188,18 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
     ctx->catalog = catalog_size;
     if (const char* v = getenv("ARA_GRID_MULT")) ctx->grid_mult = atof(v);
     if (const char* v = getenv("ARA_KERNEL")) ctx->kernel_variant = atoi(v);
-    if (const char* v = getenv("ARA_PFN")) ctx->pf_sectors = atoi(v);
     if (const char* v = getenv("ARA_NO_SKIP")) ctx->no_skip = atoi(v) != 0;
     if (const char* v = getenv("ARA_NO_P2P")) ctx->use_p2p = atoi(v) == 0;
     if (const char* v = getenv("ARA_METRICS_DIST")) ctx->metrics_dist = atoi(v);
-    if (const char* v = getenv("ARA_BATCH")) ctx->batch = (uint32_t)atoi(v) ? (uint32_t)atoi(v) : 4u;
+    if (const char* v = getenv("ARA_LOOPBACK")) {
+        int w = 0, r = 0;
+        if (cfg->world != 1 || sscanf(v, "%d,%d", &w, &r) != 2 || w < 1 || w > ara::kMaxPeers || r < 0 || r >= w) {
+            delete ctx;
+            return ARA_ERR_INVALID_ARG;
+        }
+        ctx->lb_world = w;
+        ctx->lb_rank = r;
+    }
     auto bail = [&](ara_status st) {
         ara_destroy(ctx);
         return st;
@@ -250,11 +216,6 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
         ctx->own_stream = true;
     }
     if (cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking) != cudaSuccess) return bail(ARA_ERR_CUDA);
-    if (cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking) != cudaSuccess) return bail(ARA_ERR_CUDA);
-    if (cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess)
-        return bail(ARA_ERR_CUDA);
-    if (cudaMalloc(&ctx->d_work, sizeof(unsigned long long)) != cudaSuccess) return bail(ARA_ERR_OOM);
     for (auto& e : ctx->ev)
         if (cudaEventCreate(&e) != cudaSuccess) return bail(ARA_ERR_CUDA);
     if (cudaMalloc(&ctx->d_err, 64) != cudaSuccess) return bail(ARA_ERR_OOM);
@@ -299,8 +260,6 @@ extern "C" void ara_destroy(ara_ctx* ctx) {
     cudaFree(ctx->d_ylt_global);
     cudaFree(ctx->d_lossy);
     cudaFree(ctx->d_fold);
-    cudaFree(ctx->d_occ4);
-    cudaFree(ctx->d_bm_union);
     cudaFree(ctx->d_sp_off);
     cudaFree(ctx->d_sp_ev);
     cudaFree(ctx->d_sp_ls);
@@ -311,10 +270,6 @@ extern "C" void ara_destroy(ara_ctx* ctx) {
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
-    if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
-    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
-    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
-    cudaFree(ctx->d_work);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
     cudaGetLastError();
     delete ctx;
@@ -462,23 +417,27 @@ extern "C" ara_status ara_load_elts(ara_ctx* ctx, uint32_t n_elts, const uint64_
     uint64_t nrec = (st == ARA_OK && root) ? hoff[n_elts] : 0;
     SparseDev sp;
     if (ctx->world > 1) {
-        // Agree on (status, n_elts, records) first so a failing root cannot
-        // strand the others; then rank 0's sparse records (a few MB) go over
-        // NVLink and every rank densifies locally — instead of N host copies
-        // of the replicated data or a broadcast of the
-        // whole table.
+        // Agree on (status, n_elts, records) first so that no failing rank
+        // can strand the others in the broadcasts below: one max-all-reduce of
+        // [status, n_elts, ~n_elts, records] gives every rank the worst
+        // status, whether all n_elts agree (max == min), and rank 0's record
+        // count (the others contribute 0).  Then rank 0's sparse records (a
+        // few MB) go over NVLink and every rank densifies locally — instead of
+        // N host copies of the replicated data or a
+        // broadcast of the whole table.
         ctx->h_small[0] = (uint64_t)st;
         ctx->h_small[1] = n_elts;
-        ctx->h_small[2] = nrec;
-        CK(cudaMemcpyAsync(ctx->d_small, ctx->h_small, 3 * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
-        NK(ncclBroadcast(ctx->d_small, ctx->d_small, 3, ncclUint64, 0, ctx->comm, ctx->stream));
-        CK(cudaMemcpyAsync(ctx->h_small + 8, ctx->d_small, 3 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx->h_small[2] = ~(uint64_t)n_elts;
+        ctx->h_small[3] = root ? nrec : 0;
+        CK(cudaMemcpyAsync(ctx->d_small, ctx->h_small, 4 * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+        NK(ncclAllReduce(ctx->d_small, ctx->d_small, 4, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_small + 8, ctx->d_small, 4 * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         const ara_status rst = (ara_status)ctx->h_small[8];
-        if (rst != ARA_OK) return root ? st : fail(ctx, rst, "rank 0 rejected the ELTs");
-        if (ctx->h_small[9] != n_elts) return fail(ctx, ARA_ERR_INVALID_ARG, "n_elts differs from rank 0");
-        if (st != ARA_OK) return st;   // non-root terms invalid (checked locally)
-        nrec = ctx->h_small[10];
+        if (rst != ARA_OK) return st != ARA_OK ? st : fail(ctx, rst, "another rank rejected the ELTs");
+        if (ctx->h_small[9] != ~ctx->h_small[10])
+            return fail(ctx, ARA_ERR_INVALID_ARG, "ranks disagree on n_elts");
+        nrec = ctx->h_small[11];
         ara_status s2 = stage_sparse(ctx, n_elts, nrec, root ? hoff.data() : nullptr, elt_offsets, event_ids, losses,
                                      /*to_staging=*/true, &sp);
         if (s2 != ARA_OK) return s2;
@@ -495,6 +454,10 @@ extern "C" ara_status ara_load_elts(ara_ctx* ctx, uint32_t n_elts, const uint64_
                                      /*to_staging=*/false, &sp);
         if (s2 != ARA_OK) return s2;
     }
+    // From here the table changes: until this load succeeds there are no
+    // usable ELTs (ara_run -> STATE) and no run whose metrics could be read.
+    ctx->n_elts = 0;
+    ctx->last_layers = 0;
     st = densify_local(ctx, n_elts, nrec, sp);   // every rank sees the same records: same verdict
     if (st != ARA_OK) return st;
     ctx->n_elts = n_elts;
@@ -851,7 +814,13 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     const uint64_t T_local = ctx->T_local, T_global = ctx->T_global;
 
     // Ranks must hold ara_partition's split (checked once per load, collective).
-    if (world == 1 && (ctx->first != 0 || T_local != T_global))
+    if (ctx->lb_world) {
+        uint64_t f = 0, c = 0;
+        ara_partition(T_global, ctx->lb_world, ctx->lb_rank, &f, &c);
+        if (f != ctx->first || c != T_local)
+            return fail(ctx, ARA_ERR_INVALID_ARG, "loopback: the YET must be ara_partition(%llu, %d)[%d]",
+                        (unsigned long long)T_global, ctx->lb_world, ctx->lb_rank);
+    } else if (world == 1 && (ctx->first != 0 || T_local != T_global))
         return fail(ctx, ARA_ERR_INVALID_ARG, "a single-rank context must load the whole YET (first 0, %llu trials)",
                     (unsigned long long)T_global);
     if (world > 1 && !ctx->tiling_checked) {
@@ -982,44 +951,40 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     // Kernels.
     const TableGeo& geo = ctx->geo;
     const uint32_t spb = geo.epb / eps;   // sectors per block row
-    // Multi-window compacted rounds: 2-4 disjoint single-layer windows of equal
-    // width, each inside one sparse column block, scanned by ONE launch (one id
-    // stream and one combined occupancy word per event instead of one launch
-    // per layer re-reading the YET).
-    bool multiwin = false;
-    {
-        const TableGeo& g0 = ctx->geo;
-        const uint32_t spb0 = g0.epb / eps;
-        // opt-in (ARA_KERNEL=15): measured slower than one launch per layer on the
-        // 4-layer config (33.1 vs 32.0 ms): the per-window FIFOs must be 2 deep
-        // to fit the registers, which raises the round count, and the four
-        // blocks' occupied rows (152 MB) no longer fit in L2
-        multiwin = !fold && n_programs == 0 && groups.size() >= 2 && groups.size() <= (size_t)kMaxLB &&
-                   ctx->kernel_variant == 15 && !ctx->no_skip;
-        for (size_t gi = 0; gi < groups.size() && multiwin; ++gi) {
-            const Group& g = groups[gi];
-            const uint32_t blk = g.q0 / spb0;
-            multiwin = g.nl == 1 && !g.wide && g.nsec == groups[0].nsec && g.nsec <= 4 && (g.q0 % spb0) + g.nsec <= spb0 &&
-                       blk < ctx->occ_rows.size() && 2ull * ctx->occ_rows[blk] <= (uint64_t)ctx->catalog + 1;
-        }
-    }
     // Fused YLT assembly: one launch group per chunk (no wide layers, no
     // programs, one fold chunk) with a kernel whose epilogue stores to peers.
-    bool p2p_ok_kernel = ctx->kernel_variant < 0 || ctx->kernel_variant == 0 || ctx->kernel_variant == 5 ||
-                         ctx->kernel_variant == 12 || ctx->kernel_variant == 14 || ctx->kernel_variant == 15 ||
-                         (ctx->kernel_variant >= 16 && ctx->kernel_variant <= 21);
-    bool single_group = (groups.size() == 1 || multiwin) && !groups[0].wide && n_programs == 0 &&
+    bool p2p_ok_kernel = true;   // every trial kernel has the peer-store epilogue
+    bool single_group = groups.size() == 1 && !groups[0].wide && n_programs == 0 &&
                         (!fold || (n_layers + nlc - 1) / nlc == 1) && world <= (uint32_t)kMaxPeers;
     bool use_p2p = false;
     if (world > 1 && ctx->use_p2p && p2p_ok_kernel && single_group) {
         st = p2p_ensure(ctx, (size_t)rows * T_global);
         if (st != ARA_OK) return st;
         use_p2p = ctx->p2p_state > 0;
+    } else if (ctx->lb_world) {
+        if (!p2p_ok_kernel || !single_group)
+            return fail(ctx, ARA_ERR_INVALID_ARG, "loopback: needs a single-launch run with a peer-store kernel");
+        // the two global-YLT buffers are local; bytes 0xff (NaN) wherever no store lands
+        const size_t need = (size_t)rows * T_global;
+        if (ctx->p2p_cap < need) {
+            for (int b = 0; b < 2; ++b) {
+                cudaFree(ctx->d_p2p[b]);
+                ctx->d_p2p[b] = nullptr;
+            }
+            ctx->p2p_cap = 0;
+            for (int b = 0; b < 2; ++b) {
+                CK(cudaMalloc(&ctx->d_p2p[b], need * sizeof(double)));
+                CK(cudaMemsetAsync(ctx->d_p2p[b], 0xff, need * sizeof(double), ctx->stream));
+                ctx->peer_p2p[b][0] = ctx->d_p2p[b];
+            }
+            ctx->p2p_cap = need;
+        }
+        use_p2p = true;
     }
     const int p2p_buf = ctx->p2p_next;
     TrialParams base{};
     if (use_p2p) {
-        base.n_peers = world;
+        base.n_peers = world;   // loopback: 1, the local buffer
         for (uint32_t r = 0; r < world; ++r) base.peer_ylt[r] = ctx->peer_p2p[p2p_buf][r];
         base.peer_ld = T_global;
         base.peer_t0 = ctx->first;
@@ -1034,7 +999,6 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     base.ld = ld;
     base.lossy = d_lossy;
     base.err = ctx->d_err;
-    base.pf_sectors = ctx->pf_sectors;
     base.portfolio_row = n_layers + n_programs;
     uint32_t launches = 0;
     int used_variant = fold ? -2 : -1;
@@ -1078,45 +1042,9 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
             }
         }
     };
-    if (multiwin) {   // the windows' combined occupancy map (4 bits per event)
-        const size_t words = ((size_t)ctx->catalog + 1 + 7) / 8;
-        st = ensure(ctx, ctx->d_occ4, ctx->occ4_cap, words);
-        if (st != ARA_OK) return st;
-        uint32_t blk[kMaxLB] = {};
-        for (size_t gi = 0; gi < groups.size(); ++gi) blk[gi] = groups[gi].q0 / spb;
-        CK(launch_occ4(reinterpret_cast<const uint32_t*>(static_cast<const char*>(ctx->d_table) + geo.bm_off),
-                       geo.bm_words, blk, (uint32_t)groups.size(), ctx->catalog, ctx->d_occ4, s));
-    }
     const uint32_t n_chunks_fold = (n_layers + nlc - 1) / nlc;
     const uint64_t fold_rows = (uint64_t)ctx->catalog + 1;
     CK(cudaEventRecord(ctx->ev[1], s));
-    // fold mode: per fold chunk, the union occupancy bitmap of its layers'
-    // column blocks (an event outside it has an all-+0 fold row), or null when
-    // some block is dense
-    std::vector<const uint32_t*> fold_bm(n_chunks_fold, nullptr);
-    if (fold && !ctx->no_skip) {
-        const uint32_t* bms = reinterpret_cast<const uint32_t*>(static_cast<const char*>(ctx->d_table) + geo.bm_off);
-        std::vector<std::vector<uint32_t>> blks(n_chunks_fold);
-        bool ok = true;
-        for (uint32_t l = 0; l < n_layers && ok; ++l) {
-            const uint32_t q0 = layers[l].elt_begin / eps, q1 = (layers[l].elt_end + eps - 1) / eps;
-            for (uint32_t b = q0 / spb; b <= (q1 - 1) / spb; ++b) {
-                if (b >= ctx->occ_rows.size() || 2ull * ctx->occ_rows[b] > (uint64_t)ctx->catalog + 1) ok = false;
-                auto& v = blks[l / nlc];
-                if (std::find(v.begin(), v.end(), b) == v.end()) v.push_back(b);
-            }
-        }
-        for (uint32_t fc = 0; fc < n_chunks_fold && ok; ++fc) {
-            if (blks[fc].size() == 1) { fold_bm[fc] = bms + (uint64_t)blks[fc][0] * geo.bm_words; continue; }
-            if (blks[fc].empty() || blks[fc].size() > 8) continue;
-            st = ensure(ctx, ctx->d_bm_union, ctx->bm_union_cap, (size_t)n_chunks_fold * geo.bm_words);
-            if (st != ARA_OK) return st;
-            uint32_t* u = ctx->d_bm_union + (uint64_t)fc * geo.bm_words;
-            CK(launch_bm_union(bms, geo.bm_words, blks[fc].data(), (uint32_t)blks[fc].size(), u, s));
-            fold_bm[fc] = u;
-        }
-        if (!ok) std::fill(fold_bm.begin(), fold_bm.end(), nullptr);
-    }
     if (fold) {
         // a0': fold the catalogue once per run (all layers), bit-identical per-event values
         st = ensure(ctx, ctx->d_fold, ctx->fold_cap, (size_t)n_chunks_fold * fold_rows * nlc);
@@ -1143,7 +1071,6 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 TrialParams p = base;
                 p.t_begin = chunks[c].first;
                 p.t_end = chunks[c].second;
-                p.bm = fold_bm[fc];
                 p.n_layers = (n_layers - fc * nlc) < nlc ? (n_layers - fc * nlc) : nlc;
                 p.ylt_row0 = fc * nlc;
                 p.portfolio_mode = fc == 0 ? 0 : 1;
@@ -1156,38 +1083,6 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 CK(launch_trials_folded(p, (int)(100 * ctx->grid_mult), s));
                 ++launches;
             }
-            continue;
-        }
-        if (multiwin) {
-            TrialParams p = base;
-            p.t_begin = chunks[c].first;
-            p.t_end = chunks[c].second;
-            p.n_layers = (uint32_t)groups.size();
-            p.ylt_row0 = 0;
-            p.portfolio_mode = 0;
-            double occ_sum = 0.0;
-            for (uint32_t u = 0; u < p.n_layers; ++u) {
-                const Group& g = groups[u];
-                const LayerI& L = layers[g.l0];
-                p.lw[u] = {L.occ_retention, L.occ_limit, L.agg_retention, L.agg_limit};
-                p.win0[u] = (uint64_t)(g.q0 / spb) * geo.block_elems + (uint64_t)(g.q0 % spb) * eps;
-                for (uint32_t w = 0; w < (uint32_t)kMaxWin; ++w) {
-                    const uint32_t col = g.q0 * eps + w;
-                    if (w / eps < g.nsec && L.member(col))
-                        p.term[u][w] = make_double2(ctx->terms[col].deductible, ctx->terms[col].limit);
-                    else
-                        p.term[u][w] = make_double2(INFINITY, INFINITY);   // contributes exactly +0
-                }
-                occ_sum += (double)ctx->occ_rows[g.q0 / spb] / ((double)ctx->catalog + 1.0);
-            }
-            for (uint32_t sct = 0; sct < (uint32_t)kMaxSec; ++sct)
-                p.sec_off[sct] = p.win0[0] + (uint64_t)(sct < groups[0].nsec ? sct : 0) * eps;
-            p.bm = ctx->d_occ4;
-            used_variant = 15;
-            used_occupancy = occ_sum / p.n_layers;
-            const int grid = (int)(trial_kernel_grid(fp32, groups[0].nsec, 4, 15) * ctx->grid_mult);
-            CK(launch_trials(p, fp32, groups[0].nsec, grid > 0 ? grid : 1, 15, s));
-            ++launches;
             continue;
         }
         for (size_t gi = 0; gi < groups.size(); ++gi) {
@@ -1223,56 +1118,21 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 CK(launch_trials_wide(p, fp32, d_wc, d_wt, (uint32_t)wcols.size(), grid, s));
             } else {
                 setup_window(g, p);
-                // Kernel choice (measured, profiles/r01_kernel_variants.md): windows over a
-                // sparse column block (occupancy bitmap set) use the compacted-rounds kernel over
-                // packed rows with rounds packed across trials (21); dense fp64 windows of <= 4 sectors the cooperative cp.async ring at
-                // 3 CTAs/SM (12); dense fp32 windows the register-pipelined LDG kernel at
-                // 3 CTAs/SM (5) for single layers, 2 CTAs/SM (0) for shared-window towers.
-                // The other variants stay ARA_KERNEL-selectable for A/B runs.
+                // Kernel choice (measured): windows over a sparse
+                // column block (occupancy bitmap + packed rows set) use the
+                // ballot-compacted rounds kernel (30); dense fp64 windows of <= 4
+                // sectors the cooperative cp.async ring (12); other dense windows the
+                // register pipeline at 3 CTAs/SM (5) for single layers, 2 CTAs/SM
+                // (0) for shared-window towers.  ARA_KERNEL forces one (A/B runs).
                 int variant = ctx->kernel_variant;
-                if (variant == 15) variant = 14;   // multi-window only for multi-window runs (above)
-                if (variant < 0 && p.bm) variant = 21;   // compacted rounds over the packed rows, across trials
-                if (variant >= 17 && variant <= 21 && !p.pk) variant = 16;
-                if (p.bm) {   // rows actually gathered: the occupied fraction of the block
-                    const uint32_t blk = g.q0 / spb;
-                    used_occupancy = (double)ctx->occ_rows[blk] / ((double)ctx->catalog + 1.0);
-                } else {
-                    used_occupancy = 1.0;
-                }
-                const uint32_t box_sec = g.nsec <= 1 ? 1 : (g.nsec <= 2 ? 2 : 4);
-                const bool tma_ok = g.nsec <= 4 && (g.q0 % spb) + g.nsec <= spb && encode_tiled() != nullptr;
+                if (variant == 30 && !p.bm) variant = -1;   // bc needs the bitmap and packed rows
+                if (variant < 0 && p.bm) variant = 30;
+                if (variant != 30) p.bm = nullptr, p.pk = nullptr;   // the dense kernels read every row
+                used_occupancy = p.bm ? (double)ctx->occ_rows[g.q0 / spb] / ((double)ctx->catalog + 1.0) : 1.0;
                 if (variant < 0) variant = (!fp32 && g.nsec <= 4) ? 12 : (g.nl == 1 ? 5 : 0);
-                if ((variant == 8 || variant == 9) && !tma_ok) variant = g.nl == 1 ? 5 : 0;
-                if (variant == 8 || variant == 9) {
-                    if (!make_block_map(ctx, g.q0 / spb, box_sec, &p.tmap))
-                        return fail(ctx, ARA_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-                    p.tma_col = (g.q0 % spb) * eps;
-                }
                 used_variant = variant;
-                if (variant == 9) {
-                    // Hybrid: the register-pipelined LDG kernel (2 CTAs/SM) and the TMA
-                    // gather4 kernel (1 CTA/SM, shared-memory ring) run side by side on two
-                    // streams, co-resident on every SM (registers + shared memory both hold
-                    // rows in flight), claiming trial batches from one counter.
-                    p.work_ctr = ctx->d_work;
-                    p.batch = ctx->batch;
-                    CK(cudaMemsetAsync(ctx->d_work, 0, sizeof(unsigned long long), s));
-                    CK(cudaEventRecord(ctx->ev_fork, s));
-                    CK(cudaStreamWaitEvent(ctx->aux_stream, ctx->ev_fork, 0));
-                    // TMA kernel first (1 CTA/SM, ~213 KB smem); the LDG kernel asks for the
-                    // max-shared carveout so its CTAs do not force the SM into an L1-heavy
-                    // split that would keep the TMA CTA out.
-                    CK(launch_trials(p, fp32, g.nsec, ctx->n_sm, 8, ctx->aux_stream));
-                    set_ldg_carveout(fp32, g.nsec, (int)g.nl, 100);
-                    CK(launch_trials(p, fp32, g.nsec, 2 * ctx->n_sm, 5, s));
-                    set_ldg_carveout(fp32, g.nsec, (int)g.nl, -1);
-                    CK(cudaEventRecord(ctx->ev_join, ctx->aux_stream));
-                    CK(cudaStreamWaitEvent(s, ctx->ev_join, 0));
-                    p.work_ctr = nullptr;
-                } else {
-                    const int grid = (int)(trial_kernel_grid(fp32, g.nsec, (int)g.nl, variant) * ctx->grid_mult);
-                    CK(launch_trials(p, fp32, g.nsec, grid > 0 ? grid : 1, variant, s));
-                }
+                const int grid = (int)(trial_kernel_grid(fp32, g.nsec, (int)g.nl, variant) * ctx->grid_mult);
+                CK(launch_trials(p, fp32, g.nsec, grid > 0 ? grid : 1, variant, s));
             }
             ++launches;
         }
@@ -1367,6 +1227,8 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     ctx->last_rows = rows;
     ctx->d_last_full = d_full;
     ctx->last_ld_local = ld;
+    ctx->run_T_global = T_global;
+    ctx->run_T_local = T_local;
     if (use_p2p) ctx->p2p_next ^= 1;
     if (stats) {
         const uint64_t nev = T_local ? ctx->h_small[2] - ctx->h_small[1] : 0;
@@ -1397,7 +1259,9 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
     if (ctx->last_layers == 0) return fail(ctx, ARA_ERR_STATE, "no successful ara_run yet");
     if (n_rp == 0 || n_rp > ARA_MAX_RP || !return_periods || !pml || !tvar)
         return fail(ctx, ARA_ERR_INVALID_ARG, "n_rp must be in [1, %d] with non-NULL arrays", ARA_MAX_RP);
-    const uint64_t T = ctx->T_global;
+    // the last run's YET (a later ara_load_yet does not change it); loopback:
+    // the shard, as if it were the whole YLT
+    const uint64_t T = ctx->lb_world ? ctx->run_T_local : ctx->run_T_global;
     uint64_t hk[ARA_MAX_RP];
     for (uint32_t r = 0; r < n_rp; ++r)
         if (ara_return_period_rank(T, return_periods[r], &hk[r]) != ARA_OK)
@@ -1411,7 +1275,7 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
         ld = T;
     } else {
         d_y = ctx->d_ylt_local;
-        ld = ctx->T_local ? ctx->T_local : 1;
+        ld = ctx->last_ld_local;
     }
     int nblk = (int)((T + 4095) / 4096);
     static const int blk_mult = [] { const char* v = getenv("ARA_METRICS_BLOCKS"); return v ? atoi(v) : 2; }();
@@ -1424,14 +1288,16 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
     // Distributed select (F4) on large global YLTs: every rank histograms only
     // its own shard and the histograms are all-reduced, instead of every rank
     // sweeping the whole global YLT (which grows with N under weak scaling).
-    const bool dist = ctx->world > 1 && (ctx->metrics_dist > 0 || (ctx->metrics_dist < 0 && T >= 3000000));
+    // (world 1 with ARA_METRICS_DIST=1 or loopback: the same passes with an identity reduce)
+    const bool dist = ctx->lb_world > 0 || ctx->metrics_dist > 0 ||
+                      (ctx->world > 1 && ctx->metrics_dist < 0 && T >= 3000000);
     if (dist) {
         int nerr = 0;
-        const uint64_t Tl = ctx->T_local;
+        const uint64_t Tl = ctx->run_T_local;
         int nb = (int)((Tl + 4095) / 4096);
         if (nb > maxblk) nb = maxblk;
         if (nb < 1) nb = 1;
-        CK(launch_metrics_dist(ctx->d_ylt_local, Tl, ctx->last_ld_local ? ctx->last_ld_local : 1, rows, n_rp, hk,
+        CK(launch_metrics_dist(ctx->d_ylt_local, Tl, ctx->last_ld_local, rows, n_rp, hk,
                                ctx->ms, nb, ctx->comm, s, &nerr));
         if (nerr) return fail(ctx, ARA_ERR_NCCL, "NCCL all-reduce in the distributed metrics failed");
     } else {

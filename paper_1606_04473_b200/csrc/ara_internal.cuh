@@ -86,15 +86,13 @@ struct LayerWin {
 // columns outside a layer carry deductible +inf, so they contribute an exact
 // +0 and need no predicate.  Passed by value (constant bank).
 struct TrialParams {
-    CUtensorMap tmap;           // TMA variant: the window's column block as a 2D [C+1][epb] tensor
-    uint32_t tma_col;           // TMA variant: first window column inside the block
     const uint64_t* off;        // local CSR offsets [n_local + 1]
     const uint32_t* ids;        // events of off[0] ...
     uint64_t t_begin, t_end;    // trial range of this launch (local indices)
     uint32_t catalog;
     uint32_t n_layers;          // layers in this launch (<= kMaxLB)
     const void* table;          // column-blocked direct-access table (+ pad)
-    const uint32_t* bm;         // row-occupancy bitmap of the window's column block, or null (no skipping)
+    const uint32_t* bm;         // row-occupancy bitmap of the window's (sparse) column block, or null
     uint64_t row_stride;        // elements per block row (= epb)
     uint64_t block_stride;      // elements per column block (= (C+1) * epb)
     uint64_t sec_off[kMaxSec];  // window sector offsets (elements, event 0)
@@ -105,9 +103,6 @@ struct TrialParams {
     uint32_t portfolio_row;
     uint32_t* lossy;            // [.. rows][ld] or null
     uint32_t* err;              // device error word
-    int pf_sectors;             // sectors per prefetched window (prefetching kernels)
-    unsigned long long* work_ctr;   // dynamic trial batches (hybrid launches), or null = static stride
-    uint32_t batch;             // trials per dynamic claim
     double* fold;               // fold mode: per-event occurrence-net losses, [C+1][fold_stride] per chunk
     uint32_t fold_stride;       // doubles per fold row (layers of one chunk, power of two <= 8)
     uint32_t fold_col0;         // fold column of the launch's first layer
@@ -117,10 +112,6 @@ struct TrialParams {
     // mapped into this process (CUDA IPC over NVLink); 0 peers = not used
     double* peer_ylt[kMaxPeers];
     uint32_t n_peers;
-    // multi-window compacted rounds (disjoint layers, one launch): element
-    // offset of layer u's window (event 0); bm then points at the combined
-    // 4-bit-per-event occupancy map of the windows' column blocks
-    uint64_t win0[kMaxLB];
     // packed rows of the window's (sparse) column block, or null: slot e holds
     // row e's non-zero mask over the block's columns, e, and its first
     // 24 / esz non-zero values in column order; the window is block columns
@@ -129,6 +120,7 @@ struct TrialParams {
     uint32_t pk_col0, pk_wmask;
     uint64_t peer_ld;           // = T_global
     uint64_t peer_t0;           // global index of local trial 0 (this rank's first trial)
+    uint32_t bm_smem_words;     // trial_kernel_bc: leading bitmap words staged in shared memory (set by the launcher)
 };
 
 // ---- launchers (defined in the .cu files; all enqueue on `s`)
@@ -136,19 +128,14 @@ cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const d
                            uint32_t n_elts, uint64_t n_records, uint32_t catalog, void* d_table,
                            const TableGeo& geo, int fp32, uint32_t* d_err, cudaStream_t s);
 
-// combined occupancy of up to 4 column blocks: 4 bits per event (bit u = block blk[u])
-cudaError_t launch_occ4(const uint32_t* bitmaps, uint64_t bm_words, const uint32_t* blk, uint32_t n_win,
-                        uint32_t catalog, uint32_t* occ4, cudaStream_t s);
-// OR of up to 8 column blocks' occupancy bitmaps
-cudaError_t launch_bm_union(const uint32_t* bitmaps, uint64_t bm_words, const uint32_t* blk, uint32_t nb,
-                            uint32_t* out, cudaStream_t s);
 // packed rows (TrialParams::pk) of every sparse column block (<= half its rows occupied)
 cudaError_t launch_pack_rows(void* d_table, const TableGeo& geo, uint32_t catalog, int fp32, cudaStream_t s);
 // zero exactly the rows the occupancy bitmaps mark, then the bitmaps and counters
 cudaError_t launch_clear_rows(void* d_table, const TableGeo& geo, uint32_t catalog, cudaStream_t s);
 cudaError_t launch_trials(const TrialParams& p, int fp32, uint32_t max_nsec, int grid, int variant, cudaStream_t s);
+// trial_kernel_bc (kernel_sparse.cu): needs p.bm and p.pk; grid = one CTA per SM
+cudaError_t launch_trials_bc(const TrialParams& p, int fp32, int grid, cudaStream_t s);
 int trial_kernel_grid(int fp32, uint32_t max_nsec, int n_layers, int variant);
-void set_ldg_carveout(int fp32, uint32_t nsec, int nl, int pct);
 cudaError_t launch_fold(const TrialParams& p, int fp32, uint32_t nsec, cudaStream_t s);
 cudaError_t launch_unpack(const uint32_t* packed, uint32_t bits, uint64_t e0, uint64_t e1, uint32_t* ids,
                           cudaStream_t s);
@@ -195,10 +182,7 @@ struct ara_ctx {
     ara_load_mode load_mode = ARA_LOAD_ALL_AT_ONCE;
     uint64_t chunk_trials = 65536;
     int l2_persist = 0;
-    cudaStream_t stream = nullptr, copy_stream = nullptr, aux_stream = nullptr;
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-    unsigned long long* d_work = nullptr;   // dynamic trial counter (hybrid launches)
-    uint32_t batch = 4;                     // ARA_BATCH
+    cudaStream_t stream = nullptr, copy_stream = nullptr;
     bool own_stream = false;
     ncclComm_t comm = nullptr;
     int n_sm = 148;
@@ -264,19 +248,22 @@ struct ara_ctx {
     int p2p_next = 0;                 // buffer of the next run
     bool use_p2p = true;              // ARA_NO_P2P=1: assemble the YLT with ncclAllGather instead
     const double* d_last_full = nullptr;   // global YLT of the last run (metrics input)
-    uint64_t last_ld_local = 0;       // row stride of d_ylt_local in the last run
+    uint64_t last_ld_local = 1;       // row stride of d_ylt_local in the last run
+    uint64_t run_T_global = 0;        // trials of the last run (global / this rank's): ara_metrics reads
+    uint64_t run_T_local = 0;         //   the last run's YLT, whatever ara_load_yet happened since
     int metrics_dist = -1;            // ARA_METRICS_DIST: -1 auto (distributed when T >= 3M), 0 off, 1 on
-    uint32_t* d_occ4 = nullptr;       // combined occupancy map of a multi-window launch
-    size_t occ4_cap = 0;
-    uint32_t* d_bm_union = nullptr;   // fold mode: union occupancy of each fold chunk's blocks
-    size_t bm_union_cap = 0;
+    // ARA_LOOPBACK="W,r" (test knob, world == 1): this context holds rank r's
+    // ara_partition shard of a W-rank job and runs the fused peer-store
+    // epilogue into a local global-YLT buffer (peer_t0 = first trial,
+    // peer_ld = T_global), so a9's indexing runs on one GPU; its metrics are
+    // the distributed select over the shard with an identity reduce
+    int lb_world = 0, lb_rank = 0;
     int run_mode = 0;                  // ARA_RUN_DIRECT / ARA_RUN_FOLD
     double* d_fold = nullptr;          // fold mode: per-event occurrence-net losses
     size_t fold_cap = 0;
     // tuning knobs (environment, read at ara_create; not part of the ABI)
     double grid_mult = 1.0;           // ARA_GRID_MULT
     int kernel_variant = -1;          // ARA_KERNEL (-1 auto; see pick_kernel in ara_kernel.cu)
-    int pf_sectors = 1;               // ARA_PFN
     bool no_skip = false;             // ARA_NO_SKIP=1: never skip zero rows via the occupancy bitmap (A/B)
     std::vector<uint32_t> occ_rows;   // occupied rows per column block (from densify)
     bool table_clean = false;         // table content is exactly described by its occupancy bitmaps

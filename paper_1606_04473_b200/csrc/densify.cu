@@ -168,61 +168,6 @@ cudaError_t launch_unpack(const uint32_t* packed, uint32_t bits, uint64_t e0, ui
     return cudaGetLastError();
 }
 
-// occ4[e / 8] bits 4 (e % 8) + u = bit e of bitmap blk[u]
-__global__ void __launch_bounds__(256) occ4_kernel(const uint32_t* __restrict__ bitmaps, uint64_t bm_words,
-                                                   uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3, uint32_t n_win,
-                                                   uint64_t n_words, uint32_t* __restrict__ occ4) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_words;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t e0 = i * 8;   // events e0 .. e0 + 7
-        uint32_t out = 0;
-        const uint32_t blk[4] = {b0, b1, b2, b3};
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if ((uint32_t)u >= n_win) break;
-            const uint32_t w = bitmaps[(uint64_t)blk[u] * bm_words + (e0 >> 5)];
-            const uint32_t byte = (w >> (e0 & 31)) & 0xffu;   // bits of events e0 .. e0 + 7
-#pragma unroll
-            for (int k = 0; k < 8; ++k) out |= ((byte >> k) & 1u) << (4 * k + u);
-        }
-        occ4[i] = out;
-    }
-}
-
-cudaError_t launch_occ4(const uint32_t* bitmaps, uint64_t bm_words, const uint32_t* blk, uint32_t n_win,
-                        uint32_t catalog, uint32_t* occ4, cudaStream_t s) {
-    const uint64_t n_words = ((uint64_t)catalog + 1 + 7) / 8;
-    uint64_t blocks = (n_words + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    occ4_kernel<<<(unsigned)blocks, 256, 0, s>>>(bitmaps, bm_words, blk[0], n_win > 1 ? blk[1] : 0,
-                                                 n_win > 2 ? blk[2] : 0, n_win > 3 ? blk[3] : 0, n_win, n_words, occ4);
-    return cudaGetLastError();
-}
-
-// union of up to 8 column blocks' occupancy bitmaps (fold chunks of several layers)
-__global__ void __launch_bounds__(256) bm_union_kernel(const uint32_t* __restrict__ bitmaps, uint64_t bm_words,
-                                                       const uint4 blk_lo, const uint4 blk_hi, uint32_t nb,
-                                                       uint32_t* __restrict__ out) {
-    const uint32_t blk[8] = {blk_lo.x, blk_lo.y, blk_lo.z, blk_lo.w, blk_hi.x, blk_hi.y, blk_hi.z, blk_hi.w};
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < bm_words;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t w = 0;
-        for (uint32_t k = 0; k < nb; ++k) w |= bitmaps[(uint64_t)blk[k] * bm_words + i];
-        out[i] = w;
-    }
-}
-
-cudaError_t launch_bm_union(const uint32_t* bitmaps, uint64_t bm_words, const uint32_t* blk, uint32_t nb,
-                            uint32_t* out, cudaStream_t s) {
-    uint32_t b[8] = {};
-    for (uint32_t k = 0; k < nb && k < 8; ++k) b[k] = blk[k];
-    uint64_t blocks = (bm_words + 255) / 256;
-    if (blocks > 148 * 4) blocks = 148 * 4;
-    bm_union_kernel<<<(unsigned)blocks, 256, 0, s>>>(bitmaps, bm_words, make_uint4(b[0], b[1], b[2], b[3]),
-                                                     make_uint4(b[4], b[5], b[6], b[7]), nb < 8 ? nb : 8, out);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_clear_rows(void* d_table, const TableGeo& geo, uint32_t catalog, cudaStream_t s) {
     const uint64_t n = (uint64_t)geo.n_blocks * geo.bm_words;
     uint64_t blocks = (n + 255) / 256;

@@ -1,0 +1,440 @@
+// kernel_sparse.cu -- trial_kernel_bc: ballot-compacted rounds over packed
+// rows, the ARA trial kernel for sparse column blocks (SURVEY.md 8a rows
+// a2-a8 on the paper's ELTs).
+//
+// The paper's ELTs hold 10k-30k losses over a catalogue of millions,
+// so most events of a trial hit an all-zero row of the direct-access table,
+// which adds an exact +0 (every deductible and retention is >= 0).  Per event
+// the only work left is the occupancy test; the loss arithmetic (P:359-P:375)
+// runs for the occupied events only, 32 at a time.
+//
+//  * persistent: one CTA of 16 warps per SM; each warp owns a contiguous range
+//    of trials holding an equal share of the launch's events (a 32-ary search
+//    over the CSR offsets), so its event ids are ONE contiguous stream;
+//  * the stream is staged by the Tensor Memory Accelerator: one elected lane
+//    issues cp.async.bulk copies of 512-B chunks (128 ids) into a 4-stage
+//    per-warp ring, completion counted by an mbarrier per stage, with an
+//    L2::evict_first policy (the 4 GB YET is read exactly once; the paper's
+//    "chunking ... for the efficient use of shared memory");
+//  * the block's row-occupancy bitmap is copied once per CTA into shared
+//    memory (as much as fits next to the rings: ~72 % of a 2M-event
+//    catalogue); probes of the rest go to L1/L2.  The ids and probe words of
+//    batch c+1 are loaded while batch c is scanned;
+//  * scan: 32 consecutive events per ballot; occupied events are appended,
+//    in stream order, to a per-warp compaction ring in shared memory (the
+//    popc of the ballot below the lane gives the slot);
+//  * round: 32 queued events, queue entry i to lane i; each lane gathers its
+//    event's 32-B packed slot (one sector: non-zero mask, id, first values)
+//    and does a4-a7 for the layers of the launch.  A round's slot loads are
+//    issued one round before its arithmetic, and a trial's last (partial)
+//    round is finished -- with the trial's tree and stores -- when the next
+//    round is issued, so gathers overlap the scan and no trial end stalls;
+//  * the rounds of a trial start at an empty queue, so lane l adds the
+//    trial's occupied events l, l+32, ... in stream order, then a fixed
+//    5-step xor tree: an order that depends only on the trial's own events
+//    (partition and alignment invariant; A18/A21) and exact on
+//    integer-valued data (P10).
+#include <cstdlib>
+
+#include "ara_device.cuh"
+
+namespace ara {
+namespace {
+
+struct BcGeo {
+    static constexpr int WARPS = 16;
+    static constexpr int THREADS = WARPS * 32;
+    static constexpr int CHB = 512;                  // bytes per id chunk = one 128-event batch
+    static constexpr int NSTG = 4;                   // chunks per warp ring (power of two)
+    static constexpr int RING = NSTG * CHB;          // id ring bytes per warp
+    static constexpr int CBUF = 256;                 // compaction ring entries per warp (>= 31 + 128)
+    static constexpr int FIXED = WARPS * (RING + CBUF * 4);   // dynamic smem before the bitmap
+};
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                         uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_nohint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+// a shared-memory address the compiler must keep in a register (instead of
+// re-deriving it from the CTA's shared window at every use)
+__device__ __forceinline__ uint32_t pin(uint32_t v) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(v));
+    return v;
+}
+// occupancy word wi: shared memory for the first Ws words, else L1/L2
+__device__ __forceinline__ uint32_t probe(uint32_t wi, uint32_t Ws, uint32_t s_bm, const uint32_t* bm) {
+    uint32_t w;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %1, %2;\n\t@p ld.shared.u32 %0, [%3];\n\t"
+        "@!p ld.global.nc.u32 %0, [%4];\n\t}"
+        : "=r"(w)
+        : "r"(wi), "r"(Ws), "r"(s_bm + 4u * wi), "l"(bm + wi)
+        : "memory");
+    return w;
+}
+
+// One packed slot (kPackBytes) in registers: u32 mask, u32 id, then the row's
+// first non-zero values in column order (3 fp64 / 6 fp32).
+template <typename TV> struct Slot;
+template <> struct Slot<double> {
+    static constexpr int CAP = 3;
+    uint64_t q[4];
+    __device__ __forceinline__ uint32_t mask() const { return (uint32_t)q[0]; }
+    __device__ __forceinline__ uint32_t id() const { return (uint32_t)(q[0] >> 32); }
+    __device__ __forceinline__ double val(uint32_t v) const {
+        return __longlong_as_double((long long)(v == 0 ? q[1] : (v == 1 ? q[2] : q[3])));
+    }
+};
+template <> struct Slot<float> {
+    static constexpr int CAP = 6;
+    uint64_t q[4];
+    __device__ __forceinline__ uint32_t mask() const { return (uint32_t)q[0]; }
+    __device__ __forceinline__ uint32_t id() const { return (uint32_t)(q[0] >> 32); }
+    __device__ __forceinline__ double val(uint32_t v) const {
+        const uint64_t w = v < 2 ? q[1] : (v < 4 ? q[2] : q[3]);
+        return (double)__int_as_float((int)(uint32_t)((v & 1u) ? (w >> 32) : w));
+    }
+};
+__device__ __forceinline__ void ld_slot(const void* p, uint64_t (&q)[4]) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
+                 : "=l"(q[0]), "=l"(q[1]), "=l"(q[2]), "=l"(q[3])
+                 : "l"(p));
+}
+__device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a));
+    return v;
+}
+
+template <typename TV, int NLB>
+__global__ void __launch_bounds__(BcGeo::THREADS, 1) trial_kernel_bc(const __grid_constant__ TrialParams p) {
+    using Geo = BcGeo;
+    constexpr int CAP = Slot<TV>::CAP;
+    constexpr uint32_t CHE = Geo::CHB / 4;   // ids per chunk (= per batch)
+    constexpr uint32_t NSTG = Geo::NSTG;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(16) double2 s_term[NLB][32];
+    __shared__ __align__(8) uint64_t s_bar[Geo::WARPS * Geo::NSTG + 1];
+    const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
+    const uint32_t sbase = pin((uint32_t)__cvta_generic_to_shared(smem));
+    const uint32_t ring = sbase + wib * (uint32_t)Geo::RING;
+    const uint32_t cbuf = sbase + (uint32_t)(Geo::WARPS * Geo::RING) + wib * (uint32_t)(Geo::CBUF * 4);
+    const uint32_t s_bm = sbase + (uint32_t)Geo::FIXED;
+    const uint32_t s_tm = pin((uint32_t)__cvta_generic_to_shared(&s_term[0][0]));
+    const uint32_t bar0 = pin((uint32_t)__cvta_generic_to_shared(&s_bar[wib * Geo::NSTG]));
+    const uint32_t bmbar = (uint32_t)__cvta_generic_to_shared(&s_bar[Geo::WARPS * Geo::NSTG]);
+    const uint32_t Ws = p.bm_smem_words;
+    const uint32_t* bm = p.bm;
+
+    for (int i = threadIdx.x; i < NLB * 32; i += Geo::THREADS) s_term[i / 32][i % 32] = p.term[i / 32][i % 32];
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < Geo::WARPS * Geo::NSTG + 1; ++s)
+            mbar_init((uint32_t)__cvta_generic_to_shared(&s_bar[s]), 1u);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && Ws) {   // the shared-memory part of the occupancy bitmap (read by every CTA)
+        mbar_expect_tx(bmbar, Ws * 4u);
+        bulk_g2s_nohint(s_bm, bm, Ws * 4u, bmbar);
+    }
+
+    // ---- this warp's trials [tb, te): an equal share of the launch's events
+    const uint64_t nw = (uint64_t)gridDim.x * Geo::WARPS, gw = (uint64_t)blockIdx.x * Geo::WARPS + wib;
+    const uint64_t base = __ldg(p.off);
+    const uint64_t o_b = __ldg(p.off + p.t_begin);
+    uint64_t o_e = __ldg(p.off + p.t_end);
+    uint32_t err = 0;
+    if (o_b < base || o_e < o_b) { err |= ERRBIT_OFFSETS; o_e = o_b; }
+    // first t in [t_begin, t_end] with off[t] >= target (32-ary search; the
+    // offsets are non-decreasing when valid, and a violation is caught below)
+    auto lower_bound = [&](uint64_t target) {
+        uint64_t lo = p.t_begin, hi = p.t_end;
+        while (hi > lo) {
+            const uint64_t step = (hi - lo + 31) / 32;
+            const uint64_t idx = lo + (uint64_t)lane * step;
+            const bool ge = idx >= hi || __ldg(p.off + idx) >= target;
+            const uint32_t m = __ballot_sync(0xffffffffu, ge);
+            if (m == 0u) {
+                lo = lo + 31 * step + 1;
+            } else {
+                const uint32_t f = (uint32_t)(__ffs(m) - 1);
+                if (f == 0u) {
+                    hi = lo;
+                } else {
+                    const uint64_t l0 = lo;
+                    lo = l0 + (f - 1) * step + 1;
+                    hi = l0 + f * step < hi ? l0 + f * step : hi;
+                }
+            }
+        }
+        return lo;
+    };
+    const uint64_t span_ev = o_e - o_b;
+    const uint64_t tb = gw == 0 ? p.t_begin : lower_bound(o_b + span_ev * gw / nw);
+    uint64_t te = gw + 1 == nw ? p.t_end : lower_bound(o_b + span_ev * (gw + 1) / nw);
+    if (te < tb) { err |= ERRBIT_OFFSETS; te = tb; }
+    int64_t S0 = 0, S1 = 0;   // the warp's event stream [S0, S1), indices into p.ids
+    if (te > tb) {
+        const uint64_t a = __ldg(p.off + tb), b = __ldg(p.off + te);
+        if (a < o_b || b < a || b > o_e) { err |= ERRBIT_OFFSETS; te = tb; }
+        else { S0 = (int64_t)(a - base); S1 = (int64_t)(b - base); }
+    }
+
+    // ---- the stream's chunks, 16-B aligned; chunk c = batch c.  Positions
+    // are 32-bit offsets from P0, the stream index of the ring's first id.
+    const uintptr_t a_s = reinterpret_cast<uintptr_t>(p.ids + S0);
+    const uintptr_t a0 = a_s & ~(uintptr_t)15;
+    const uintptr_t aend = (reinterpret_cast<uintptr_t>(p.ids + S1) + 15) & ~(uintptr_t)15;
+    const int64_t P0 = S0 - (int64_t)((a_s - a0) >> 2);
+    if (S1 - P0 > (int64_t)0x7fffff00) { err |= ERRBIT_OFFSETS; te = tb; S1 = S0; }   // > 2^31 events in one warp
+    const uint32_t nchunks = S1 > S0 ? (uint32_t)((aend - a0 + Geo::CHB - 1) / Geo::CHB) : 0u;
+    const uint64_t pol = policy_evict_first();
+    auto issue_chunk = [&](uint32_t c) {   // lane 0
+        const uintptr_t src = a0 + (uintptr_t)c * Geo::CHB;
+        const uint32_t bytes = aend - src < (uintptr_t)Geo::CHB ? (uint32_t)(aend - src) : (uint32_t)Geo::CHB;
+        const uint32_t st = c & (NSTG - 1);
+        mbar_expect_tx(bar0 + 8u * st, bytes);
+        bulk_g2s(ring + st * Geo::CHB, reinterpret_cast<const void*>(src), bytes, bar0 + 8u * st, pol);
+    };
+    if (lane == 0)
+        for (uint32_t c = 0; c < NSTG && c < nchunks; ++c) issue_chunk(c);
+    if (Ws) mbar_wait(bmbar, 0u);   // the bitmap has landed
+
+    // batch c: its ids (0 for an id outside [1, C], A14 -- row 0 is never
+    // occupied) and their occupancy words; the chunk's stage is refilled as
+    // soon as its ids are in registers.  A batch past the stream's end reads
+    // stale ids: none of its positions is ever live.
+    const uint32_t C = p.catalog;
+    auto load_batch = [&](uint32_t c, uint32_t (&x)[4], uint32_t (&wd)[4]) {
+        const uint32_t st = c & (NSTG - 1);
+        if (c < nchunks) mbar_wait(bar0 + 8u * st, (c / NSTG) & 1u);
+        const uint32_t ra = ring + st * (uint32_t)Geo::CHB + lane * 4u;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t v = lds32(ra + 128u * j);
+            const uint32_t xc = v - 1u < C ? v : 0u;
+            x[j] = xc;
+            wd[j] = probe(xc >> 5, Ws, s_bm, bm);
+        }
+        if (c + NSTG < nchunks) {
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // our reads precede the refill
+                issue_chunk(c + NSTG);
+            }
+        }
+    };
+
+    uint32_t head = 0, tail = 0;   // compaction ring: queued entries [head, tail) (warp-uniform)
+    double G[NLB];
+    uint32_t m[NLB];
+#pragma unroll
+    for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
+    Slot<TV> sl;
+    bool pend = false;       // a round's slots are in flight
+    bool pend_fin = false;   // ... and it is the last round of trial pend_t
+    uint64_t pend_t = 0;
+
+    // scan the current batch over its positions [dlo, dhi): append the
+    // occupied events in stream order
+    const uint32_t lt = (1u << lane) - 1u;
+    auto scan = [&](uint32_t dlo, uint32_t dhi, const uint32_t (&x)[4], const uint32_t (&wd)[4]) {
+        const uint32_t span = dhi - dlo;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t k = 32u * j + lane;
+            const bool live = k - dlo < span;
+            err |= (live && x[j] == 0u) ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
+            uint32_t r;
+            asm("shf.r.wrap.b32 %0, %1, %1, %2;" : "=r"(r) : "r"(wd[j]), "r"(x[j]));
+            const bool occ = live && (r & 1u);
+            const uint32_t M = __ballot_sync(0xffffffffu, occ);
+            if (occ) sts32(cbuf + ((tail + __popc(M & lt)) & (uint32_t)(Geo::CBUF - 1)) * 4u, x[j]);
+            tail += __popc(M);
+        }
+    };
+    // a7 tree + a8 stores of trial t (lane 0), accumulators reset
+    auto finalize = [&](uint64_t t) {
+#pragma unroll
+        for (int l = 0; l < NLB; ++l) {
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) G[l] = __dadd_rn(G[l], __shfl_xor_sync(0xffffffffu, G[l], off));
+            m[l] = __reduce_add_sync(0xffffffffu, m[l]);
+        }
+        if (lane == 0) store_trial(p, t, G, m);
+#pragma unroll
+        for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
+    };
+    // a4-a7 for the lane's event of the pending round (a lane without one
+    // adds +0); the trial's tree and stores when it was its last round
+    auto consume = [&]() {
+        pend = false;
+        const uint32_t mask = sl.mask();
+        double le[NLB];
+#pragma unroll
+        for (int l = 0; l < NLB; ++l) le[l] = 0.0;
+        auto add = [&](double xv, uint32_t j) {
+#pragma unroll
+            for (int l = 0; l < NLB; ++l) {
+                if (l == 0 || l < (int)p.n_layers) {
+                    const double2 tc = lds_f64x2(s_tm + ((uint32_t)l * 32u + j) * 16u);
+                    le[l] = __dadd_rn(le[l], terms(xv, tc.x, tc.y));
+                }
+            }
+        };
+        if (__popc(mask) <= CAP) {
+            // the slot holds all of the row's non-zeros: walk them in column order
+            uint32_t mm = mask, v = 0;
+            while (mm) {
+                const uint32_t b = (uint32_t)(__ffs(mm) - 1);
+                mm &= mm - 1u;
+                const uint32_t j = b - p.pk_col0;   // window element (wraps when b < col0)
+                if (j < 32u && ((p.pk_wmask >> j) & 1u)) add(sl.val(v), j);
+                ++v;
+            }
+        } else {
+            // more non-zeros than the slot holds: the rest from the dense table
+            uint32_t mm = (mask >> p.pk_col0) & p.pk_wmask;
+            while (mm) {
+                const uint32_t j = (uint32_t)(__ffs(mm) - 1);
+                mm &= mm - 1u;
+                const uint32_t v = __popc(mask & ((1u << (j + p.pk_col0)) - 1u));
+                const double xv = v < (uint32_t)CAP ? sl.val(v)
+                                                    : (double)__ldg(static_cast<const TV*>(p.table) + p.sec_off[0] +
+                                                                    (uint64_t)sl.id() * p.row_stride + j);
+                add(xv, j);
+            }
+        }
+#pragma unroll
+        for (int l = 0; l < NLB; ++l) {
+            if (l >= (int)p.n_layers) break;
+            const double o = terms(le[l], p.lw[l].occ_r, p.lw[l].occ_l);
+            G[l] = __dadd_rn(G[l], o);
+            m[l] += (o > 0.0) ? 1u : 0u;
+        }
+        if (pend_fin) {
+            pend_fin = false;
+            finalize(pend_t);
+        }
+    };
+    // issue a round of trial t: up to 32 queued events, entry head + i to lane i
+    auto issue_round = [&](uint64_t t) {
+        __syncwarp();   // the scan's appends (other lanes' stores) are visible
+        const uint32_t nr = tail - head < 32u ? tail - head : 32u;
+        if (lane < nr) {
+            const uint32_t e = lds32(cbuf + ((head + lane) & (uint32_t)(Geo::CBUF - 1)) * 4u);
+            ld_slot(static_cast<const char*>(p.pk) + (uint64_t)e * kPackBytes, sl.q);
+        } else {
+            sl.q[0] = 0; sl.q[1] = 0; sl.q[2] = 0; sl.q[3] = 0;
+        }
+        head += nr;
+        pend = true;
+        pend_t = t;
+    };
+
+    uint32_t cx[4], cw[4], nx[4], nwd[4];
+    load_batch(0, cx, cw);
+    load_batch(1, nx, nwd);
+    uint32_t c = 0;                                   // current batch
+    uint32_t rlo = (uint32_t)(S0 - P0);               // next position of the stream
+    const uint32_t rS1 = (uint32_t)(S1 - P0);
+    uint64_t o_hi = te > tb ? __ldg(p.off + tb + 1) : 0;   // off[t + 1] of the current trial
+#pragma unroll 1
+    for (uint64_t t = tb; t < te; ++t) {
+        const uint64_t o_nx = t + 2 <= te ? __ldg(p.off + t + 2) : 0;   // next trial's end, one trial ahead
+        const int64_t hi64 = (int64_t)(o_hi - base) - P0;
+        uint32_t rhi = (uint32_t)hi64;
+        if (o_hi < base || hi64 < (int64_t)rlo) { err |= ERRBIT_OFFSETS; rhi = rlo; }
+        if (rhi > rS1) { err |= ERRBIT_OFFSETS; rhi = rS1 > rlo ? rS1 : rlo; }
+#pragma unroll 1
+        for (;;) {
+            const uint32_t bs = c * CHE;
+            const uint32_t dlo = rlo > bs ? rlo - bs : 0u;            // <= CHE
+            const uint32_t dhi = rhi - bs < CHE ? rhi - bs : CHE;
+            if (dhi > dlo) scan(dlo, dhi, cx, cw);
+            const bool fin = rhi <= bs + CHE;   // the trial ends in this batch
+#pragma unroll 1
+            while (tail - head >= 32u || (fin && tail != head)) {
+                if (pend) consume();
+                issue_round(t);
+            }
+            if (fin) break;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) { cx[j] = nx[j]; cw[j] = nwd[j]; }
+            ++c;
+            load_batch(c + 1, nx, nwd);
+        }
+        if (pend && pend_t == t) {
+            pend_fin = true;   // finished when the next round is issued (or at the end)
+        } else {
+            if (pend) consume();   // the previous trial's last round (finalises it)
+            finalize(t);           // no round of t in flight: its sum is complete
+        }
+        rlo = rhi;
+        o_hi = o_nx;
+    }
+    if (pend) consume();
+    // every issued chunk has landed before the CTA's shared memory is released
+    const uint32_t loaded = c + 2 < nchunks ? c + 2 : nchunks;
+    for (uint32_t cc = loaded; cc < nchunks && cc < loaded + NSTG; ++cc)
+        mbar_wait(bar0 + 8u * (cc & (NSTG - 1)), (cc / NSTG) & 1u);
+    peer_fence(p);
+    if (err) atomicOr(p.err, err);
+}
+
+template <typename TV>
+void* pick_bc(int nl) {
+    if (nl <= 1) return (void*)trial_kernel_bc<TV, 1>;
+    if (nl <= 2) return (void*)trial_kernel_bc<TV, 2>;
+    return (void*)trial_kernel_bc<TV, 4>;
+}
+
+}  // namespace
+
+// One CTA of 16 warps per SM; dynamic shared memory = the rings plus as much
+// of the occupancy bitmap as the opt-in limit leaves (a 16-B multiple).
+cudaError_t launch_trials_bc(const TrialParams& p, int fp32, int grid, cudaStream_t s) {
+    if (p.t_end <= p.t_begin) return cudaSuccess;
+    if (!p.bm || !p.pk) return cudaErrorInvalidValue;
+    void* fn = fp32 ? pick_bc<float>((int)p.n_layers) : pick_bc<double>((int)p.n_layers);
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+    if (e != cudaSuccess) return e;
+    const int64_t avail = (int64_t)optin - (int64_t)fa.sharedSizeBytes - BcGeo::FIXED;
+    uint64_t ws = avail > 0 ? (uint64_t)avail / 16 * 4 : 0;   // words, 16-B multiple
+    const uint64_t need = (((uint64_t)p.catalog + 1 + 31) / 32 + 3) / 4 * 4;   // within the padded bitmap
+    if (ws > need) ws = need;
+    if (const char* v = getenv("ARA_BC_SMEM_WORDS")) {   // A/B: cap the shared-memory part of the bitmap
+        const uint64_t cap = strtoull(v, nullptr, 10) / 4 * 4;
+        if (cap < ws) ws = cap;
+    }
+    TrialParams q = p;
+    q.bm_smem_words = (uint32_t)ws;
+    const size_t dyn = (size_t)BcGeo::FIXED + ws * 4;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (e != cudaSuccess) return e;
+    void* args[] = {(void*)&q};
+    return cudaLaunchKernel(fn, dim3(grid > 0 ? grid : 1), dim3(BcGeo::THREADS), args, dyn, s);
+}
+
+}  // namespace ara

@@ -551,7 +551,7 @@ cudaError_t launch_metrics_dist(const double* d_ylt, uint64_t T_local, uint64_t 
     P.dist = 1;
     for (uint32_t i = 0; i < n_rp; ++i) P.k[i] = h_k[i];
     const size_t smem = (size_t)n_rp * 256 * sizeof(uint32_t);
-    if (smem > 48 * 1024) {
+    if (smem > 32 * 1024) {   // leaves room for the kernels' static shared memory under the 48 KB default
         cudaError_t e = cudaFuncSetAttribute(radix_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -562,14 +562,15 @@ cudaError_t launch_metrics_dist(const double* d_ylt, uint64_t T_local, uint64_t 
     const size_t nh = (size_t)rows * n_rp * 256;
     for (int pass = 0; pass < 8; ++pass) {
         radix_pass_kernel<<<dim3(P.nblk, rows), 256, smem, s>>>(P, pass);
-        if (ncclAllReduce(P.hist, P.hist, nh, ncclUint32, ncclSum, comm, s) != ncclSuccess) { *nccl_err = 1; break; }
+        // comm == null: a single shard (world 1, ARA_METRICS_DIST / loopback): the reduce is the identity
+        if (comm && ncclAllReduce(P.hist, P.hist, nh, ncclUint32, ncclSum, comm, s) != ncclSuccess) { *nccl_err = 1; break; }
         select_kernel<<<rows, 256, smem, s>>>(P, pass);
     }
     if (*nccl_err) return cudaGetLastError();
     tail_kernel<<<dim3(P.nblk, rows), 256, 0, s>>>(P);
     const size_t nq = (size_t)rows * n_rp;
-    if (ncclGroupStart() != ncclSuccess || ncclAllReduce(P.dsum, P.dsum, nq, ncclDouble, ncclSum, comm, s) != ncclSuccess ||
-        ncclAllReduce(P.dcnt, P.dcnt, nq, ncclUint64, ncclSum, comm, s) != ncclSuccess || ncclGroupEnd() != ncclSuccess) {
+    if (comm && (ncclGroupStart() != ncclSuccess || ncclAllReduce(P.dsum, P.dsum, nq, ncclDouble, ncclSum, comm, s) != ncclSuccess ||
+        ncclAllReduce(P.dcnt, P.dcnt, nq, ncclUint64, ncclSum, comm, s) != ncclSuccess || ncclGroupEnd() != ncclSuccess)) {
         *nccl_err = 1;
         return cudaGetLastError();
     }
@@ -630,7 +631,7 @@ cudaError_t launch_metrics(const double* d_ylt, uint64_t T, uint64_t ld, uint32_
     P.rep = m.done + rows;
     for (uint32_t i = 0; i < n_rp; ++i) P.k[i] = h_k[i];
     const size_t smem = (size_t)n_rp * 256 * sizeof(uint32_t);
-    if (smem > 48 * 1024) {
+    if (smem > 32 * 1024) {   // leaves room for the kernels' static shared memory under the 48 KB default
         cudaError_t e = cudaFuncSetAttribute(radix_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
         if (e != cudaSuccess) return e;

@@ -30,7 +30,7 @@ def run_oracle(off, ids, elts, w, layers, fp32=False, terms=None):
                       oracle.layers_from_specs(layers), lookup="dense", fp32_storage=fp32)
 
 
-KERNEL_VARIANTS = (-1, 0, 1, 5, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 19, 20, 21)   # ARA_KERNEL: auto, register, cp.async ring, register/3 CTAs, TMA gather4, hybrid, cooperative cp.async ring at 1/2/3 CTAs/SM, compacted rounds (single / multi-window / 1-stage), packed rounds (1 / 4 stages, 256-event steps, cross-trial rounds)
+KERNEL_VARIANTS = (-1, 0, 5, 12, 30)   # ARA_KERNEL: auto, register pipeline (2 / 3 CTAs/SM), cooperative cp.async ring, ballot-compacted rounds (sparse blocks; elsewhere the auto choice)
 
 
 def run_gpu(off, ids, elts, w, layers, precision="f64", terms=None, load_mode="all", chunk_trials=0,

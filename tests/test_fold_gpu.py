@@ -1,7 +1,8 @@
 """Catalogue-fold mode: o(e) evaluated once per catalogue
-event, one gather per occurrence.  It must reproduce the direct path bit for
-bit (same per-event arithmetic, same per-trial order) and hence match the
-oracle within the same tolerance."""
+event, one gather per occurrence.  It must match the oracle (A21 tolerance,
+exact lossy counts) and reproduce the dense direct kernels bit for bit
+(ARA_NO_SKIP=1: same per-event arithmetic, same lane mapping and per-trial
+order)."""
 import math
 
 import numpy as np
@@ -14,30 +15,28 @@ pytestmark = pytest.mark.gpu
 INF = math.inf
 
 
-@pytest.mark.parametrize("fold_kernel", ["scan", "per_trial"])
+NO_SKIP = {"ARA_NO_SKIP": 1}
+
+
 @pytest.mark.parametrize("rho", [0.3, 0.02])
 @pytest.mark.parametrize("precision", ["f64", "f32"])
-def test_fold_equals_direct_tiny(cuda, precision, rho, fold_kernel):
-    """rho = 0.02: the folded pass skips unoccupied events (union occupancy
-    bitmap); fold_kernel: the per-trial pass (default) or the scan-based one
-    (ARA_FOLD_KERNEL=1)."""
+def test_fold_equals_direct_tiny(cuda, precision, rho):
     w = synth.get_config("tiny").with_(rho=rho)
     off, ids, elts = make_inputs(w)
-    env = {"ARA_FOLD_KERNEL": 1} if fold_kernel == "scan" else None
-    a = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100))
-    b = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100), run_mode="fold",
-                env=env)
+    a = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100), env=NO_SKIP)
+    b = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100), run_mode="fold")
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     assert np.array_equal(a[3][1], b[3][1]) and np.array_equal(a[3][2], b[3][2])
-    assert_ylt_close(b[0], run_oracle(off, ids, elts, w, w.layers, fp32=precision == "f32"))
+    orc = run_oracle(off, ids, elts, w, w.layers, fp32=precision == "f32")
+    assert_ylt_close(b[0], orc)
+    assert np.array_equal(b[1], orc["lossy"])
 
 
 @pytest.mark.parametrize("rho", [0.3, 0.01])
 @pytest.mark.parametrize("n_layers", [1, 3, 5, 9, 17])
 def test_fold_many_layers_and_chunks(cuda, n_layers, rho):
     """Layer counts that exercise fold chunks of 1, 4, 8 layers and several
-    folded launches; windows unaligned and shared; rho = 0.01: sparse blocks,
-    union occupancy bitmaps over 1-2 blocks per fold chunk."""
+    folded launches; windows unaligned and shared; rho = 0.01: sparse blocks."""
     w = synth.get_config("tiny").with_(n_elts=24, catalog=2000, rho=rho, n_trials=600, nmin=0, nmax=260)
     off, ids, elts = make_inputs(w)
     rng = np.random.default_rng(n_layers)
@@ -47,7 +46,7 @@ def test_fold_many_layers_and_chunks(cuda, n_layers, rho):
         e = int(rng.integers(b + 1, min(24, b + 16) + 1))
         layers.append(synth.LayerSpec(b, e, float(rng.uniform(0, 5e4)), float(rng.choice([INF, rng.uniform(1e5, 1e6)])),
                                       float(rng.uniform(0, 2e6)), float(rng.choice([INF, rng.uniform(1e6, 5e6)]))))
-    a = run_gpu(off, ids, elts, w, layers)
+    a = run_gpu(off, ids, elts, w, layers, env=NO_SKIP)
     b = run_gpu(off, ids, elts, w, layers, run_mode="fold")
     assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
     orc = run_oracle(off, ids, elts, w, layers)
@@ -58,13 +57,17 @@ def test_fold_many_layers_and_chunks(cuda, n_layers, rho):
 def test_fold_chunked_h2d(cuda):
     w = synth.get_config("tiny").with_(n_trials=2000)
     off, ids, elts = make_inputs(w)
-    a = run_gpu(off, ids, elts, w, w.layers)
+    a = run_gpu(off, ids, elts, w, w.layers, env=NO_SKIP)
     b = run_gpu(off, ids, elts, w, w.layers, run_mode="fold", load_mode="chunked", chunk_trials=77)
     assert np.array_equal(a[0], b[0])
+    assert_ylt_close(b[0], run_oracle(off, ids, elts, w, w.layers))
 
 
 def test_fold_fullsize_equals_direct(cuda):
-    """Paper-shaped (1M trials, 1e9 events): fold == direct, bit for bit."""
+    """Paper-shaped (1M trials, 1e9 events): fold == the dense direct kernel
+    (ARA_NO_SKIP), bit for bit, and faster than it; the default sparse kernel
+    within the A21 bound of both (its summation order differs)."""
+    import os
     import torch
     from paper_1606_04473_b200 import ara
     w = synth.get_config("paper")
@@ -73,9 +76,14 @@ def test_fold_fullsize_equals_direct(cuda):
     d_off = torch.from_numpy(off.view(np.int64)).cuda()
     d_ids = torch.from_numpy(ids.view(np.int32)).cuda()
     out = []
-    for mode in ("direct", "fold"):
+    for mode, no_skip in (("direct", "1"), ("fold", "0"), ("direct", "0")):
         y = torch.empty((2, w.n_trials), dtype=torch.float64, device="cuda")
-        with ara.Context(w.catalog, run_mode=mode, stream=torch.cuda.current_stream()) as ctx:
+        os.environ["ARA_NO_SKIP"] = no_skip
+        try:
+            ctx = ara.Context(w.catalog, run_mode=mode, stream=torch.cuda.current_stream())
+        finally:
+            os.environ.pop("ARA_NO_SKIP", None)
+        with ctx:
             ctx.load_elts(eo, ev, ls, w.elt_terms())
             ctx.load_yet(w.n_trials, 0, d_off, d_ids)
             ctx.run(w.layers, y)            # first launch (module loading) untimed
@@ -84,3 +92,7 @@ def test_fold_fullsize_equals_direct(cuda):
         out.append((y.cpu().numpy(), st))
     assert np.array_equal(out[0][0], out[1][0])
     assert out[1][1]["kernel_ms"] < out[0][1]["kernel_ms"]
+    # A21: |dY| <= 1e-9 S_t, and S_t >= G_t >= Y_t + AggR wherever Y_t > 0 in
+    # either run (the portfolio row is the one layer's row here)
+    aggr = w.layers[0].agg_retention
+    assert (np.abs(out[2][0] - out[1][0]) <= 1e-9 * (np.maximum(out[1][0], out[2][0]) + aggr + 1.0)).all()
