@@ -59,6 +59,7 @@ extern "C" {
 #define ARA_MAX_LAYERS 64       /* layers per ara_run call */
 #define ARA_MAX_RP 64           /* return periods per ara_metrics call */
 #define ARA_MAX_PROGRAMS 64     /* programs per ara_run_portfolio call */
+#define ARA_MAX_EP_POINTS 4096  /* thresholds per ara_ep_curve call */
 
 typedef struct ara_ctx ara_ctx;
 
@@ -290,6 +291,22 @@ ara_status ara_run_portfolio(ara_ctx* ctx, uint32_t n_programs, const uint32_t* 
  * DOMAIN (R outside [1, T]), CUDA, NCCL. */
 ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* return_periods,
                        uint64_t* k, double* pml, double* tvar, double* device_ms);
+
+/* Aggregate exceedance-probability (EP) curve of every row of the last
+ * ara_run's YLT (SURVEY 8f F4 "full EP curve"; the risk-metric stage of P:273;
+ * reading A23):
+ *   counts[row][i] = #{t : Y[row][t] > thresholds[i]},  EP(x_i) = counts / n_trials_global
+ * (strict exceedance: the fraction of simulated years whose loss is larger).
+ * The other direction of the curve, the loss at exceedance probability p, is
+ * PML(1/p): ara_metrics with return period 1/p.
+ *   thresholds [n_points] HOST doubles, non-decreasing, no NaN (+-inf allowed)
+ *   counts     [rows][n_points] HOST u64, rows as in ara_metrics
+ * Exact integers, computed on the device (one sweep of the YLT, binary search
+ * over the thresholds, integer histograms).  COLLECTIVE when world > 1: each
+ * rank counts its own trials and the counts are all-reduced.
+ * Errors: STATE (no run yet), INVALID_ARG (n_points 0 or > ARA_MAX_EP_POINTS,
+ * NULL or device arrays), DOMAIN (NaN or decreasing thresholds), CUDA, NCCL. */
+ara_status ara_ep_curve(ara_ctx* ctx, uint32_t n_points, const double* thresholds, uint64_t* counts);
 
 #ifdef __cplusplus
 }

@@ -57,6 +57,8 @@ def lib():
         L.oracle_rank.argtypes = [u64, d]
         L.oracle_metrics.restype = i32
         L.oracle_metrics.argtypes = [vp, u64, u32, vp, vp, vp, vp]
+        L.oracle_ep_counts.restype = None
+        L.oracle_ep_counts.argtypes = [vp, u64, u32, vp, vp]
         _LIB = L
     return _LIB
 
@@ -167,6 +169,15 @@ def metrics(y, return_periods):
     if rc != 0:
         raise ValueError("return period outside [1, T]")
     return k, pml, tvar
+
+
+def ep_counts(y, thresholds):
+    """counts[i] = #{t : y[t] > thresholds[i]} (A23, SURVEY 8f F4 EP curve)."""
+    y = _c(y, np.float64)
+    x = _c(thresholds, np.float64)
+    out = np.zeros(len(x), dtype=np.uint64)
+    lib().oracle_ep_counts(y.ctypes.data, len(y), len(x), x.ctypes.data, out.ctypes.data)
+    return out
 
 
 def layers_from_specs(specs) -> List[Tuple[List[int], float, float, float, float]]:

@@ -152,3 +152,13 @@ int oracle_metrics(const double* y, uint64_t n_trials, uint32_t n_rp,
     free(s);
     return 0;
 }
+
+/* A23: counts[i] = #{t : y[t] > x[i]} (strict exceedance), by brute force. */
+void oracle_ep_counts(const double* y, uint64_t n_trials, uint32_t n_points, const double* x, uint64_t* counts) {
+    for (uint32_t i = 0; i < n_points; ++i) {
+        uint64_t c = 0;
+        for (uint64_t t = 0; t < n_trials; ++t)
+            if (y[t] > x[i]) c = c + 1;
+        counts[i] = c;
+    }
+}

@@ -96,6 +96,13 @@ uint64_t oracle_rank(uint64_t n_trials, double return_period);
 int oracle_metrics(const double* y, uint64_t n_trials, uint32_t n_rp,
                    const double* return_periods, uint64_t* k, double* pml, double* tvar);
 
+/* Aggregate exceedance-probability curve of a YLT row (SURVEY 8f F4 "full EP
+ * curve", reading A23): for each threshold x[i], the number of trials whose
+ * year loss exceeds it, counts[i] = #{t : y[t] > x[i]}; EP(x[i]) =
+ * counts[i] / T, the fraction of simulated years with a larger loss.  Plain
+ * double loop. */
+void oracle_ep_counts(const double* y, uint64_t n_trials, uint32_t n_points, const double* x, uint64_t* counts);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,6 +33,7 @@ ARA_RUN_DIRECT, ARA_RUN_FOLD = 0, 1
 ARA_NCCL_ID_BYTES = 128
 ARA_MAX_LAYERS = 64
 ARA_MAX_RP = 64
+ARA_MAX_EP_POINTS = 4096
 
 
 class ara_config(ctypes.Structure):
@@ -89,6 +90,7 @@ _sig = {
     "ara_run": (_i, [_vp, _u32, _vp, _vp, _vp, ctypes.POINTER(ara_run_stats)]),
     "ara_run_portfolio": (_i, [_vp, _u32, _vp, _u32, _vp, _vp, _vp, ctypes.POINTER(ara_run_stats)]),
     "ara_metrics": (_i, [_vp, _u32, _vp, _vp, _vp, _vp, ctypes.POINTER(_d)]),
+    "ara_ep_curve": (_i, [_vp, _u32, _vp, _vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -278,6 +280,14 @@ def ara_metrics(h, n_rows: int, return_periods: Sequence[float]):
     return k, pml, tvar, ms.value
 
 
+def ara_ep_curve(h, n_rows: int, thresholds):
+    """counts [n_rows][n] u64: #{t : Y[row][t] > thresholds[i]} (thresholds non-decreasing)."""
+    x = np.ascontiguousarray(thresholds, dtype=np.float64)
+    counts = np.zeros((n_rows, len(x)), dtype=np.uint64)
+    _check(_lib.ara_ep_curve(h, len(x), x.ctypes.data, counts.ctypes.data), h)
+    return counts
+
+
 class Context:
     """One ARA context on one GPU (one per rank).  See include/ara.h."""
 
@@ -358,8 +368,11 @@ class Context:
     def metrics(self, return_periods):
         return ara_metrics(self.h, self.n_rows, return_periods)
 
+    def ep_curve(self, thresholds):
+        return ara_ep_curve(self.h, self.n_rows, thresholds)
+
 
 __all__ = ["Context", "AraError", "ara_create", "ara_destroy", "ara_load_elts", "ara_set_elt_terms",
            "ara_load_yet", "ara_run", "ara_metrics", "ara_partition", "ara_return_period_rank",
-           "ara_nccl_unique_id", "ara_load_yet_packed", "ara_run_portfolio", "ara_pack_ids", "ara_packed_words", "bits_for_catalog",
+           "ara_nccl_unique_id", "ara_load_yet_packed", "ara_ep_curve", "ara_run_portfolio", "ara_pack_ids", "ara_packed_words", "bits_for_catalog",
            "status_string", "version", "EXPORTED"]

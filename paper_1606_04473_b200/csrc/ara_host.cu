@@ -260,6 +260,7 @@ extern "C" void ara_destroy(ara_ctx* ctx) {
     cudaFree(ctx->d_ylt_global);
     cudaFree(ctx->d_lossy);
     cudaFree(ctx->d_fold);
+    cudaFree(ctx->d_ep);
     cudaFree(ctx->d_sp_off);
     cudaFree(ctx->d_sp_ev);
     cudaFree(ctx->d_sp_ls);
@@ -385,16 +386,24 @@ ara_status densify_local(ara_ctx* ctx, uint32_t n_elts, uint64_t nrec, const Spa
     return device_errors(ctx, (uint32_t)(ctx->h_small[0] & 0xffffffffu));
 }
 
-void set_l2_window(ara_ctx* ctx) {
-    if (!ctx->l2_persist || !ctx->d_table) return;
+// L2 persisting access-policy window (cfg.l2_persist; north star "HBM layout":
+// keep the hot ELT data resident in B200's L2) over the bytes a launch
+// actually gathers: for the sparse kernel the block's packed rows (the
+// occupied slots are touched at random), for the dense
+// kernels the window's column block of the table (256 MB at the paper's
+// catalogue in fp64, 128 MB in fp32).  hitRatio = persisting carve-out /
+// window bytes, so the persisting lines are a random subset of the window.
+// Set on the context stream before the launch, cleared after the run (the
+// stream may be the caller's).
+void set_l2_window(ara_ctx* ctx, const void* base, size_t bytes) {
+    if (!ctx->l2_persist) return;
     cudaDeviceProp prop{};
     if (cudaGetDeviceProperties(&prop, ctx->device) != cudaSuccess) { cudaGetLastError(); return; }
-    const size_t win = ctx->table_bytes < (size_t)prop.accessPolicyMaxWindowSize ? ctx->table_bytes
-                                                                                 : (size_t)prop.accessPolicyMaxWindowSize;
+    const size_t win = bytes < (size_t)prop.accessPolicyMaxWindowSize ? bytes : (size_t)prop.accessPolicyMaxWindowSize;
     cudaStreamAttrValue v{};
-    v.accessPolicyWindow.base_ptr = ctx->d_table;
-    v.accessPolicyWindow.num_bytes = win;
-    double hr = win ? (double)prop.persistingL2CacheMaxSize / (double)win : 0.0;
+    v.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+    v.accessPolicyWindow.num_bytes = base ? win : 0;
+    const double hr = win ? (double)prop.persistingL2CacheMaxSize / (double)win : 0.0;
     v.accessPolicyWindow.hitRatio = (float)(hr > 1.0 ? 1.0 : hr);
     v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
     v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
@@ -464,7 +473,6 @@ extern "C" ara_status ara_load_elts(ara_ctx* ctx, uint32_t n_elts, const uint64_
     ctx->terms.assign(n_elts, ara_elt_terms{0.0, INFINITY});
     if (terms)
         for (uint32_t j = 0; j < n_elts; ++j) ctx->terms[j] = terms[j];
-    set_l2_window(ctx);
     return ARA_OK;
 }
 
@@ -1131,6 +1139,14 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 used_occupancy = p.bm ? (double)ctx->occ_rows[g.q0 / spb] / ((double)ctx->catalog + 1.0) : 1.0;
                 if (variant < 0) variant = (!fp32 && g.nsec <= 4) ? 12 : (g.nl == 1 ? 5 : 0);
                 used_variant = variant;
+                if (ctx->l2_persist) {
+                    const char* tb = static_cast<const char*>(ctx->d_table);
+                    const size_t blk = g.q0 / spb;
+                    if (p.bm)   // the block's packed rows (its 250 KB bitmap is hot in any case)
+                        set_l2_window(ctx, p.pk, ((size_t)ctx->catalog + 1) * kPackBytes);
+                    else
+                        set_l2_window(ctx, tb + blk * geo.block_elems * geo.esz, geo.block_elems * geo.esz);
+                }
                 const int grid = (int)(trial_kernel_grid(fp32, g.nsec, (int)g.nl, variant) * ctx->grid_mult);
                 CK(launch_trials(p, fp32, g.nsec, grid > 0 ? grid : 1, variant, s));
             }
@@ -1146,6 +1162,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         ++launches;
     }
     CK(cudaEventRecord(ctx->ev[2], s));
+    if (ctx->l2_persist) set_l2_window(ctx, nullptr, 0);   // the stream may be the caller's
     for (void* q : wide_free) CK(cudaFreeAsync(q, s));
     for (auto e : chunk_ev) cudaEventDestroy(e);   // safe: destruction defers until complete
     if (stream_in) {
@@ -1315,5 +1332,39 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
     if (k)
         for (uint32_t q = 0; q < n_rp; ++q) k[q] = hk[q];
     if (device_ms) *device_ms = ev_ms(ctx->ev[0], ctx->ev[1]);
+    return ARA_OK;
+}
+
+// ============================================================ EP curve
+extern "C" ara_status ara_ep_curve(ara_ctx* ctx, uint32_t n_points, const double* thresholds, uint64_t* counts) {
+    if (!ctx) return ARA_ERR_INVALID_ARG;
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->last_layers == 0) return fail(ctx, ARA_ERR_STATE, "no successful ara_run yet");
+    if (n_points == 0 || n_points > ARA_MAX_EP_POINTS || !thresholds || !counts)
+        return fail(ctx, ARA_ERR_INVALID_ARG, "n_points must be in [1, %d] with non-NULL arrays", ARA_MAX_EP_POINTS);
+    if (classify(thresholds) == Mem::Device || classify(counts) == Mem::Device)
+        return fail(ctx, ARA_ERR_INVALID_ARG, "thresholds and counts must be host memory");
+    for (uint32_t i = 0; i < n_points; ++i) {
+        if (std::isnan(thresholds[i])) return fail(ctx, ARA_ERR_DOMAIN, "threshold %u is NaN", i);
+        if (i && thresholds[i] < thresholds[i - 1])
+            return fail(ctx, ARA_ERR_DOMAIN, "thresholds must be non-decreasing (index %u)", i);
+    }
+    const uint32_t rows = ctx->last_rows;
+    const size_t n = n_points;
+    const size_t bytes = n * sizeof(double) + (n + 1) * rows * sizeof(unsigned long long) + n * rows * sizeof(uint64_t);
+    ara_status st = ensure(ctx, ctx->d_ep, ctx->ep_cap, bytes);
+    if (st != ARA_OK) return st;
+    double* d_x = reinterpret_cast<double*>(ctx->d_ep);
+    unsigned long long* d_hist = reinterpret_cast<unsigned long long*>(ctx->d_ep + n * sizeof(double));
+    uint64_t* d_cnt = reinterpret_cast<uint64_t*>(ctx->d_ep + n * sizeof(double) +
+                                                  (n + 1) * rows * sizeof(unsigned long long));
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemcpyAsync(d_x, thresholds, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    // this rank's trials of the last run (world 1: all of them); the shards' counts add up
+    CK(launch_ep_curve(ctx->d_ylt_local, ctx->run_T_local, ctx->last_ld_local, rows, d_x, n_points, d_hist, d_cnt,
+                       ctx->n_sm, s));
+    if (ctx->world > 1) NK(ncclAllReduce(d_cnt, d_cnt, n * rows, ncclUint64, ncclSum, ctx->comm, s));
+    CK(cudaMemcpyAsync(counts, d_cnt, n * rows * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     return ARA_OK;
 }

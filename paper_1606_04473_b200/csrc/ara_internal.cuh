@@ -145,6 +145,10 @@ cudaError_t launch_trials_wide(const TrialParams& p, int fp32, const uint32_t* d
 cudaError_t launch_program_sums(double* ylt, uint64_t ld, uint64_t t_local, uint32_t n_programs,
                                 const uint32_t* d_program_layers, uint32_t n_layers, cudaStream_t s);
 
+// EP curve (ep_curve.cu): counts[row][i] = #{t < T : ylt[row * ld + t] > x[i]}, x non-decreasing
+cudaError_t launch_ep_curve(const double* d_ylt, uint64_t T, uint64_t ld, uint32_t rows, const double* d_x,
+                            uint32_t n, unsigned long long* d_hist, uint64_t* d_counts, int n_sm, cudaStream_t s);
+
 // metrics: radix select over the [rows][T] YLT (device), fixed-order tail sums
 struct MetricsScratch {
     uint32_t* hist = nullptr;       // [rows][n_rp][256]
@@ -258,6 +262,8 @@ struct ara_ctx {
     // peer_ld = T_global), so a9's indexing runs on one GPU; its metrics are
     // the distributed select over the shard with an identity reduce
     int lb_world = 0, lb_rank = 0;
+    unsigned char* d_ep = nullptr;    // EP-curve scratch: thresholds, histograms, counts
+    size_t ep_cap = 0;
     int run_mode = 0;                  // ARA_RUN_DIRECT / ARA_RUN_FOLD
     double* d_fold = nullptr;          // fold mode: per-event occurrence-net losses
     size_t fold_cap = 0;

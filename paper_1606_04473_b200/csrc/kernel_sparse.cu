@@ -8,11 +8,11 @@
 // the only work left is the occupancy test; the loss arithmetic (P:359-P:375)
 // runs for the occupied events only, 32 at a time.
 //
-//  * persistent: one CTA of 16 warps per SM; each warp owns a contiguous range
+//  * persistent: one CTA of 24-32 warps per SM; each warp owns a contiguous range
 //    of trials holding an equal share of the launch's events (a 32-ary search
 //    over the CSR offsets), so its event ids are ONE contiguous stream;
 //  * the stream is staged by the Tensor Memory Accelerator: one elected lane
-//    issues cp.async.bulk copies of 512-B chunks (128 ids) into a 4-stage
+//    issues cp.async.bulk copies of 512-B chunks (128 ids) into a 2-stage
 //    per-warp ring, completion counted by an mbarrier per stage, with an
 //    L2::evict_first policy (the 4 GB YET is read exactly once; the paper's
 //    "chunking ... for the efficient use of shared memory");
@@ -41,11 +41,19 @@
 namespace ara {
 namespace {
 
+#ifndef BC_NSTG
+#define BC_NSTG 2
+#endif
+// Warps per CTA (one CTA per SM) by layers per launch, measured
+// (profiles/r02_ab_bc_warps.txt): the loop is latency-bound, so as many warps
+// as the registers allow -- 32 for one layer (64 registers), 24 for towers.
+template <int NLB> struct BcWarps { static constexpr int value = NLB <= 1 ? 32 : 24; };
+template <int W>
 struct BcGeo {
-    static constexpr int WARPS = 16;
+    static constexpr int WARPS = W;                  // per CTA, one CTA per SM
     static constexpr int THREADS = WARPS * 32;
     static constexpr int CHB = 512;                  // bytes per id chunk = one 128-event batch
-    static constexpr int NSTG = 4;                   // chunks per warp ring (power of two)
+    static constexpr int NSTG = BC_NSTG;             // chunks per warp ring (power of two)
     static constexpr int RING = NSTG * CHB;          // id ring bytes per warp
     static constexpr int CBUF = 256;                 // compaction ring entries per warp (>= 31 + 128)
     static constexpr int FIXED = WARPS * (RING + CBUF * 4);   // dynamic smem before the bitmap
@@ -123,9 +131,9 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
     return v;
 }
 
-template <typename TV, int NLB>
-__global__ void __launch_bounds__(BcGeo::THREADS, 1) trial_kernel_bc(const __grid_constant__ TrialParams p) {
-    using Geo = BcGeo;
+template <typename TV, int NLB, int W = BcWarps<NLB>::value>
+__global__ void __launch_bounds__(BcGeo<W>::THREADS, 1) trial_kernel_bc(const __grid_constant__ TrialParams p) {
+    using Geo = BcGeo<W>;
     constexpr int CAP = Slot<TV>::CAP;
     constexpr uint32_t CHE = Geo::CHB / 4;   // ids per chunk (= per batch)
     constexpr uint32_t NSTG = Geo::NSTG;
@@ -206,9 +214,10 @@ __global__ void __launch_bounds__(BcGeo::THREADS, 1) trial_kernel_bc(const __gri
     if (S1 - P0 > (int64_t)0x7fffff00) { err |= ERRBIT_OFFSETS; te = tb; S1 = S0; }   // > 2^31 events in one warp
     const uint32_t nchunks = S1 > S0 ? (uint32_t)((aend - a0 + Geo::CHB - 1) / Geo::CHB) : 0u;
     const uint64_t pol = policy_evict_first();
+    // chunk c goes to stage c % NSTG; only the stream's last chunk is short
     auto issue_chunk = [&](uint32_t c) {   // lane 0
         const uintptr_t src = a0 + (uintptr_t)c * Geo::CHB;
-        const uint32_t bytes = aend - src < (uintptr_t)Geo::CHB ? (uint32_t)(aend - src) : (uint32_t)Geo::CHB;
+        const uint32_t bytes = c + 1 < nchunks ? (uint32_t)Geo::CHB : (uint32_t)(aend - src);
         const uint32_t st = c & (NSTG - 1);
         mbar_expect_tx(bar0 + 8u * st, bytes);
         bulk_g2s(ring + st * Geo::CHB, reinterpret_cast<const void*>(src), bytes, bar0 + 8u * st, pol);
@@ -254,14 +263,18 @@ __global__ void __launch_bounds__(BcGeo::THREADS, 1) trial_kernel_bc(const __gri
 
     // scan the current batch over its positions [dlo, dhi): append the
     // occupied events in stream order
+    // (full: the whole batch belongs to the trial -- no position masks, and
+    // invalid ids are caught by a running minimum instead of a per-event test)
     const uint32_t lt = (1u << lane) - 1u;
-    auto scan = [&](uint32_t dlo, uint32_t dhi, const uint32_t (&x)[4], const uint32_t (&wd)[4]) {
+    uint32_t xmin = 1u;   // min over the ids of full batches (0 = an id outside [1, C])
+    auto scan = [&](bool full, uint32_t dlo, uint32_t dhi, const uint32_t (&x)[4], const uint32_t (&wd)[4]) {
         const uint32_t span = dhi - dlo;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const uint32_t k = 32u * j + lane;
-            const bool live = k - dlo < span;
-            err |= (live && x[j] == 0u) ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
+            const bool live = full || k - dlo < span;
+            if (full) xmin = min(xmin, x[j]);
+            else err |= (live && x[j] == 0u) ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
             uint32_t r;
             asm("shf.r.wrap.b32 %0, %1, %1, %2;" : "=r"(r) : "r"(wd[j]), "r"(x[j]));
             const bool occ = live && (r & 1u);
@@ -349,9 +362,11 @@ __global__ void __launch_bounds__(BcGeo::THREADS, 1) trial_kernel_bc(const __gri
         pend_t = t;
     };
 
-    uint32_t cx[4], cw[4], nx[4], nwd[4];
-    load_batch(0, cx, cw);
-    load_batch(1, nx, nwd);
+    // two register sets, A and B, alternate between the current batch and the
+    // next one (no copies): batch c lives in set (c & 1)
+    uint32_t xa[4], wa[4], xb[4], wb[4];
+    load_batch(0, xa, wa);
+    load_batch(1, xb, wb);
     uint32_t c = 0;                                   // current batch
     uint32_t rlo = (uint32_t)(S0 - P0);               // next position of the stream
     const uint32_t rS1 = (uint32_t)(S1 - P0);
@@ -368,7 +383,15 @@ __global__ void __launch_bounds__(BcGeo::THREADS, 1) trial_kernel_bc(const __gri
             const uint32_t bs = c * CHE;
             const uint32_t dlo = rlo > bs ? rlo - bs : 0u;            // <= CHE
             const uint32_t dhi = rhi - bs < CHE ? rhi - bs : CHE;
-            if (dhi > dlo) scan(dlo, dhi, cx, cw);
+            if (dhi > dlo) {
+                if (dhi - dlo == CHE) {
+                    if (c & 1u) scan(true, 0u, CHE, xb, wb);
+                    else scan(true, 0u, CHE, xa, wa);
+                } else {
+                    if (c & 1u) scan(false, dlo, dhi, xb, wb);
+                    else scan(false, dlo, dhi, xa, wa);
+                }
+            }
             const bool fin = rhi <= bs + CHE;   // the trial ends in this batch
 #pragma unroll 1
             while (tail - head >= 32u || (fin && tail != head)) {
@@ -376,10 +399,10 @@ __global__ void __launch_bounds__(BcGeo::THREADS, 1) trial_kernel_bc(const __gri
                 issue_round(t);
             }
             if (fin) break;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) { cx[j] = nx[j]; cw[j] = nwd[j]; }
+            // the finished batch's set receives batch c + 2
+            if (c & 1u) load_batch(c + 2, xb, wb);
+            else load_batch(c + 2, xa, wa);
             ++c;
-            load_batch(c + 1, nx, nwd);
         }
         if (pend && pend_t == t) {
             pend_fin = true;   // finished when the next round is issued (or at the end)
@@ -395,32 +418,36 @@ __global__ void __launch_bounds__(BcGeo::THREADS, 1) trial_kernel_bc(const __gri
     const uint32_t loaded = c + 2 < nchunks ? c + 2 : nchunks;
     for (uint32_t cc = loaded; cc < nchunks && cc < loaded + NSTG; ++cc)
         mbar_wait(bar0 + 8u * (cc & (NSTG - 1)), (cc / NSTG) & 1u);
+    if (xmin == 0u) err |= ERRBIT_EVENT_RANGE;
     peer_fence(p);
     if (err) atomicOr(p.err, err);
 }
 
 template <typename TV>
-void* pick_bc(int nl) {
-    if (nl <= 1) return (void*)trial_kernel_bc<TV, 1>;
-    if (nl <= 2) return (void*)trial_kernel_bc<TV, 2>;
+void* pick_bc(int nl, int* warps) {
+    if (nl <= 1) { *warps = BcWarps<1>::value; return (void*)trial_kernel_bc<TV, 1>; }
+    if (nl <= 2) { *warps = BcWarps<2>::value; return (void*)trial_kernel_bc<TV, 2>; }
+    *warps = BcWarps<4>::value;
     return (void*)trial_kernel_bc<TV, 4>;
 }
 
 }  // namespace
 
-// One CTA of 16 warps per SM; dynamic shared memory = the rings plus as much
+// One CTA of 24-32 warps per SM; dynamic shared memory = the rings plus as much
 // of the occupancy bitmap as the opt-in limit leaves (a 16-B multiple).
 cudaError_t launch_trials_bc(const TrialParams& p, int fp32, int grid, cudaStream_t s) {
     if (p.t_end <= p.t_begin) return cudaSuccess;
     if (!p.bm || !p.pk) return cudaErrorInvalidValue;
-    void* fn = fp32 ? pick_bc<float>((int)p.n_layers) : pick_bc<double>((int)p.n_layers);
+    int warps = 16;
+    void* fn = fp32 ? pick_bc<float>((int)p.n_layers, &warps) : pick_bc<double>((int)p.n_layers, &warps);
+    const int fixed = warps * (BcGeo<16>::RING + BcGeo<16>::CBUF * 4);   // per-warp rings are W-independent
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     cudaFuncAttributes fa{};
     cudaError_t e = cudaFuncGetAttributes(&fa, fn);
     if (e != cudaSuccess) return e;
-    const int64_t avail = (int64_t)optin - (int64_t)fa.sharedSizeBytes - BcGeo::FIXED;
+    const int64_t avail = (int64_t)optin - (int64_t)fa.sharedSizeBytes - fixed;
     uint64_t ws = avail > 0 ? (uint64_t)avail / 16 * 4 : 0;   // words, 16-B multiple
     const uint64_t need = (((uint64_t)p.catalog + 1 + 31) / 32 + 3) / 4 * 4;   // within the padded bitmap
     if (ws > need) ws = need;
@@ -430,11 +457,11 @@ cudaError_t launch_trials_bc(const TrialParams& p, int fp32, int grid, cudaStrea
     }
     TrialParams q = p;
     q.bm_smem_words = (uint32_t)ws;
-    const size_t dyn = (size_t)BcGeo::FIXED + ws * 4;
+    const size_t dyn = (size_t)fixed + ws * 4;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (e != cudaSuccess) return e;
     void* args[] = {(void*)&q};
-    return cudaLaunchKernel(fn, dim3(grid > 0 ? grid : 1), dim3(BcGeo::THREADS), args, dyn, s);
+    return cudaLaunchKernel(fn, dim3(grid > 0 ? grid : 1), dim3(warps * 32), args, dyn, s);
 }
 
 }  // namespace ara

@@ -13,6 +13,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+EP_X = np.concatenate([[-1.0, 0.0], np.linspace(1.0, 1.2e7, 255), [np.inf]])   # EP-curve thresholds
+
+
 def bumped_layers(layers):
     return tuple(L.__class__(L.elt_begin, L.elt_end, L.occ_retention * 1.5 + 1.0, L.occ_limit, L.agg_retention,
                              L.agg_limit) for L in layers)
@@ -50,13 +53,14 @@ def main():
         for layers in (w.layers, bumped_layers(w.layers), w.layers):
             ylt, lossy, st = ctx.run_host(layers, n_local=count)
             k, pml, tvar, _ = ctx.metrics(R)
-            res.append((ylt, pml, tvar, k, st))
+            ep = ctx.ep_curve(EP_X)           # collective: shard counts all-reduced
+            res.append((ylt, pml, tvar, k, st, ep))
         # every rank holds the same global YLT and metrics
         g = [None] * world
-        dist.all_gather_object(g, [(y.tobytes(), p.tobytes(), t.tobytes()) for y, p, t, _, _ in res])
+        dist.all_gather_object(g, [(y.tobytes(), p.tobytes(), t.tobytes(), e.tobytes()) for y, p, t, _, _, e in res])
         same = all(x == g[0] for x in g)
         if rank == 0:
-            np.savez(out, ylt=res[0][0], pml=res[0][1], tvar=res[0][2], k=res[0][3], same=same,
+            np.savez(out, ylt=res[0][0], pml=res[0][1], tvar=res[0][2], k=res[0][3], same=same, ep=res[0][5],
                      allgather_ms=res[0][4]["allgather_ms"], ylt_b=res[1][0], pml_b=res[1][1], ylt_c=res[2][0])
     dist.destroy_process_group()
 

@@ -34,7 +34,7 @@ KERNEL_VARIANTS = (-1, 0, 5, 12, 30)   # ARA_KERNEL: auto, register pipeline (2 
 
 
 def run_gpu(off, ids, elts, w, layers, precision="f64", terms=None, load_mode="all", chunk_trials=0,
-            device_inputs=False, return_periods=None, variant=None, run_mode="direct", env=None):
+            device_inputs=False, return_periods=None, variant=None, run_mode="direct", env=None, l2_persist=False):
     """env: extra ARA_* tuning variables read at ara_create (e.g. ARA_NO_SKIP)."""
     import os
     import torch
@@ -47,7 +47,7 @@ def run_gpu(off, ids, elts, w, layers, precision="f64", terms=None, load_mode="a
     os.environ.update({k: str(v) for k, v in env.items()})
     try:
         ctx = ara.Context(w.catalog, precision=precision, load_mode=load_mode, chunk_trials=chunk_trials,
-                          run_mode=run_mode)
+                          run_mode=run_mode, l2_persist=l2_persist)
     finally:
         for k, v in old.items():
             if v is None:

@@ -186,3 +186,45 @@ def test_metrics_read_the_last_run_after_a_new_yet(cuda):
             got = ctx.metrics(R)
             assert all(np.array_equal(a, b) for a, b in zip(got[:3], ref[:3]))
     assert_metrics_close(ref, oracle_rows(orc), orc["scale"], R)
+
+
+@pytest.mark.parametrize("int_cap", [None, 2.0 ** 31])
+def test_ep_curve_matches_oracle(cuda, int_cap):
+    """SURVEY 8f F4 EP curve (A23): counts[row][i] = #{t : Y_t > x_i}, exact
+    against the oracle's brute-force count over the same YLT (the GPU's, and
+    on integer-valued data the oracle's own), for thresholds at -inf, below,
+    at and between the losses (ties), at the maximum and +inf; consistent
+    with the device PML: #{Y > PML(R)} < k <= #{Y >= PML(R)}."""
+    from paper_1606_04473_b200 import ara
+    kw = {"int_cap": int_cap} if int_cap else {}
+    w = synth.get_config("tiny").with_(n_trials=5003, rho=0.02, **kw)
+    layers = (w.layers[0], w.layers[0].__class__(0, 3, 1e5, 4e5, 0.0, INF))
+    off, ids, elts = make_inputs(w)
+    orc = run_oracle(off, ids, elts, w, layers)
+    R = (1, 2, 5, 10, 100, 1000, 5003)
+    with ara.Context(w.catalog) as ctx:
+        ctx.load_elts(*elts, w.elt_terms())
+        ctx.load_yet(w.n_trials, 0, off, ids)
+        ylt, _, _ = ctx.run_host(layers)
+        k, pml, _, _ = ctx.metrics(R)
+        vals = np.unique(ylt)
+        x = np.sort(np.concatenate([[-INF, -1.0, 0.0], vals[:: max(1, len(vals) // 500)],
+                                    np.quantile(ylt, np.linspace(0, 1, 300)), [ylt.max(), ylt.max() * 2, INF]]))
+        counts = ctx.ep_curve(x)
+        assert counts.shape == (len(layers) + 1, len(x))
+        for r in range(len(layers) + 1):
+            assert np.array_equal(counts[r], oracle.ep_counts(ylt[r], x))
+            if int_cap:
+                rows = list(orc["ylt"]) + [orc["portfolio"]]
+                assert np.array_equal(counts[r], oracle.ep_counts(rows[r], x))
+            above = ctx.ep_curve(pml[r])[r]
+            at_or_above = ctx.ep_curve(np.nextafter(pml[r], -INF))[r]
+            assert (above < k).all() and (k <= at_or_above).all()
+        assert counts[:, 0].tolist() == [w.n_trials] * (len(layers) + 1) and (counts[:, -1] == 0).all()
+        for bad, status in (([2.0, 1.0], ara.ARA_ERR_DOMAIN), ([0.0, np.nan], ara.ARA_ERR_DOMAIN)):
+            with pytest.raises(ara.AraError) as e:
+                ctx.ep_curve(bad)
+            assert e.value.status == status
+        with pytest.raises(ara.AraError) as e:
+            ctx.ep_curve([])
+        assert e.value.status == ara.ARA_ERR_INVALID_ARG

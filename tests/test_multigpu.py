@@ -14,6 +14,7 @@ from parity_util import make_inputs, run_gpu
 
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
 
 
 def _ngpu():
@@ -68,10 +69,13 @@ def test_sharded_run_matches_single_gpu(cuda, tmp_path, name, n_trials, rho, p2p
     R = [x for x in w.return_periods if x <= w.n_trials]
     ylt, _, _, met = run_gpu(off, ids, elts, w, w.layers, return_periods=R)
     assert np.array_equal(got["ylt"], ylt)
+    import oracle
+    from mgpu_worker import EP_X
+    for r in range(ylt.shape[0]):   # EP curve: the all-reduced shard counts == a count over the global YLT
+        assert np.array_equal(got["ep"][r], oracle.ep_counts(ylt[r], EP_X))
     assert np.array_equal(got["pml"], met[1]) and np.array_equal(got["k"], met[0])
     assert np.allclose(got["tvar"], met[2], rtol=1e-12, atol=0)
     # the second and third consecutive runs (other terms, then the first again)
-    sys.path.insert(0, HERE)
     from mgpu_worker import bumped_layers
     ylt_b, _, _, met_b = run_gpu(off, ids, elts, w, bumped_layers(w.layers), return_periods=R)
     assert np.array_equal(got["ylt_b"], ylt_b) and np.array_equal(got["pml_b"], met_b[1])

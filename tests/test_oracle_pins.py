@@ -353,3 +353,30 @@ def test_programs_closed_forms():
     for bad in ([0, 2, 2, 4], [1, 4], [0, 3]):
         with pytest.raises(ValueError):
             oracle.programs(r["ylt"], bad)
+
+
+# ------------------------------------------------- EP curve
+def test_ep_counts_against_sorted_search_and_pml():
+    """A23: counts[i] = #{t : y[t] > x_i}.  Pinned against an independent
+    method (binary search in the sorted YLT), closed forms (a threshold below
+    every loss counts all T years, one at or above the maximum counts none,
+    thresholds at each distinct loss count the strictly larger ones), the
+    curve's monotonicity, and its relation to the oracle's PML: with
+    k = ceil(T/R), #{Y > PML(R)} < k <= #{Y >= PML(R)}.  Catches >= for >,
+    an off-by-one count, a reversed threshold order."""
+    rng = np.random.default_rng(23)
+    for it in range(300):
+        T = int(rng.integers(1, 60))
+        y = rng.integers(0, 9, size=T).astype(np.float64) * float(rng.choice([1.0, 0.5, 1e6]))
+        x = np.sort(np.concatenate([rng.uniform(-1, y.max() + 1, 5), y[: min(T, 4)], [-1.0, y.max()]]))
+        got = oracle.ep_counts(y, x)
+        s = np.sort(y)
+        want = T - np.searchsorted(s, x, side="right")      # #{y > x}
+        assert np.array_equal(got, want)
+        assert got[0] == T and got[-1] == 0                  # x = -1 and x = max
+        assert (np.diff(got.astype(np.int64)) <= 0).all()     # non-increasing in x
+        R = float(rng.integers(1, T + 1))
+        k, pml, _ = oracle.metrics(y, [R])
+        above = int(oracle.ep_counts(y, [pml[0]])[0])
+        at_or_above = T - int(np.searchsorted(s, pml[0], side="left"))
+        assert above < int(k[0]) <= at_or_above

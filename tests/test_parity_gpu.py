@@ -504,3 +504,21 @@ def test_cross_trial_rounds_short_and_empty_trials(cuda, variant, rho):
     ylt_i, lossy_i, _, _ = run_gpu(off, ids, elts_i, wi, wi.layers, variant=variant)
     assert np.array_equal(ylt_i[:-1], orc_i["ylt"]) and np.array_equal(ylt_i[-1], orc_i["portfolio"])
     assert np.array_equal(lossy_i, orc_i["lossy"])
+
+
+@pytest.mark.parametrize("rho", [0.02, 1.0])
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_l2_persisting_window(cuda, rho, precision):
+    """cfg.l2_persist: an L2 access-policy window over the packed rows (sparse
+    kernel) or the layer's column block (dense kernels) during ara_run --
+    a cache hint only: the oracle's YLT and counts, and the same bits as
+    without the window."""
+    w = synth.get_config("tiny").with_(rho=rho, n_trials=2000, catalog=50_000, n_elts=6)
+    off, ids, elts = make_inputs(w)
+    orc = run_oracle(off, ids, elts, w, w.layers, fp32=precision == "f32")
+    ylt, lossy, _, met = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10),
+                                 l2_persist=True)
+    assert_ylt_close(ylt, orc)
+    assert np.array_equal(lossy, orc["lossy"])
+    ref, ref_lossy, _, _ = run_gpu(off, ids, elts, w, w.layers, precision=precision)
+    assert np.array_equal(ylt, ref) and np.array_equal(lossy, ref_lossy)

@@ -74,5 +74,13 @@ for rho in (0.01, 0.1, 0.3):
 w = synth.get_config("mini").with_(n_trials=20000, rho=0.01)
 off, ids, elts = make_inputs(w)
 check("mini rho=0.01", off, ids, elts, w, w.layers)
+# the paper's 2M-event catalogue (bitmap larger than shared memory: L1/L2 probes), 12k trials
+for prec in ("f64", "f32"):
+    w = synth.get_config("paper").with_(n_trials=12000)
+    off, ids, elts = make_inputs(w)
+    check("paper 12k trials", off, ids, elts, w, w.layers, prec)
+w = synth.get_config("tower").with_(n_trials=6000)
+off, ids, elts = make_inputs(w)
+check("tower 6k trials", off, ids, elts, w, w.layers)
 print("FAILS", fails)
 sys.exit(1 if fails else 0)
