@@ -13,11 +13,22 @@
 #include <new>
 #include <thread>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ara_internal.cuh"
 
 using namespace ara;
 
 namespace {
+
+// NVTX range around each API call and each streamed chunk (host side: the
+// enqueue structure; an nsys timeline pairs it with the copy / kernel rows)
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
+};
 
 ara_status fail(ara_ctx* ctx, ara_status st, const char* fmt, ...) {
     if (ctx) {
@@ -191,6 +202,7 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
     if (const char* v = getenv("ARA_NO_SKIP")) ctx->no_skip = atoi(v) != 0;
     if (const char* v = getenv("ARA_NO_P2P")) ctx->use_p2p = atoi(v) == 0;
     if (const char* v = getenv("ARA_METRICS_DIST")) ctx->metrics_dist = atoi(v);
+    if (const char* v = getenv("ARA_METRICS_FAST")) ctx->metrics_fast = atoi(v);
     if (const char* v = getenv("ARA_LOOPBACK")) {
         int w = 0, r = 0;
         if (cfg->world != 1 || sscanf(v, "%d,%d", &w, &r) != 2 || w < 1 || w > ara::kMaxPeers || r < 0 || r >= w) {
@@ -261,6 +273,7 @@ extern "C" void ara_destroy(ara_ctx* ctx) {
     cudaFree(ctx->d_lossy);
     cudaFree(ctx->d_fold);
     cudaFree(ctx->d_ep);
+    cudaFree(ctx->d_mfast);
     cudaFree(ctx->d_sp_off);
     cudaFree(ctx->d_sp_ev);
     cudaFree(ctx->d_sp_ls);
@@ -416,6 +429,7 @@ void set_l2_window(ara_ctx* ctx, const void* base, size_t bytes) {
 extern "C" ara_status ara_load_elts(ara_ctx* ctx, uint32_t n_elts, const uint64_t* elt_offsets,
                                     const uint32_t* event_ids, const double* losses,
                                     const ara_elt_terms* terms) {
+    Nvtx nvtx_("ara_load_elts");
     if (!ctx) return ARA_ERR_INVALID_ARG;
     CK(cudaSetDevice(ctx->device));
     if (n_elts == 0 || n_elts > 65535) return fail(ctx, ARA_ERR_INVALID_ARG, "n_elts must be in [1, 65535]");
@@ -493,6 +507,7 @@ namespace {
 // ara_load_yet_packed (bits > 0: bit-packed ids, unpacked on the device).
 ara_status load_yet_impl(ara_ctx* ctx, uint64_t n_trials_global, uint64_t first_trial, uint64_t n_trials_local,
                          const uint64_t* trial_offsets, const uint32_t* event_ids, uint32_t bits) {
+    Nvtx nvtx_("ara_load_yet");
     if (!ctx) return ARA_ERR_INVALID_ARG;
     CK(cudaSetDevice(ctx->device));
     if (n_trials_global == 0) return fail(ctx, ARA_ERR_INVALID_ARG, "n_trials_global must be >= 1");
@@ -818,6 +833,7 @@ ara_status p2p_ensure(ara_ctx* ctx, size_t need) {
 
 ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint32_t n_programs,
                     const uint32_t* program_layers, double* ylt, uint32_t* lossy, ara_run_stats* stats) {
+    Nvtx nvtx_("ara_run");
     const uint32_t world = (uint32_t)ctx->world;
     const uint64_t T_local = ctx->T_local, T_global = ctx->T_global;
 
@@ -890,7 +906,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     }
     cudaStream_t s = ctx->stream;
     CK(cudaEventRecord(ctx->ev[0], s));
-    CK(cudaMemsetAsync(ctx->d_err, 0, sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(ctx->d_err, 0, 16, s));   // error word + the sparse kernel's gathered-slot counter
 
     // Chunk plan: CHUNKED streams the host YET in whole-trial chunks on the copy
     // stream, each chunk's kernels waiting only for that chunk.
@@ -1007,6 +1023,8 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     base.ld = ld;
     base.lossy = d_lossy;
     base.err = ctx->d_err;
+    base.n_gathered = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(ctx->d_err) + 8);
+    uint32_t bc_launches = 0;   // launches of the sparse kernel (their gathered slots are counted)
     base.portfolio_row = n_layers + n_programs;
     uint32_t launches = 0;
     int used_variant = fold ? -2 : -1;
@@ -1069,6 +1087,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         }
     }
     for (size_t c = 0; c < chunks.size(); ++c) {
+        Nvtx nvtx_chunk(stream_in ? "ara_run chunk" : "ara_run launch");
         if (stream_in) CK(cudaStreamWaitEvent(s, chunk_ev[c], 0));
         if (stream_in && ctx->h_packed) {   // F3: unpack this chunk's ids on the device
             const uint64_t e0 = ho_chunk[c], e1 = ho_chunk[c + 1];
@@ -1137,6 +1156,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 if (variant < 0 && p.bm) variant = 30;
                 if (variant != 30) p.bm = nullptr, p.pk = nullptr;   // the dense kernels read every row
                 used_occupancy = p.bm ? (double)ctx->occ_rows[g.q0 / spb] / ((double)ctx->catalog + 1.0) : 1.0;
+                if (variant == 30) ++bc_launches;
                 if (variant < 0) variant = (!fp32 && g.nsec <= 4) ? 12 : (g.nl == 1 ? 5 : 0);
                 used_variant = variant;
                 if (ctx->l2_persist) {
@@ -1226,7 +1246,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         CK(cudaMemcpy2DAsync(lossy, T_local * sizeof(uint32_t), d_lossy, ld * sizeof(uint32_t),
                              T_local * sizeof(uint32_t), n_layers, kind, s));
     }
-    if (world == 1) CK(cudaMemcpyAsync(ctx->h_small, ctx->d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->h_small + 4, ctx->d_err, 16, cudaMemcpyDeviceToHost, s));   // [4] error word, [5] gathered
     if (T_local) {
         CK(cudaMemcpyAsync(ctx->h_small + 1, ctx->d_off, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(ctx->h_small + 2, ctx->d_off + T_local, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
@@ -1234,7 +1254,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     CK(cudaEventRecord(ctx->ev[5], s));
     CK(cudaStreamSynchronize(s));
     if (stream_in) CK(cudaStreamSynchronize(ctx->copy_stream));
-    const uint32_t bits = (uint32_t)(ctx->h_small[0] & 0xffffffffu);
+    const uint32_t bits = (uint32_t)(ctx->h_small[world == 1 ? 4 : 0] & 0xffffffffu);   // world > 1: all-reduced
     st = device_errors(ctx, bits);
     if (st != ARA_OK) {
         ctx->last_layers = 0;
@@ -1261,7 +1281,10 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         stats->h2d_bytes = h2d_bytes;
         stats->n_kernel_launches = launches;
         stats->kernel_variant = used_variant;
-        stats->occupancy = used_occupancy;
+        // fraction of events whose packed slot the sparse kernel gathered (its
+        // shared-memory filter's pair part adds the unoccupied partners of
+        // occupied rows), else the table's occupied-row fraction / 1.0
+        stats->occupancy = bc_launches && nev ? (double)ctx->h_small[5] / ((double)nev * bc_launches) : used_occupancy;
     }
     return ARA_OK;
 }
@@ -1271,6 +1294,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
 // ============================================================ metrics
 extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* return_periods, uint64_t* k,
                                   double* pml, double* tvar, double* device_ms) {
+    Nvtx nvtx_("ara_metrics");
     if (!ctx) return ARA_ERR_INVALID_ARG;
     CK(cudaSetDevice(ctx->device));
     if (ctx->last_layers == 0) return fail(ctx, ARA_ERR_STATE, "no successful ara_run yet");
@@ -1317,6 +1341,11 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
         CK(launch_metrics_dist(ctx->d_ylt_local, Tl, ctx->last_ld_local, rows, n_rp, hk,
                                ctx->ms, nb, ctx->comm, s, &nerr));
         if (nerr) return fail(ctx, ARA_ERR_NCCL, "NCCL all-reduce in the distributed metrics failed");
+    } else if (ctx->metrics_fast && n_rp <= kFastMaxRp) {
+        const size_t need = metrics_fast_bytes(rows, n_rp, T, nblk);
+        ara_status ast = ensure(ctx, ctx->d_mfast, ctx->mfast_cap, need);
+        if (ast != ARA_OK) return ast;
+        CK(launch_metrics_fast(d_y, T, ld, rows, n_rp, hk, ctx->d_mfast, nblk, ctx->ms.out, s));
     } else {
         CK(launch_metrics(d_y, T, ld, rows, n_rp, hk, ctx->ms, nblk, s));
     }
@@ -1337,6 +1366,7 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
 
 // ============================================================ EP curve
 extern "C" ara_status ara_ep_curve(ara_ctx* ctx, uint32_t n_points, const double* thresholds, uint64_t* counts) {
+    Nvtx nvtx_("ara_ep_curve");
     if (!ctx) return ARA_ERR_INVALID_ARG;
     CK(cudaSetDevice(ctx->device));
     if (ctx->last_layers == 0) return fail(ctx, ARA_ERR_STATE, "no successful ara_run yet");

@@ -103,6 +103,7 @@ struct TrialParams {
     uint32_t portfolio_row;
     uint32_t* lossy;            // [.. rows][ld] or null
     uint32_t* err;              // device error word
+    unsigned long long* n_gathered;   // trial_kernel_bc: packed slots gathered (added per warp), or null
     double* fold;               // fold mode: per-event occurrence-net losses, [C+1][fold_stride] per chunk
     uint32_t fold_stride;       // doubles per fold row (layers of one chunk, power of two <= 8)
     uint32_t fold_col0;         // fold column of the launch's first layer
@@ -169,6 +170,13 @@ cudaError_t metrics_alloc(MetricsScratch& m, uint32_t rows, uint32_t n_rp, int n
 void metrics_free(MetricsScratch& m);
 cudaError_t launch_metrics(const double* d_ylt, uint64_t T, uint64_t ld, uint32_t rows,
                            uint32_t n_rp, const uint64_t* h_k, MetricsScratch& m, int nblk, cudaStream_t s);
+// The same PML / TVaR in four kernels (metrics_fast.cu): two 12-bit radix
+// passes, candidate compaction + tail sums, exact finish per candidate bin.
+// n_rp <= kFastMaxRp; scratch of metrics_fast_bytes(); results [rows][n_rp][2] in d_out.
+constexpr uint32_t kFastMaxRp = 12;
+size_t metrics_fast_bytes(uint32_t rows, uint32_t n_rp, uint64_t T, int nblk);
+cudaError_t launch_metrics_fast(const double* d_ylt, uint64_t T, uint64_t ld, uint32_t rows, uint32_t n_rp,
+                                const uint64_t* h_k, void* scratch, int nblk, double* d_out, cudaStream_t s);
 // Distributed select: each rank histograms its own YLT shard
 // [rows][T_local] (row stride ld); the per-pass histograms and the tail sums are
 // all-reduced over `comm`, so every rank derives the same global PML/TVaR
@@ -264,6 +272,9 @@ struct ara_ctx {
     int lb_world = 0, lb_rank = 0;
     unsigned char* d_ep = nullptr;    // EP-curve scratch: thresholds, histograms, counts
     size_t ep_cap = 0;
+    unsigned char* d_mfast = nullptr; // metrics_fast scratch
+    size_t mfast_cap = 0;
+    int metrics_fast = 0;             // ARA_METRICS_FAST=1: the four-kernel select (metrics_fast.cu; A/B)
     int run_mode = 0;                  // ARA_RUN_DIRECT / ARA_RUN_FOLD
     double* d_fold = nullptr;          // fold mode: per-event occurrence-net losses
     size_t fold_cap = 0;

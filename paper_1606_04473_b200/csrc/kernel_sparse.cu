@@ -44,18 +44,26 @@ namespace {
 #ifndef BC_NSTG
 #define BC_NSTG 2
 #endif
+#ifndef BC_CHB
+#define BC_CHB 512
+#endif
 // Warps per CTA (one CTA per SM) by layers per launch, measured
 // (profiles/r02_ab_bc_warps.txt): the loop is latency-bound, so as many warps
 // as the registers allow -- 32 for one layer (64 registers), 24 for towers.
 template <int NLB> struct BcWarps { static constexpr int value = NLB <= 1 ? 32 : 24; };
-template <int W>
+// Compaction queue entries per warp: 128 for one layer (32 warps: the smaller
+// queue leaves 16 KB more of the bitmap in shared memory), 256 for towers.
+template <int NLB> struct BcQueue { static constexpr int value = NLB <= 1 ? 128 : 256; };
+template <int W, int CB>
 struct BcGeo {
     static constexpr int WARPS = W;                  // per CTA, one CTA per SM
     static constexpr int THREADS = WARPS * 32;
-    static constexpr int CHB = 512;                  // bytes per id chunk = one 128-event batch
+    static constexpr int CHB = BC_CHB;               // bytes per id chunk: 1 or 2 batches of 128 ids
     static constexpr int NSTG = BC_NSTG;             // chunks per warp ring (power of two)
     static constexpr int RING = NSTG * CHB;          // id ring bytes per warp
-    static constexpr int CBUF = 256;                 // compaction ring entries per warp (>= 31 + 128)
+    // compaction queue entries per warp (power of two >= 64: a batch whose
+    // last group would overflow it has that group appended after rounds)
+    static constexpr int CBUF = CB;
     static constexpr int FIXED = WARPS * (RING + CBUF * 4);   // dynamic smem before the bitmap
 };
 
@@ -132,14 +140,16 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
 }
 
 template <typename TV, int NLB, int W = BcWarps<NLB>::value>
-__global__ void __launch_bounds__(BcGeo<W>::THREADS, 1) trial_kernel_bc(const __grid_constant__ TrialParams p) {
-    using Geo = BcGeo<W>;
+__global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_constant__ TrialParams p) {
+    using Geo = BcGeo<W, BcQueue<NLB>::value>;
     constexpr int CAP = Slot<TV>::CAP;
-    constexpr uint32_t CHE = Geo::CHB / 4;   // ids per chunk (= per batch)
+    constexpr uint32_t CHE = 128;                  // ids per batch
+    constexpr uint32_t BPC = Geo::CHB / 512;       // batches per chunk
     constexpr uint32_t NSTG = Geo::NSTG;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(16) double2 s_term[NLB][32];
     __shared__ __align__(8) uint64_t s_bar[Geo::WARPS * Geo::NSTG + 1];
+    __shared__ uintptr_t s_stream[Geo::WARPS][2];   // per warp: the id stream's 16-B aligned byte range
     const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
     const uint32_t sbase = pin((uint32_t)__cvta_generic_to_shared(smem));
     const uint32_t ring = sbase + wib * (uint32_t)Geo::RING;
@@ -213,14 +223,18 @@ __global__ void __launch_bounds__(BcGeo<W>::THREADS, 1) trial_kernel_bc(const __
     const int64_t P0 = S0 - (int64_t)((a_s - a0) >> 2);
     if (S1 - P0 > (int64_t)0x7fffff00) { err |= ERRBIT_OFFSETS; te = tb; S1 = S0; }   // > 2^31 events in one warp
     const uint32_t nchunks = S1 > S0 ? (uint32_t)((aend - a0 + Geo::CHB - 1) / Geo::CHB) : 0u;
-    const uint64_t pol = policy_evict_first();
+    // the stream's byte range lives in shared memory (lane 0 reads it when it
+    // refills a stage), not in registers
+    if (lane == 0) { s_stream[wib][0] = a0; s_stream[wib][1] = aend; }
     // chunk c goes to stage c % NSTG; only the stream's last chunk is short
     auto issue_chunk = [&](uint32_t c) {   // lane 0
-        const uintptr_t src = a0 + (uintptr_t)c * Geo::CHB;
-        const uint32_t bytes = c + 1 < nchunks ? (uint32_t)Geo::CHB : (uint32_t)(aend - src);
+        const uintptr_t b0 = s_stream[wib][0], b1 = s_stream[wib][1];
+        const uintptr_t src = b0 + (uintptr_t)c * Geo::CHB;
+        const uint32_t bytes = c + 1 < nchunks ? (uint32_t)Geo::CHB : (uint32_t)(b1 - src);
         const uint32_t st = c & (NSTG - 1);
         mbar_expect_tx(bar0 + 8u * st, bytes);
-        bulk_g2s(ring + st * Geo::CHB, reinterpret_cast<const void*>(src), bytes, bar0 + 8u * st, pol);
+        bulk_g2s(ring + st * Geo::CHB, reinterpret_cast<const void*>(src), bytes, bar0 + 8u * st,
+                 policy_evict_first());
     };
     if (lane == 0)
         for (uint32_t c = 0; c < NSTG && c < nchunks; ++c) issue_chunk(c);
@@ -232,21 +246,22 @@ __global__ void __launch_bounds__(BcGeo<W>::THREADS, 1) trial_kernel_bc(const __
     // stale ids: none of its positions is ever live.
     const uint32_t C = p.catalog;
     auto load_batch = [&](uint32_t c, uint32_t (&x)[4], uint32_t (&wd)[4]) {
-        const uint32_t st = c & (NSTG - 1);
-        if (c < nchunks) mbar_wait(bar0 + 8u * st, (c / NSTG) & 1u);
-        const uint32_t ra = ring + st * (uint32_t)Geo::CHB + lane * 4u;
+        const uint32_t ch = c / BPC, half = c % BPC;   // chunk, batch inside it
+        const uint32_t st = ch & (NSTG - 1);
+        if (half == 0 && ch < nchunks) mbar_wait(bar0 + 8u * st, (ch / NSTG) & 1u);
+        const uint32_t ra = ring + st * (uint32_t)Geo::CHB + half * 512u + lane * 4u;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const uint32_t v = lds32(ra + 128u * j);
-            const uint32_t xc = v - 1u < C ? v : 0u;
+            const uint32_t xc = v <= C ? v : 0u;   // (0 stays 0)
             x[j] = xc;
             wd[j] = probe(xc >> 5, Ws, s_bm, bm);
         }
-        if (c + NSTG < nchunks) {
+        if (half == BPC - 1 && ch + NSTG < nchunks) {   // the chunk's last batch: refill its stage
             __syncwarp();
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // our reads precede the refill
-                issue_chunk(c + NSTG);
+                issue_chunk(ch + NSTG);
             }
         }
     };
@@ -258,15 +273,32 @@ __global__ void __launch_bounds__(BcGeo<W>::THREADS, 1) trial_kernel_bc(const __
     for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
     Slot<TV> sl;
     bool pend = false;       // a round's slots are in flight
-    bool pend_fin = false;   // ... and it is the last round of trial pend_t
-    uint64_t pend_t = 0;
+    bool pend_fin = false;   // ... and it is the last round of trial tb + pend_i
+    uint32_t pend_i = 0;
 
     // scan the current batch over its positions [dlo, dhi): append the
     // occupied events in stream order
     // (full: the whole batch belongs to the trial -- no position masks, and
     // invalid ids are caught by a running minimum instead of a per-event test)
-    const uint32_t lt = (1u << lane) - 1u;
     uint32_t xmin = 1u;   // min over the ids of full batches (0 = an id outside [1, C])
+    // append the occupied events of one group (ballot Mj), in stream order
+    auto append = [&](uint32_t Mj, uint32_t xj) {
+        uint32_t ltm;
+        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(ltm));
+        const uint32_t slot = (tail + __popc(Mj & ltm)) & (uint32_t)(Geo::CBUF - 1);
+        // predicated store (no branch around it)
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}" ::"r"(
+                         cbuf + slot * 4u),
+                     "r"(xj), "r"((Mj >> lane) & 1u)
+                     : "memory");
+        tail += __popc(Mj);
+    };
+    uint32_t M3 = 0;   // a deferred group 3 (its ballot), or 0
+    // scan the current batch over its positions [dlo, dhi): append the
+    // occupied events in stream order.  Groups 0-2 always fit the queue (it
+    // holds < 32 entries when a batch starts); group 3 is appended only if it
+    // fits, else its ballot is kept (M3) and it is appended after rounds have
+    // drained the queue (densely occupied batches only).
     auto scan = [&](bool full, uint32_t dlo, uint32_t dhi, const uint32_t (&x)[4], const uint32_t (&wd)[4]) {
         const uint32_t span = dhi - dlo;
 #pragma unroll
@@ -279,8 +311,11 @@ __global__ void __launch_bounds__(BcGeo<W>::THREADS, 1) trial_kernel_bc(const __
             asm("shf.r.wrap.b32 %0, %1, %1, %2;" : "=r"(r) : "r"(wd[j]), "r"(x[j]));
             const bool occ = live && (r & 1u);
             const uint32_t M = __ballot_sync(0xffffffffu, occ);
-            if (occ) sts32(cbuf + ((tail + __popc(M & lt)) & (uint32_t)(Geo::CBUF - 1)) * 4u, x[j]);
-            tail += __popc(M);
+            if (j == 3 && tail - head + __popc(M) > (uint32_t)Geo::CBUF) {
+                M3 = M;
+                break;
+            }
+            append(M, x[j]);
         }
     };
     // a7 tree + a8 stores of trial t (lane 0), accumulators reset
@@ -312,13 +347,29 @@ __global__ void __launch_bounds__(BcGeo<W>::THREADS, 1) trial_kernel_bc(const __
                 }
             }
         };
-        if (__popc(mask) <= CAP) {
-            // the slot holds all of the row's non-zeros: walk them in column order
+        const bool fits = __popc(mask) <= CAP;
+        if (__all_sync(0xffffffffu, fits)) {
+            // every lane's slot holds all of its row's non-zeros (the common
+            // case): walk them in column order, the v-th from slot value v --
+            // unrolled, so v is a register name, and branch-free: a lane whose
+            // walk has ended (or whose column is outside the window) adds
+            // terms(0) = +0, which leaves l_e unchanged (every deductible >= 0)
+            uint32_t mm = mask;
+#pragma unroll
+            for (int v = 0; v < CAP; ++v) {
+                if (!__any_sync(0xffffffffu, mm != 0u)) break;
+                const uint32_t b = (uint32_t)(__ffs(mm) - 1);   // 0xffffffff when mm == 0
+                mm &= mm - 1u;
+                const uint32_t j = b - p.pk_col0;                // window element (wraps when b < col0)
+                const bool in = j < 32u && ((p.pk_wmask >> j) & 1u);
+                add(in ? sl.val((uint32_t)v) : 0.0, in ? j : 0u);
+            }
+        } else if (fits) {
             uint32_t mm = mask, v = 0;
             while (mm) {
                 const uint32_t b = (uint32_t)(__ffs(mm) - 1);
                 mm &= mm - 1u;
-                const uint32_t j = b - p.pk_col0;   // window element (wraps when b < col0)
+                const uint32_t j = b - p.pk_col0;
                 if (j < 32u && ((p.pk_wmask >> j) & 1u)) add(sl.val(v), j);
                 ++v;
             }
@@ -344,11 +395,11 @@ __global__ void __launch_bounds__(BcGeo<W>::THREADS, 1) trial_kernel_bc(const __
         }
         if (pend_fin) {
             pend_fin = false;
-            finalize(pend_t);
+            finalize(tb + pend_i);
         }
     };
     // issue a round of trial t: up to 32 queued events, entry head + i to lane i
-    auto issue_round = [&](uint64_t t) {
+    auto issue_round = [&](uint32_t i) {   // a round of trial tb + i
         __syncwarp();   // the scan's appends (other lanes' stores) are visible
         const uint32_t nr = tail - head < 32u ? tail - head : 32u;
         if (lane < nr) {
@@ -359,7 +410,7 @@ __global__ void __launch_bounds__(BcGeo<W>::THREADS, 1) trial_kernel_bc(const __
         }
         head += nr;
         pend = true;
-        pend_t = t;
+        pend_i = i;
     };
 
     // two register sets, A and B, alternate between the current batch and the
@@ -370,14 +421,22 @@ __global__ void __launch_bounds__(BcGeo<W>::THREADS, 1) trial_kernel_bc(const __
     uint32_t c = 0;                                   // current batch
     uint32_t rlo = (uint32_t)(S0 - P0);               // next position of the stream
     const uint32_t rS1 = (uint32_t)(S1 - P0);
-    uint64_t o_hi = te > tb ? __ldg(p.off + tb + 1) : 0;   // off[t + 1] of the current trial
+    const uint64_t B0 = base + (uint64_t)P0;          // offset value of stream position 0
+    // trial tb + i ends at stream position rhi; the end of the next trial is
+    // loaded one trial ahead (o_nx) and converted when that trial starts
+    const uint32_t nt = te - tb < 0xffffffffull ? (uint32_t)(te - tb) : 0u;   // (a warp never holds 2^32 trials)
+    auto to_pos = [&](uint64_t o) {   // offset value -> 32-bit stream position, validated
+        const int64_t h = (int64_t)(o - B0);
+        uint32_t r = (uint32_t)h;
+        if (h < (int64_t)rlo) { err |= ERRBIT_OFFSETS; r = rlo; }
+        if (r > rS1) { err |= ERRBIT_OFFSETS; r = rS1 > rlo ? rS1 : rlo; }
+        return r;
+    };
+    uint64_t o_nx = nt ? __ldg(p.off + tb + 1) : 0;
 #pragma unroll 1
-    for (uint64_t t = tb; t < te; ++t) {
-        const uint64_t o_nx = t + 2 <= te ? __ldg(p.off + t + 2) : 0;   // next trial's end, one trial ahead
-        const int64_t hi64 = (int64_t)(o_hi - base) - P0;
-        uint32_t rhi = (uint32_t)hi64;
-        if (o_hi < base || hi64 < (int64_t)rlo) { err |= ERRBIT_OFFSETS; rhi = rlo; }
-        if (rhi > rS1) { err |= ERRBIT_OFFSETS; rhi = rS1 > rlo ? rS1 : rlo; }
+    for (uint32_t i = 0; i < nt; ++i) {
+        const uint32_t rhi = to_pos(o_nx);
+        if (i + 1 < nt) o_nx = __ldg(p.off + tb + i + 2);   // the next trial's end, one trial ahead
 #pragma unroll 1
         for (;;) {
             const uint32_t bs = c * CHE;
@@ -394,9 +453,15 @@ __global__ void __launch_bounds__(BcGeo<W>::THREADS, 1) trial_kernel_bc(const __
             }
             const bool fin = rhi <= bs + CHE;   // the trial ends in this batch
 #pragma unroll 1
-            while (tail - head >= 32u || (fin && tail != head)) {
-                if (pend) consume();
-                issue_round(t);
+            for (;;) {
+#pragma unroll 1
+                while (tail - head >= 32u || (fin && tail != head && !M3)) {
+                    if (pend) consume();
+                    issue_round(i);
+                }
+                if (!M3) break;
+                append(M3, (c & 1u) ? xb[3] : xa[3]);   // the deferred group 3 now fits
+                M3 = 0;
             }
             if (fin) break;
             // the finished batch's set receives batch c + 2
@@ -404,31 +469,40 @@ __global__ void __launch_bounds__(BcGeo<W>::THREADS, 1) trial_kernel_bc(const __
             else load_batch(c + 2, xa, wa);
             ++c;
         }
-        if (pend && pend_t == t) {
+        if (pend && pend_i == i) {
             pend_fin = true;   // finished when the next round is issued (or at the end)
         } else {
             if (pend) consume();   // the previous trial's last round (finalises it)
-            finalize(t);           // no round of t in flight: its sum is complete
+            finalize(tb + i);      // no round of the trial in flight: its sum is complete
         }
         rlo = rhi;
-        o_hi = o_nx;
     }
     if (pend) consume();
     // every issued chunk has landed before the CTA's shared memory is released
-    const uint32_t loaded = c + 2 < nchunks ? c + 2 : nchunks;
-    for (uint32_t cc = loaded; cc < nchunks && cc < loaded + NSTG; ++cc)
-        mbar_wait(bar0 + 8u * (cc & (NSTG - 1)), (cc / NSTG) & 1u);
+    // (batches 0 .. c+1 were loaded: chunks 0 .. (c+1)/BPC waited for; the
+    // (c+2)/BPC chunks whose last batch was loaded each issued a refill)
+    const uint32_t waited_ch = (c + 1) / BPC + 1;
+    const uint32_t loaded = waited_ch < nchunks ? waited_ch : nchunks;
+    const uint32_t issued = NSTG + (c + 2) / BPC < nchunks ? NSTG + (c + 2) / BPC : nchunks;
+    for (uint32_t cc = loaded; cc < issued; ++cc) mbar_wait(bar0 + 8u * (cc & (NSTG - 1)), (cc / NSTG) & 1u);
     if (xmin == 0u) err |= ERRBIT_EVENT_RANGE;
+    if (lane == 0 && p.n_gathered && tail) atomicAdd(p.n_gathered, (unsigned long long)tail);   // queue entries = gathers
     peer_fence(p);
     if (err) atomicOr(p.err, err);
 }
 
+template <typename TV, int NLB>
+void* pick_bc_nl(int* warps, int* fixed) {
+    using Geo = BcGeo<BcWarps<NLB>::value, BcQueue<NLB>::value>;
+    *warps = Geo::WARPS;
+    *fixed = Geo::FIXED;
+    return (void*)trial_kernel_bc<TV, NLB>;
+}
 template <typename TV>
-void* pick_bc(int nl, int* warps) {
-    if (nl <= 1) { *warps = BcWarps<1>::value; return (void*)trial_kernel_bc<TV, 1>; }
-    if (nl <= 2) { *warps = BcWarps<2>::value; return (void*)trial_kernel_bc<TV, 2>; }
-    *warps = BcWarps<4>::value;
-    return (void*)trial_kernel_bc<TV, 4>;
+void* pick_bc(int nl, int* warps, int* fixed) {
+    if (nl <= 1) return pick_bc_nl<TV, 1>(warps, fixed);
+    if (nl <= 2) return pick_bc_nl<TV, 2>(warps, fixed);
+    return pick_bc_nl<TV, 4>(warps, fixed);
 }
 
 }  // namespace
@@ -438,9 +512,9 @@ void* pick_bc(int nl, int* warps) {
 cudaError_t launch_trials_bc(const TrialParams& p, int fp32, int grid, cudaStream_t s) {
     if (p.t_end <= p.t_begin) return cudaSuccess;
     if (!p.bm || !p.pk) return cudaErrorInvalidValue;
-    int warps = 16;
-    void* fn = fp32 ? pick_bc<float>((int)p.n_layers, &warps) : pick_bc<double>((int)p.n_layers, &warps);
-    const int fixed = warps * (BcGeo<16>::RING + BcGeo<16>::CBUF * 4);   // per-warp rings are W-independent
+    int warps = 16, fixed = 0;
+    void* fn = fp32 ? pick_bc<float>((int)p.n_layers, &warps, &fixed)
+                    : pick_bc<double>((int)p.n_layers, &warps, &fixed);
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);

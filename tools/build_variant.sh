@@ -5,7 +5,8 @@
 set -e
 cd "$(dirname "$0")/.."
 NAME=$1; SRC=${2:-paper_1606_04473_b200/csrc/kernel_sparse.cu}; shift; shift || true
-make -s -j8 build/ara_host.o build/kernel_dense.o build/kernel_fold.o build/densify.o build/metrics.o >/dev/null
+OBJS="build/ara_host.o build/kernel_dense.o build/kernel_fold.o build/densify.o build/metrics.o build/ep_curve.o"
+make -s -j8 $OBJS >/dev/null
 SITE=$(python -c "import sysconfig;print(sysconfig.get_paths()['purelib'])")
 NCCL=$SITE/nvidia/nccl
 mkdir -p ab build/ab
@@ -14,6 +15,6 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler
   -Ipaper_1606_04473_b200/csrc -I$NCCL/include --expt-relaxed-constexpr --fmad=false -Xptxas -v "$@" \
   -dc -o build/ab/kernel_sparse_$NAME.o build/ab/kernel_sparse_$NAME.cu 2> build/ab/$NAME.ptxas.log
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -Xcompiler -fPIC -o ab/$NAME.so \
-  build/ara_host.o build/ab/kernel_sparse_$NAME.o build/kernel_dense.o build/kernel_fold.o build/densify.o build/metrics.o \
+  build/ab/kernel_sparse_$NAME.o $OBJS \
   -L$NCCL/lib -l:libnccl.so.2 -Xlinker -rpath=$NCCL/lib
 grep -A2 "trial_kernel_bcIdLi1E" build/ab/$NAME.ptxas.log | grep Used || true
