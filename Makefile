@@ -11,8 +11,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall 
 PKG       := paper_1606_04473_b200
 CSRC      := $(PKG)/csrc
 CU_SRCS   := $(CSRC)/ara_host.cu $(CSRC)/kernel_sparse.cu $(CSRC)/kernel_dense.cu $(CSRC)/kernel_fold.cu \
-             $(CSRC)/densify.cu $(CSRC)/metrics.cu $(CSRC)/metrics_fast.cu \
-             $(CSRC)/ep_curve.cu
+             $(CSRC)/densify.cu $(CSRC)/metrics.cu $(CSRC)/ep_curve.cu
 CU_OBJS   := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
 
 all: oracle/liboracle.so synth/libsynth.so $(PKG)/libara.so $(PKG)/libara_mb.so

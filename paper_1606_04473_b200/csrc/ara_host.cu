@@ -202,7 +202,6 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
     if (const char* v = getenv("ARA_NO_SKIP")) ctx->no_skip = atoi(v) != 0;
     if (const char* v = getenv("ARA_NO_P2P")) ctx->use_p2p = atoi(v) == 0;
     if (const char* v = getenv("ARA_METRICS_DIST")) ctx->metrics_dist = atoi(v);
-    if (const char* v = getenv("ARA_METRICS_FAST")) ctx->metrics_fast = atoi(v);
     if (const char* v = getenv("ARA_LOOPBACK")) {
         int w = 0, r = 0;
         if (cfg->world != 1 || sscanf(v, "%d,%d", &w, &r) != 2 || w < 1 || w > ara::kMaxPeers || r < 0 || r >= w) {
@@ -273,7 +272,6 @@ extern "C" void ara_destroy(ara_ctx* ctx) {
     cudaFree(ctx->d_lossy);
     cudaFree(ctx->d_fold);
     cudaFree(ctx->d_ep);
-    cudaFree(ctx->d_mfast);
     cudaFree(ctx->d_sp_off);
     cudaFree(ctx->d_sp_ev);
     cudaFree(ctx->d_sp_ls);
@@ -1341,11 +1339,6 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
         CK(launch_metrics_dist(ctx->d_ylt_local, Tl, ctx->last_ld_local, rows, n_rp, hk,
                                ctx->ms, nb, ctx->comm, s, &nerr));
         if (nerr) return fail(ctx, ARA_ERR_NCCL, "NCCL all-reduce in the distributed metrics failed");
-    } else if (ctx->metrics_fast && n_rp <= kFastMaxRp) {
-        const size_t need = metrics_fast_bytes(rows, n_rp, T, nblk);
-        ara_status ast = ensure(ctx, ctx->d_mfast, ctx->mfast_cap, need);
-        if (ast != ARA_OK) return ast;
-        CK(launch_metrics_fast(d_y, T, ld, rows, n_rp, hk, ctx->d_mfast, nblk, ctx->ms.out, s));
     } else {
         CK(launch_metrics(d_y, T, ld, rows, n_rp, hk, ctx->ms, nblk, s));
     }

@@ -170,13 +170,6 @@ cudaError_t metrics_alloc(MetricsScratch& m, uint32_t rows, uint32_t n_rp, int n
 void metrics_free(MetricsScratch& m);
 cudaError_t launch_metrics(const double* d_ylt, uint64_t T, uint64_t ld, uint32_t rows,
                            uint32_t n_rp, const uint64_t* h_k, MetricsScratch& m, int nblk, cudaStream_t s);
-// The same PML / TVaR in four kernels (metrics_fast.cu): two 12-bit radix
-// passes, candidate compaction + tail sums, exact finish per candidate bin.
-// n_rp <= kFastMaxRp; scratch of metrics_fast_bytes(); results [rows][n_rp][2] in d_out.
-constexpr uint32_t kFastMaxRp = 12;
-size_t metrics_fast_bytes(uint32_t rows, uint32_t n_rp, uint64_t T, int nblk);
-cudaError_t launch_metrics_fast(const double* d_ylt, uint64_t T, uint64_t ld, uint32_t rows, uint32_t n_rp,
-                                const uint64_t* h_k, void* scratch, int nblk, double* d_out, cudaStream_t s);
 // Distributed select: each rank histograms its own YLT shard
 // [rows][T_local] (row stride ld); the per-pass histograms and the tail sums are
 // all-reduced over `comm`, so every rank derives the same global PML/TVaR
@@ -272,9 +265,6 @@ struct ara_ctx {
     int lb_world = 0, lb_rank = 0;
     unsigned char* d_ep = nullptr;    // EP-curve scratch: thresholds, histograms, counts
     size_t ep_cap = 0;
-    unsigned char* d_mfast = nullptr; // metrics_fast scratch
-    size_t mfast_cap = 0;
-    int metrics_fast = 0;             // ARA_METRICS_FAST=1: the four-kernel select (metrics_fast.cu; A/B)
     int run_mode = 0;                  // ARA_RUN_DIRECT / ARA_RUN_FOLD
     double* d_fold = nullptr;          // fold mode: per-event occurrence-net losses
     size_t fold_cap = 0;
