@@ -1317,8 +1317,10 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
         ld = ctx->last_ld_local;
     }
     int nblk = (int)((T + 4095) / 4096);
-    static const int blk_mult = [] { const char* v = getenv("ARA_METRICS_BLOCKS"); return v ? atoi(v) : 2; }();
-    const int maxblk = (blk_mult * ctx->n_sm + (int)rows - 1) / (int)rows;
+    // grid: ARA_METRICS_BLOCKS blocks per SM over all rows (A/B knob; fractional allowed)
+    static const double blk_mult = [] { const char* v = getenv("ARA_METRICS_BLOCKS"); return v ? atof(v) : 1.0; }();
+    int maxblk = (int)(blk_mult * ctx->n_sm / rows + 0.5);
+    if (maxblk < 1) maxblk = 1;
     if (nblk > maxblk) nblk = maxblk;
     if (nblk < 1) nblk = 1;
     CK(metrics_alloc(ctx->ms, rows, n_rp, nblk > 2 * ctx->n_sm ? nblk : 2 * ctx->n_sm));   // + cooperative grid

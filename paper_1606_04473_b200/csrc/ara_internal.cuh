@@ -152,16 +152,22 @@ cudaError_t launch_ep_curve(const double* d_ylt, uint64_t T, uint64_t ld, uint32
 
 // metrics: radix select over the [rows][T] YLT (device), fixed-order tail sums
 struct MetricsScratch {
-    uint32_t* hist = nullptr;       // [rows][n_rp][256]
-    uint64_t* prefix = nullptr;     // [rows][n_rp] selected bit prefix
-    uint64_t* krem = nullptr;       // [rows][n_rp] remaining rank
-    double* part_sum = nullptr;     // [rows][n_rp][nblk]
-    uint64_t* part_cnt = nullptr;   // [rows][n_rp][nblk]
+    uint32_t* hist8 = nullptr;      // [8][rows * n_rp][256] per-pass histograms
+    uint64_t* st = nullptr;         // [2][rows * n_rp][2] prefix / remaining rank, double-buffered
+    uint32_t* strep = nullptr;      // [2][rows * n_rp] histogram slots
+    double* part_sum = nullptr;     // [rows][n_rp][nblk] tail-sum partials per block
+    uint64_t* part_cnt = nullptr;
     double* out = nullptr;          // [rows][n_rp][2] pml, tvar
-    uint32_t* done = nullptr;       // block-completion counters
-    uint32_t* coop_hist = nullptr;  // [3][rows * n_rp][256] rotating histograms (cooperative path)
+    uint32_t* done = nullptr;       // [rows] block-completion counters
     double* dsum = nullptr;         // distributed select: tail sums / counts per (row, period)
     uint64_t* dcnt = nullptr;
+    uint64_t* cand = nullptr;       // candidate keys per warp region (fast path)
+    uint32_t* cand_n = nullptr;
+    double* bsum = nullptr;         // slot partial sums / counts per block (fast path)
+    uint64_t* bcnt = nullptr;
+    uint64_t cand_cap = 0, cand_n_cap = 0, bpart_cap = 0;
+    cudaGraphExec_t m4_exec = nullptr;   // the fast path's launch sequence, keyed by its arguments
+    unsigned char m4_key[1024] = {};
     size_t cap_rows_rp = 0;
     uint32_t cap_rows = 0;
     int nblk = 0;                   // capacity in blocks

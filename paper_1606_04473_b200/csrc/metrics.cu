@@ -2,84 +2,140 @@
 //
 // PAPER.md P:273 names PML and TVaR; readings A9/A10 fix them:
 //   k = ceil(T / R);  PML(R) = k-th largest Y;  TVaR(R) = mean of the k largest.
-// Method (hand-written, no library sort):
-//   1. MSD radix select, 8 passes of 8 bits over the u64 bit patterns of the
-//      (non-negative, canonical +0) fp64 YLT values — for non-negative doubles
-//      the bit order is the value order.  All return periods of all rows
-//      (layers + portfolio) are selected together; return periods whose
-//      current prefixes coincide share one histogram.  The last block of each
-//      row (threadfence + completion counter) picks the digit, so one launch
-//      per pass.
-//   2. One pass of masked tail sums with the selected value v:
-//      TVaR = (sum_{Y > v} Y + (k - #{Y > v}) v) / k, which equals the mean of
-//      the k largest exactly in real arithmetic (ties included); partial sums
-//      are combined in a fixed block order, so the result is deterministic.
-#include <cooperative_groups.h>
+// Method (hand-written, no library sort): an MSD radix select over the u64
+// bit patterns of the (non-negative, canonical +0) fp64 YLT values — for
+// non-negative doubles the bit order is the value order — with all return
+// periods of all rows (layers + portfolio) selected together (periods whose
+// current prefixes coincide share one histogram), then
+//   TVaR = (sum_{Y > v} Y + (k - #{Y > v}) v) / k,
+// which equals the mean of the k largest exactly in real arithmetic (ties
+// included).  Every sum is taken in a fixed order, so results are
+// deterministic.  Two launch sequences (below): the fast path (n_rp <= 11:
+// three full sweeps, then only the candidates that share the 16-bit prefix of
+// a selected value) and the general one (8 full sweeps + tail), both also in a
+// distributed form whose histograms and sums are all-reduced between launches.
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "ara_internal.cuh"
 
-namespace cg = cooperative_groups;
-
 namespace ara {
 namespace {
-
-struct MParams {
-    const double* ylt;
-    uint64_t T, ld;
-    uint32_t n_rp, nblk;
-    uint32_t* hist;      // [rows][n_rp][256]
-    uint64_t* prefix;    // [rows][n_rp]
-    uint64_t* krem;      // [rows][n_rp]
-    uint32_t* rep;       // [rows][n_rp]
-    double* part_sum;    // [rows][n_rp][nblk]
-    uint64_t* part_cnt;  // [rows][n_rp][nblk]
-    double* out;         // [rows][n_rp][2]
-    uint32_t* done;      // [rows]
-    double* dsum;        // distributed mode: this rank's tail sums [rows][n_rp] ...
-    uint64_t* dcnt;      // ... and counts (all-reduced across ranks, then finished)
-    int dist;            // 1: the YLT is this rank's shard; histograms and sums are all-reduced
-    uint64_t k[ARA_MAX_RP];
-};
 
 __device__ __forceinline__ uint64_t key_of(double y) {
     return (uint64_t)__double_as_longlong(y + 0.0);   // canonical +0 (A16)
 }
 
-__global__ void init_kernel(const __grid_constant__ MParams P) {
-    const uint32_t row = blockIdx.x;
-    for (uint32_t i = threadIdx.x; i < P.n_rp; i += blockDim.x) {
-        P.prefix[row * P.n_rp + i] = 0;
-        P.krem[row * P.n_rp + i] = P.k[i];
-        P.rep[row * P.n_rp + i] = 0;   // all prefixes equal: share slot 0
-    }
-    for (uint32_t i = threadIdx.x; i < P.n_rp * 256u; i += blockDim.x) P.hist[(uint64_t)row * P.n_rp * 256 + i] = 0;
-    if (threadIdx.x == 0) P.done[row] = 0;
+// lane l's 8 histogram words 248-8l .. 255-8l as two 16-B loads (coalesced; every
+// block reads the same global histogram right after a pass, so sector count matters)
+__device__ __forceinline__ void hist_words(const uint32_t* h, uint32_t lane, uint32_t (&w)[8]) {
+    const uint4 a = __ldcg(reinterpret_cast<const uint4*>(h + 248 - 8 * lane));
+    const uint4 b = __ldcg(reinterpret_cast<const uint4*>(h + 252 - 8 * lane));
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
 }
 
-// Pick the digit of every return period of `row` from the row's (complete)
-// global histograms: stage them in shared memory, one warp per return period
-// scans from the top digit down; update prefix / remaining rank / reps and
-// clear the histograms.  (The last block of a pass, or select_kernel.)
-__device__ void select_row(const MParams& P, uint32_t row, int shift, uint32_t* sh, uint64_t* s_prefix) {
+// ---------------------------------------------------------------------------
+// Default path (round 2): the same MSD radix select and tail sums, organised
+// for throughput instead of latency chains.
+//  * No "last block" hand-off between passes: every block of pass p first
+//    derives the digits of pass p-1 itself from the (complete) global
+//    histogram of pass p-1 — identical inputs, identical choices — and block 0
+//    of each row records the state for the next pass (double-buffered).
+//  * No warp-synchronous match_any per key: each thread keeps its last
+//    (prefix slot, digit) bin and its count in registers (YLT keys fall into a
+//    few bins), flushing to the block's shared histogram only when the bin
+//    changes.
+//  * Consecutive launches use programmatic dependent launch: pass p+1's blocks
+//    are resident and waiting (griddepcontrol.wait) when pass p ends.
+//  * Tail sums: per-thread fixed-order sums, fixed shuffle trees within a warp
+//    and across warps, block partials combined in block order by a fixed
+//    per-lane split + shuffle tree: deterministic for a given device and size.
+// Histogram zeroing: pass 0 clears the buffers of passes 1..7, the tail kernel
+// clears pass 0's buffer for the next call (metrics_alloc zeroes all of them
+// once).
+#ifndef M3_THREADS_V
+#define M3_THREADS_V 512
+#endif
+#ifndef M3_KB_V
+#define M3_KB_V 16
+#endif
+constexpr int M3_THREADS = M3_THREADS_V;
+constexpr int M3_KB = M3_KB_V;
+constexpr int M3_RC = 10;
+
+struct M3Params {
+    const double* ylt;
+    uint64_t T, ld;
+    uint32_t n_rp, nblk, rows;
+    uint32_t* hist;      // [8][rows][n_rp][256]
+    uint64_t* st;        // [2][rows][n_rp][2]: prefix, remaining rank
+    uint32_t* strep;     // [2][rows][n_rp]: histogram slot (first period with the same prefix)
+    double* part_sum;    // [rows][n_rp][nblk]
+    uint64_t* part_cnt;
+    uint32_t* done;      // [rows]
+    double* out;         // [rows][n_rp][2]
+    double* dsum;        // distributed: this rank's tail sums / counts
+    uint64_t* dcnt;
+    int dist;
+    uint64_t k[ARA_MAX_RP];
+};
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+struct M3Smem {   // per block, for its row
+    uint64_t pre[ARA_MAX_RP];
+    uint64_t krem[ARA_MAX_RP];
+    uint32_t rep[ARA_MAX_RP];
+    uint64_t up[ARA_MAX_RP];   // distinct current prefixes ...
+    uint32_t uq[ARA_MAX_RP];   // ... and their slots
+    uint32_t nu;
+};
+
+// S_p into shared memory: p == 0 the initial state, else the state recorded in st[p & 1].
+__device__ void m3_load(const M3Params& P, uint32_t row, int p, M3Smem& S) {
     const uint32_t n_rp = P.n_rp;
-    const uint32_t lane = threadIdx.x & 31u;
-    uint32_t* gh = P.hist + (uint64_t)row * n_rp * 256;
-    __shared__ uint32_t s_rep2[ARA_MAX_RP];
-    for (uint32_t i = threadIdx.x; i < n_rp; i += blockDim.x) s_rep2[i] = P.rep[row * n_rp + i];
+    const size_t q0 = (size_t)row * n_rp;
+    for (uint32_t r = threadIdx.x; r < n_rp; r += blockDim.x) {
+        if (p == 0) { S.pre[r] = 0; S.krem[r] = P.k[r]; S.rep[r] = 0; }
+        else {
+            const size_t b = (size_t)(p & 1) * P.rows * n_rp + q0 + r;
+            S.pre[r] = __ldcg(P.st + 2 * b);
+            S.krem[r] = __ldcg(P.st + 2 * b + 1);
+            S.rep[r] = __ldcg(P.strep + b);
+        }
+    }
     __syncthreads();
-    const uint32_t* s_rep = s_rep2;
-    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) sh[i] = (s_rep[i >> 8] == (i >> 8)) ? __ldcg(gh + i) : 0u;
+}
+
+// the distinct prefixes (up) and their histogram slots (uq)
+__device__ void m3_ulist(const M3Params& P, M3Smem& S) {
+    if (threadIdx.x == 0) {
+        uint32_t nu = 0;
+        for (uint32_t r = 0; r < P.n_rp; ++r)
+            if (S.rep[r] == r) { S.up[nu] = S.pre[r]; S.uq[nu] = r; ++nu; }
+        S.nu = nu;
+    }
     __syncthreads();
-    const uint32_t wid = threadIdx.x >> 5;
+}
+
+// S_{p+1} from S_p (in shared memory) and the complete histogram of pass p
+// (row-local); record it in st[(p + 1) & 1] when `record`.
+__device__ void m3_select(const M3Params& P, uint32_t row, int p, M3Smem& S, bool record) {
+    const uint32_t n_rp = P.n_rp, lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    const size_t q0 = (size_t)row * n_rp;
+    const int shift = 56 - 8 * p;
+    const uint32_t* gh = P.hist + ((size_t)p * P.rows * n_rp + q0) * 256;
     for (uint32_t r = wid; r < n_rp; r += blockDim.x >> 5) {
-        const uint32_t* h = sh + s_rep[r] * 256;
-        const uint64_t kr = P.krem[row * n_rp + r];
-        // lane l owns digits 255-8l .. 248-8l (descending)
+        const uint32_t* h = gh + (size_t)S.rep[r] * 256;
+        const uint64_t kr = S.krem[r];
         uint32_t c[8];
         uint64_t tot = 0;
+        uint32_t hw[8];
+        hist_words(h, lane, hw);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) { c[q] = h[255 - 8 * lane - q]; tot += c[q]; }
+        for (int j = 0; j < 8; ++j) { c[j] = hw[7 - j]; tot += c[j]; }
         uint64_t incl = tot;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -93,117 +149,214 @@ __device__ void select_row(const MParams& P, uint32_t row, int shift, uint32_t* 
             uint64_t cum = excl;
             uint32_t d = 255 - 8 * lane;
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                if (kr <= cum + c[q]) { d = 255 - 8 * lane - q; break; }
-                cum += c[q];
+            for (int j = 0; j < 8; ++j) {
+                if (kr <= cum + c[j]) { d = 255 - 8 * lane - j; break; }
+                cum += c[j];
             }
-            const uint64_t pre = s_prefix[r] | ((uint64_t)d << shift);
-            P.prefix[row * n_rp + r] = pre;
-            P.krem[row * n_rp + r] = kr - cum;
-            s_prefix[r] = pre;
+            S.pre[r] |= (uint64_t)d << shift;
+            S.krem[r] = kr - cum;
         }
     }
     __syncthreads();
     for (uint32_t r = threadIdx.x; r < n_rp; r += blockDim.x) {
         uint32_t rr = r;
         for (uint32_t q = 0; q < r; ++q)
-            if (s_prefix[q] == s_prefix[r]) { rr = q; break; }
-        P.rep[row * n_rp + r] = rr;
+            if (S.pre[q] == S.pre[r]) { rr = q; break; }
+        S.rep[r] = rr;
     }
-    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) gh[i] = 0;
+    __syncthreads();
+    m3_ulist(P, S);
+    if (record) {
+        for (uint32_t r = threadIdx.x; r < n_rp; r += blockDim.x) {
+            const size_t b = (size_t)((p + 1) & 1) * P.rows * n_rp + q0 + r;
+            P.st[2 * b] = S.pre[r];
+            P.st[2 * b + 1] = S.krem[r];
+            P.strep[b] = S.rep[r];
+        }
+    }
+    __syncthreads();
 }
 
-__global__ void __launch_bounds__(256) radix_pass_kernel(const __grid_constant__ MParams P, int pass) {
-    extern __shared__ uint32_t sh[];                      // [n_rp][256]
-    __shared__ uint64_t s_prefix[ARA_MAX_RP];
-    __shared__ uint32_t s_rep[ARA_MAX_RP];
-    __shared__ uint32_t s_last;
-    const uint32_t row = blockIdx.y, n_rp = P.n_rp;
-    const uint32_t lane = threadIdx.x & 31u;
-    const int shift = 56 - 8 * pass;
-    for (uint32_t i = threadIdx.x; i < n_rp; i += blockDim.x) {
-        s_prefix[i] = P.prefix[row * n_rp + i];
-        s_rep[i] = P.rep[row * n_rp + i];
-    }
-    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) sh[i] = 0;
-    __syncthreads();
+// S_{p+1} from the recorded S_p and the complete histogram of pass p; block 0
+// records it (p < 7) for the next pass.
+__device__ void m3_advance(const M3Params& P, uint32_t row, int p, M3Smem& S) {
+    m3_load(P, row, p, S);
+    m3_select(P, row, p, S, blockIdx.x == 0 && p < 7);
+}
 
-    // Warp-uniform sweep.  Distinct current prefixes ("reps") are disjoint, so
-    // a key belongs to at most one rep; lanes with the same (rep, digit) are
-    // merged with match_any so each pair costs one shared atomic per warp
-    // (YLT keys concentrate in a few top-byte bins).
-    __shared__ uint32_t s_ulist[ARA_MAX_RP];
-    __shared__ uint64_t s_upre[ARA_MAX_RP];
-    __shared__ uint32_t s_nu;
-    if (threadIdx.x == 0) {
-        uint32_t nu = 0;
-        for (uint32_t r = 0; r < n_rp; ++r)
-            if (s_rep[r] == r) { s_ulist[nu] = r; s_upre[nu] = s_prefix[r]; ++nu; }
-        s_nu = nu;
+
+__global__ void __launch_bounds__(M3_THREADS) m3_pass_kernel(const __grid_constant__ M3Params P, int pass) {
+    extern __shared__ uint32_t sh[];   // [n_rp][256]
+    __shared__ M3Smem S;
+    const uint32_t row = blockIdx.y, n_rp = P.n_rp;
+    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) sh[i] = 0;
+    pdl_wait();
+    pdl_trigger();
+    if (pass == 0) {
+        // clear the histograms of passes 1..7 (not touched before pass 1 starts)
+        const size_t per = (size_t)P.rows * n_rp * 256;
+        const size_t n = 7 * per, stride = (size_t)gridDim.x * gridDim.y * blockDim.x;
+        for (size_t i = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+            P.hist[per + i] = 0;
+        if (threadIdx.x == 0) S.nu = 1;
+        if (threadIdx.x == 0) { S.up[0] = 0; S.uq[0] = 0; }
+        __syncthreads();
+    } else {
+        m3_advance(P, row, pass - 1, S);
     }
-    __syncthreads();
-    const uint32_t nu = s_nu;
-    const double* y = P.ylt + (uint64_t)row * P.ld;
-    // Keys are loaded KB at a time per lane (independent loads in flight),
-    // then binned.
-    constexpr int KB = 8;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); i0 < P.T; i0 += stride * KB) {
-        uint64_t keys[KB];
+    const int shift = 56 - 8 * pass;
+    const uint32_t nu = S.nu;
+    const double* y = P.ylt + (size_t)row * P.ld;
+    const uint64_t stride = (uint64_t)gridDim.x * M3_THREADS;
+    uint32_t cbin = 0xffffffffu, ccnt = 0;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * M3_THREADS + threadIdx.x; i0 < P.T; i0 += stride * M3_KB) {
+        uint64_t keys[M3_KB];
 #pragma unroll
-        for (int q = 0; q < KB; ++q) {
-            const uint64_t i = i0 + q * stride + lane;
-            keys[q] = i < P.T ? key_of(__ldcg(y + i)) : ~0ull;   // ~0: not a key (NaN pattern)
+        for (int q = 0; q < M3_KB; ++q) {
+            const uint64_t i = i0 + q * stride;
+            keys[q] = i < P.T ? key_of(__ldcg(y + i)) : ~0ull;
         }
 #pragma unroll
-        for (int q = 0; q < KB; ++q) {
-            if (i0 + q * stride >= P.T) break;   // warp-uniform
+        for (int q = 0; q < M3_KB; ++q) {
             const uint64_t key = keys[q];
-            const bool valid = key != ~0ull;
-            const uint32_t d = (uint32_t)(key >> shift) & 255u;
-            uint32_t which = 0xffffffffu;
-            if (valid) {
-                if (pass == 0) which = 0;
+            uint32_t slot = 0xffffffffu;
+            if (key != ~0ull) {
+                if (pass == 0) slot = 0;
                 else
                     for (uint32_t u = 0; u < nu; ++u)
-                        if (((key ^ s_upre[u]) >> (shift + 8)) == 0) which = u;
+                        if (((key ^ S.up[u]) >> (shift + 8)) == 0) slot = S.uq[u];
             }
-            const uint32_t tag = which == 0xffffffffu ? 0xffffffffu : (which << 8) | d;
-            const unsigned peers = __match_any_sync(0xffffffffu, tag);
-            if (tag != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1))
-                atomicAdd(&sh[s_ulist[which] * 256 + d], (uint32_t)__popc(peers));
+            if (slot != 0xffffffffu) {
+                const uint32_t bin = slot * 256 + ((uint32_t)(key >> shift) & 255u);
+                if (bin != cbin) {
+                    if (ccnt) atomicAdd(&sh[cbin], ccnt);
+                    cbin = bin;
+                    ccnt = 0;
+                }
+                ++ccnt;
+            }
         }
     }
+    if (ccnt) atomicAdd(&sh[cbin], ccnt);
     __syncthreads();
-    uint32_t* gh = P.hist + (uint64_t)row * n_rp * 256;
+    uint32_t* gh = P.hist + ((size_t)pass * P.rows * n_rp + (size_t)row * n_rp) * 256;
     for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x)
         if (sh[i]) atomicAdd(&gh[i], sh[i]);
-    if (P.dist) return;   // the histograms are all-reduced across ranks, then select_kernel
+}
+
+__device__ __forceinline__ double warp_sum_tree(double v) {   // fixed butterfly: lane 0's result is deterministic
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ uint64_t warp_cnt_tree(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(M3_THREADS) m3_tail_kernel(const __grid_constant__ M3Params P) {
+    __shared__ M3Smem S;
+    __shared__ double s_ws[M3_RC][M3_THREADS / 32];
+    __shared__ uint64_t s_wc[M3_RC][M3_THREADS / 32];
+    __shared__ uint32_t s_last;
+    const uint32_t row = blockIdx.y, n_rp = P.n_rp;
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    constexpr uint32_t NW = M3_THREADS / 32;
+    pdl_wait();
+    pdl_trigger();
+    m3_advance(P, row, 7, S);   // S_8: the selected keys
+    if (blockIdx.x == 0 && P.dist) {   // the distributed finish reads the values from st[0]
+        for (uint32_t r = threadIdx.x; r < n_rp; r += blockDim.x) P.st[2 * ((size_t)row * n_rp + r)] = S.pre[r];
+    }
+    {   // clear this row's pass-0 histogram for the next call
+        uint32_t* h0 = P.hist + (size_t)row * n_rp * 256;
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rp * 256u; i += gridDim.x * blockDim.x) h0[i] = 0;
+    }
+    const double* y = P.ylt + (size_t)row * P.ld;
+    const uint64_t stride = (uint64_t)gridDim.x * M3_THREADS;
+    for (uint32_t r0 = 0; r0 < n_rp; r0 += M3_RC) {
+        uint64_t v[M3_RC];
+        double s[M3_RC];
+        uint64_t c[M3_RC];
+#pragma unroll
+        for (int j = 0; j < M3_RC; ++j) {
+            v[j] = r0 + j < n_rp ? S.pre[r0 + j] : ~0ull;   // past n_rp: nothing is above
+            s[j] = 0.0;
+            c[j] = 0;
+        }
+        for (uint64_t i0 = (uint64_t)blockIdx.x * M3_THREADS + threadIdx.x; i0 < P.T; i0 += stride * M3_KB) {
+            double xs[M3_KB];
+#pragma unroll
+            for (int q = 0; q < M3_KB; ++q) {
+                const uint64_t i = i0 + q * stride;
+                xs[q] = i < P.T ? __ldcg(y + i) + 0.0 : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < M3_KB; ++q) {   // fixed order per thread: deterministic
+                const uint64_t key = (uint64_t)__double_as_longlong(xs[q]);
+#pragma unroll
+                for (int j = 0; j < M3_RC; ++j)
+                    if (key > v[j]) { s[j] = __dadd_rn(s[j], xs[q]); ++c[j]; }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < M3_RC; ++j) {
+            const double ws = warp_sum_tree(s[j]);
+            const uint64_t wc = warp_cnt_tree(c[j]);
+            if (lane == 0) { s_ws[j][wid] = ws; s_wc[j][wid] = wc; }
+        }
+        __syncthreads();
+        for (uint32_t j = wid; j < (uint32_t)M3_RC && r0 + j < n_rp; j += NW) {
+            double x = lane < NW ? s_ws[j][lane] : 0.0;
+            uint64_t cc = lane < NW ? s_wc[j][lane] : 0;
+            x = warp_sum_tree(x);
+            cc = warp_cnt_tree(cc);
+            if (lane == 0) {
+                const size_t q = (size_t)row * n_rp + r0 + j;
+                P.part_sum[q * P.nblk + blockIdx.x] = x;
+                P.part_cnt[q * P.nblk + blockIdx.x] = cc;
+            }
+        }
+        __syncthreads();
+    }
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(&P.done[row], 1u) == P.nblk - 1) ? 1u : 0u;
+    if (threadIdx.x == 0) s_last = (atomicAdd(&P.done[row], 1u) == gridDim.x - 1) ? 1u : 0u;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-
-    select_row(P, row, shift, sh, s_prefix);
+    // block partials in a fixed per-lane split, then a fixed tree
+    for (uint32_t r = wid; r < n_rp; r += NW) {
+        const size_t q = (size_t)row * n_rp + r;
+        double sm = 0.0;
+        uint64_t cn = 0;
+        for (uint32_t b = lane; b < gridDim.x; b += 32) {
+            sm = __dadd_rn(sm, __ldcg(P.part_sum + q * P.nblk + b));
+            cn += __ldcg(P.part_cnt + q * P.nblk + b);
+        }
+        sm = warp_sum_tree(sm);
+        cn = warp_cnt_tree(cn);
+        if (lane == 0) {
+            if (P.dist) {
+                P.dsum[q] = sm;
+                P.dcnt[q] = cn;
+            } else {
+                const double vv = __longlong_as_double((long long)S.pre[r]);
+                const uint64_t k = P.k[r];
+                const double tail = __dadd_rn(sm, __dmul_rn((double)(k - cn), vv));
+                P.out[q * 2 + 0] = vv;
+                P.out[q * 2 + 1] = __ddiv_rn(tail, (double)k);
+            }
+        }
+    }
     if (threadIdx.x == 0) P.done[row] = 0;
 }
 
-// distributed mode: one block per row picks the digits from the all-reduced histograms
-__global__ void __launch_bounds__(256) select_kernel(const __grid_constant__ MParams P, int pass) {
-    extern __shared__ uint32_t sh[];
-    __shared__ uint64_t s_prefix[ARA_MAX_RP];
-    const uint32_t row = blockIdx.x;
-    for (uint32_t i = threadIdx.x; i < P.n_rp; i += blockDim.x) s_prefix[i] = P.prefix[row * P.n_rp + i];
-    __syncthreads();
-    select_row(P, row, 56 - 8 * pass, sh, s_prefix);
-}
-
-// distributed mode: TVaR from the all-reduced tail sums and counts
-__global__ void finish_kernel(const __grid_constant__ MParams P, uint32_t rows) {
-    for (uint32_t q = threadIdx.x; q < rows * P.n_rp; q += blockDim.x) {
-        const double v = __longlong_as_double((long long)P.prefix[q]);
+// distributed: TVaR from the all-reduced tail sums and counts
+__global__ void m3_finish_kernel(const __grid_constant__ M3Params P) {
+    for (uint32_t q = threadIdx.x; q < P.rows * P.n_rp; q += blockDim.x) {
+        const double v = __longlong_as_double((long long)P.st[2 * (size_t)q]);
         const uint64_t k = P.k[q % P.n_rp];
         const double tail = __dadd_rn(P.dsum[q], __dmul_rn((double)(k - P.dcnt[q]), v));
         P.out[(uint64_t)q * 2 + 0] = v;
@@ -211,371 +364,589 @@ __global__ void finish_kernel(const __grid_constant__ MParams P, uint32_t rows) 
     }
 }
 
-__global__ void __launch_bounds__(256) tail_kernel(const __grid_constant__ MParams P) {
-    // RC return periods per sweep over the row (each accumulator is the same
-    // per-thread sequential sum over the same keys as a one-period sweep).
-    // RC = 10 covers the paper's 10 return periods in one sweep (40 KB of
-    // static shared memory for the block reductions).
-    constexpr int RC = 10;
-    __shared__ double s_sum[RC][256];
-    __shared__ uint64_t s_cnt[RC][256];
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl,
+                       Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// ---------------------------------------------------------------------------
+// Fast path for n_rp <= 11 (the paper's 10 return periods): three full sweeps,
+// then only the candidates.
+//  pass 0, 1: full sweeps (digits 0 and 1; pass 1 finds a key's prefix slot by
+//             a 256-entry table instead of comparing with every prefix).
+//  pass 2:    full sweep.  With the 16-bit prefixes P16_r of all periods known,
+//             the distinct ones sorted u_0 < .. < u_{m-1}, a key with 16-bit
+//             prefix pk (found by binary search) is
+//               - a candidate of u_j if pk == u_j: appended to its warp's
+//                 candidate region (ballot order: deterministic), counted
+//                 in the digit-2 histogram and added to slot 2j;
+//               - in slot 2j+1 if u_j < pk < u_{j+1};
+//               - below every period otherwise.
+//             Slot sums are thread-private (fixed order).  Every key of a slot
+//             above 2 idx(r) has a larger 16-bit prefix than v_r, so
+//               sum_{Y > v_r} Y = sum_{slots > 2 idx(r)} B + sum of r's candidates > v_r.
+//  pass 3..7: digits 3..7 over the candidate regions only.
+//  tail:      the candidates > v_r of each period, block partials, then the
+//             last block combines buckets (suffix, fixed order) + candidates.
+constexpr int M4_MAXU = 16;      // sorted-prefix search array (padded)
+constexpr int M4_MAXM = 11;      // distinct 16-bit prefixes (n_rp <= 11)
+constexpr int M4_SLOTS = 2 * M4_MAXM;
+
+struct M4Params {
+    M3Params b;
+    uint64_t* cand;        // [rows][nblk * warps][cap_w] candidate keys per warp region
+    uint32_t* cand_n;      // [rows][nblk * warps]
+    uint64_t cap_w;
+    double* bsum;          // [rows][M4_SLOTS][nblk] slot sums per block
+    uint64_t* bcnt;
+};
+
+__device__ __forceinline__ uint64_t m4_region(const M4Params& Q, uint32_t row, uint32_t blk, uint32_t w) {
+    return ((uint64_t)row * Q.b.nblk * (M3_THREADS / 32) + (uint64_t)blk * (M3_THREADS / 32) + w);
+}
+
+// distinct 16-bit prefixes of the row's periods, sorted ascending, padded with 0xffffffff
+__device__ void m4_ulist(const M3Params& P, const M3Smem& S, uint32_t* s_u, uint32_t* s_uslot, uint32_t* s_m) {
+    if (threadIdx.x == 0) {
+        uint32_t m = 0;
+        for (uint32_t r = 0; r < P.n_rp; ++r) {
+            const uint32_t v = (uint32_t)(S.pre[r] >> 48);
+            bool seen = false;
+            for (uint32_t j = 0; j < m; ++j) seen |= s_u[j] == v;
+            if (seen) continue;
+            uint32_t j = m++;
+            while (j > 0 && s_u[j - 1] > v) { s_u[j] = s_u[j - 1]; s_uslot[j] = s_uslot[j - 1]; --j; }
+            s_u[j] = v;
+            s_uslot[j] = S.rep[r];
+        }
+        for (uint32_t j = m; j < M4_MAXU; ++j) s_u[j] = 0xffffffffu;
+        *s_m = m;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ uint32_t m4_rank(const uint32_t* s_u, uint32_t pk) {   // #{j : u_j <= pk}
+    uint32_t pos = 0;
+#pragma unroll
+    for (uint32_t st = M4_MAXU / 2; st >= 1; st >>= 1)
+        if (s_u[pos + st - 1] <= pk) pos += st;
+    return pos;
+}
+
+__global__ void __launch_bounds__(M3_THREADS) m4_pass01_kernel(const __grid_constant__ M4Params Q, int pass) {
+    const M3Params& P = Q.b;
+    extern __shared__ uint32_t sh[];   // [n_rp][256]
+    __shared__ M3Smem S;
+    __shared__ uint8_t t1[256];
+    const uint32_t row = blockIdx.y, n_rp = P.n_rp;
+    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) sh[i] = 0;
+    for (uint32_t i = threadIdx.x; i < 256u; i += blockDim.x) t1[i] = 0xff;
+    pdl_wait();
+    pdl_trigger();
+    if (pass == 0) {
+        const size_t per = (size_t)P.rows * n_rp * 256;
+        const size_t n = 7 * per, stride = (size_t)gridDim.x * gridDim.y * blockDim.x;
+        for (size_t i = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+            P.hist[per + i] = 0;
+        m3_load(P, row, 0, S);
+    } else {
+        m3_advance(P, row, 0, S);
+        for (uint32_t u = threadIdx.x; u < S.nu; u += blockDim.x) t1[(uint32_t)(S.up[u] >> 56)] = (uint8_t)S.uq[u];
+        __syncthreads();
+    }
+    const int shift = 56 - 8 * pass;
+    const double* y = P.ylt + (size_t)row * P.ld;
+    const uint64_t stride = (uint64_t)gridDim.x * M3_THREADS;
+    uint32_t cbin = 0xffffffffu, ccnt = 0;
+    for (uint64_t i0 = (uint64_t)blockIdx.x * M3_THREADS + threadIdx.x; i0 < P.T; i0 += stride * M3_KB) {
+        uint64_t keys[M3_KB];
+#pragma unroll
+        for (int q = 0; q < M3_KB; ++q) {
+            const uint64_t i = i0 + q * stride;
+            keys[q] = i < P.T ? key_of(__ldcg(y + i)) : ~0ull;
+        }
+#pragma unroll
+        for (int q = 0; q < M3_KB; ++q) {
+            const uint64_t key = keys[q];
+            if (key == ~0ull) continue;
+            const uint32_t slot = pass == 0 ? 0u : (uint32_t)t1[(uint32_t)(key >> 56)];
+            if (slot == 0xffu) continue;
+            const uint32_t bin = slot * 256 + ((uint32_t)(key >> shift) & 255u);
+            if (bin != cbin) {
+                if (ccnt) atomicAdd(&sh[cbin], ccnt);
+                cbin = bin;
+                ccnt = 0;
+            }
+            ++ccnt;
+        }
+    }
+    if (ccnt) atomicAdd(&sh[cbin], ccnt);
+    __syncthreads();
+    uint32_t* gh = P.hist + ((size_t)pass * P.rows * n_rp + (size_t)row * n_rp) * 256;
+    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x)
+        if (sh[i]) atomicAdd(&gh[i], sh[i]);
+}
+
+__global__ void __launch_bounds__(M3_THREADS) m4_pass2_kernel(const __grid_constant__ M4Params Q) {
+    const M3Params& P = Q.b;
+    extern __shared__ __align__(16) unsigned char dsm2[];
+    const uint32_t n_rp = P.n_rp;
+    uint32_t* sh = reinterpret_cast<uint32_t*>(dsm2);                                     // [n_rp][256]
+    double* s_bs = reinterpret_cast<double*>(dsm2 + (size_t)n_rp * 256 * 4);              // [M4_SLOTS][THREADS]
+    uint32_t* s_bc = reinterpret_cast<uint32_t*>(s_bs + (size_t)M4_SLOTS * M3_THREADS);   // [M4_SLOTS][THREADS]
+    __shared__ M3Smem S;
+    __shared__ uint32_t s_u[M4_MAXU], s_uslot[M4_MAXU], s_m;
+    const uint32_t row = blockIdx.y, tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
+    for (uint32_t i = tid; i < n_rp * 256u; i += blockDim.x) sh[i] = 0;
+    for (uint32_t i = tid; i < M4_SLOTS * M3_THREADS; i += blockDim.x) { s_bs[i] = 0.0; s_bc[i] = 0; }
+    pdl_wait();
+    pdl_trigger();
+    m3_advance(P, row, 1, S);   // S_2: the 16-bit prefixes
+    m4_ulist(P, S, s_u, s_uslot, &s_m);
+    const uint32_t m = s_m;
+    const double* y = P.ylt + (size_t)row * P.ld;
+    const uint64_t stride = (uint64_t)gridDim.x * M3_THREADS;
+    uint64_t* cr = Q.cand + m4_region(Q, row, blockIdx.x, wid) * Q.cap_w;
+    uint32_t ncand = 0;   // warp-uniform
+    const unsigned lt = (1u << lane) - 1u;
+    uint32_t cbin = 0xffffffffu, ccnt = 0;
+    // the loop trip count is warp-uniform (i0 - lane is the same for the warp)
+    for (uint64_t i0 = (uint64_t)blockIdx.x * M3_THREADS + tid; i0 - lane < P.T; i0 += stride * M3_KB) {
+        uint64_t keys[M3_KB];
+#pragma unroll
+        for (int q = 0; q < M3_KB; ++q) {
+            const uint64_t i = i0 + q * stride;
+            keys[q] = i < P.T ? key_of(__ldcg(y + i)) : ~0ull;
+        }
+#pragma unroll
+        for (int q = 0; q < M3_KB; ++q) {
+            const uint64_t key = keys[q];
+            const bool valid = key != ~0ull;
+            const uint32_t pk = (uint32_t)(key >> 48);
+            const uint32_t pos = valid ? m4_rank(s_u, pk) : 0u;
+            const bool is_c = pos > 0 && s_u[pos - 1] == pk;
+            const unsigned cm = __ballot_sync(0xffffffffu, is_c);
+            if (is_c) {
+                cr[ncand + __popc(cm & lt)] = key;
+                const uint32_t bin = s_uslot[pos - 1] * 256 + ((uint32_t)(key >> 40) & 255u);
+                if (bin != cbin) {
+                    if (ccnt) atomicAdd(&sh[cbin], ccnt);
+                    cbin = bin;
+                    ccnt = 0;
+                }
+                ++ccnt;
+            }
+            if (pos > 0) {   // slot 2(pos-1) (== u_{pos-1}) or 2(pos-1)+1 (strictly between u_{pos-1} and u_pos)
+                const uint32_t bi = (2 * (pos - 1) + (is_c ? 0u : 1u)) * M3_THREADS + tid;
+                s_bs[bi] = __dadd_rn(s_bs[bi], __longlong_as_double((long long)key));
+                s_bc[bi] += 1;
+            }
+            ncand += __popc(cm);
+        }
+    }
+    if (ccnt) atomicAdd(&sh[cbin], ccnt);
+    if (lane == 0) Q.cand_n[m4_region(Q, row, blockIdx.x, wid)] = ncand;
+    __syncthreads();
+    uint32_t* gh = P.hist + ((size_t)2 * P.rows * n_rp + (size_t)row * n_rp) * 256;
+    for (uint32_t i = tid; i < n_rp * 256u; i += blockDim.x)
+        if (sh[i]) atomicAdd(&gh[i], sh[i]);
+    // slot partials: fixed tree over the block's threads
+    const uint32_t ns = 2 * m;
+    for (uint32_t w = M3_THREADS / 2; w >= 1; w >>= 1) {
+        for (uint32_t idx = tid; idx < ns * w; idx += blockDim.x) {
+            const uint32_t j = idx / w, t = idx % w;
+            s_bs[j * M3_THREADS + t] = __dadd_rn(s_bs[j * M3_THREADS + t], s_bs[j * M3_THREADS + t + w]);
+            s_bc[j * M3_THREADS + t] += s_bc[j * M3_THREADS + t + w];
+        }
+        __syncthreads();
+    }
+    for (uint32_t j = tid; j < ns; j += blockDim.x) {
+        Q.bsum[((size_t)row * M4_SLOTS + j) * P.nblk + blockIdx.x] = s_bs[j * M3_THREADS];
+        Q.bcnt[((size_t)row * M4_SLOTS + j) * P.nblk + blockIdx.x] = s_bc[j * M3_THREADS];
+    }
+}
+
+__global__ void __launch_bounds__(M3_THREADS) m4_cand_pass_kernel(const __grid_constant__ M4Params Q, int pass) {
+    const M3Params& P = Q.b;
+    extern __shared__ uint32_t sh[];
+    __shared__ M3Smem S;
+    const uint32_t row = blockIdx.y, n_rp = P.n_rp, lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x) sh[i] = 0;
+    pdl_wait();
+    pdl_trigger();
+    m3_advance(P, row, pass - 1, S);
+    const int shift = 56 - 8 * pass;
+    const uint32_t nu = S.nu;
+    const uint64_t reg = m4_region(Q, row, blockIdx.x, wid);
+    const uint64_t* cr = Q.cand + reg * Q.cap_w;
+    const uint32_t n = __ldcg(Q.cand_n + reg);
+    uint32_t cbin = 0xffffffffu, ccnt = 0;
+    for (uint32_t i = lane; i < n; i += 32) {
+        const uint64_t key = __ldcg(cr + i);
+        uint32_t slot = 0xffffffffu;
+        for (uint32_t u = 0; u < nu; ++u)
+            if (((key ^ S.up[u]) >> (shift + 8)) == 0) slot = S.uq[u];
+        if (slot == 0xffffffffu) continue;
+        const uint32_t bin = slot * 256 + ((uint32_t)(key >> shift) & 255u);
+        if (bin != cbin) {
+            if (ccnt) atomicAdd(&sh[cbin], ccnt);
+            cbin = bin;
+            ccnt = 0;
+        }
+        ++ccnt;
+    }
+    if (ccnt) atomicAdd(&sh[cbin], ccnt);
+    __syncthreads();
+    uint32_t* gh = P.hist + ((size_t)pass * P.rows * n_rp + (size_t)row * n_rp) * 256;
+    for (uint32_t i = threadIdx.x; i < n_rp * 256u; i += blockDim.x)
+        if (sh[i]) atomicAdd(&gh[i], sh[i]);
+}
+
+__global__ void __launch_bounds__(M3_THREADS) m4_tail_kernel(const __grid_constant__ M4Params Q) {
+    const M3Params& P = Q.b;
+    __shared__ M3Smem S;
+    __shared__ uint32_t s_u[M4_MAXU], s_uslot[M4_MAXU], s_m;
+    __shared__ double s_ws[M3_RC][M3_THREADS / 32];
+    __shared__ uint64_t s_wc[M3_RC][M3_THREADS / 32];
+    __shared__ double s_B[M4_SLOTS];
+    __shared__ uint64_t s_Bc[M4_SLOTS];
     __shared__ uint32_t s_last;
     const uint32_t row = blockIdx.y, n_rp = P.n_rp;
-    const double* y = P.ylt + (uint64_t)row * P.ld;
-    constexpr int KB = 8;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint32_t r0 = 0; r0 < n_rp; r0 += RC) {
-        double v[RC], s[RC];
-        uint64_t c[RC];
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    constexpr uint32_t NW = M3_THREADS / 32;
+    pdl_wait();
+    pdl_trigger();
+    m3_advance(P, row, 7, S);   // S_8: the selected keys
+    if (blockIdx.x == 0 && P.dist)   // the distributed finish reads the values from st[0]
+        for (uint32_t r = threadIdx.x; r < n_rp; r += blockDim.x) P.st[2 * ((size_t)row * n_rp + r)] = S.pre[r];
+    {   // clear this row's pass-0 histogram for the next call
+        uint32_t* h0 = P.hist + (size_t)row * n_rp * 256;
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rp * 256u; i += gridDim.x * blockDim.x) h0[i] = 0;
+    }
+    const uint64_t reg = m4_region(Q, row, blockIdx.x, wid);
+    const uint64_t* cr = Q.cand + reg * Q.cap_w;
+    const uint32_t n = __ldcg(Q.cand_n + reg);
+    for (uint32_t r0 = 0; r0 < n_rp; r0 += M3_RC) {
+        uint64_t v[M3_RC];
+        double s[M3_RC];
+        uint64_t c[M3_RC];
 #pragma unroll
-        for (int j = 0; j < RC; ++j) {
-            // periods past n_rp compare against +inf: nothing is added
-            v[j] = r0 + j < n_rp ? __longlong_as_double((long long)P.prefix[row * n_rp + r0 + j]) : INFINITY;
+        for (int j = 0; j < M3_RC; ++j) {
+            v[j] = r0 + j < n_rp ? S.pre[r0 + j] : ~0ull;
             s[j] = 0.0;
             c[j] = 0;
         }
-        for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < P.T; i0 += stride * KB) {
-            double xs[KB];
+        for (uint32_t i = lane; i < n; i += 32) {   // fixed order: deterministic
+            const uint64_t key = __ldcg(cr + i);
 #pragma unroll
-            for (int q = 0; q < KB; ++q) {
-                const uint64_t i = i0 + q * stride;
-                xs[q] = i < P.T ? __ldcg(y + i) + 0.0 : -1.0;
-            }
-#pragma unroll
-            for (int q = 0; q < KB; ++q)   // fixed order per thread: deterministic
-#pragma unroll
-                for (int j = 0; j < RC; ++j)
-                    if (xs[q] > v[j]) { s[j] = __dadd_rn(s[j], xs[q]); ++c[j]; }
+            for (int j = 0; j < M3_RC; ++j)
+                if (key > v[j] && ((key ^ v[j]) >> 48) == 0) { s[j] = __dadd_rn(s[j], __longlong_as_double((long long)key)); ++c[j]; }
         }
 #pragma unroll
-        for (int j = 0; j < RC; ++j) {
-            s_sum[j][threadIdx.x] = s[j];
-            s_cnt[j][threadIdx.x] = c[j];
+        for (int j = 0; j < M3_RC; ++j) {
+            const double ws = warp_sum_tree(s[j]);
+            const uint64_t wc = warp_cnt_tree(c[j]);
+            if (lane == 0) { s_ws[j][wid] = ws; s_wc[j][wid] = wc; }
         }
         __syncthreads();
-        for (int w = 128; w >= 1; w >>= 1) {
-            if ((int)threadIdx.x < w) {
-#pragma unroll
-                for (int j = 0; j < RC; ++j) {
-                    s_sum[j][threadIdx.x] = __dadd_rn(s_sum[j][threadIdx.x], s_sum[j][threadIdx.x + w]);
-                    s_cnt[j][threadIdx.x] += s_cnt[j][threadIdx.x + w];
-                }
+        for (uint32_t j = wid; j < (uint32_t)M3_RC && r0 + j < n_rp; j += NW) {
+            double x = lane < NW ? s_ws[j][lane] : 0.0;
+            uint64_t cc = lane < NW ? s_wc[j][lane] : 0;
+            x = warp_sum_tree(x);
+            cc = warp_cnt_tree(cc);
+            if (lane == 0) {
+                const size_t q = (size_t)row * n_rp + r0 + j;
+                P.part_sum[q * P.nblk + blockIdx.x] = x;
+                P.part_cnt[q * P.nblk + blockIdx.x] = cc;
             }
-            __syncthreads();
-        }
-        if (threadIdx.x < RC && r0 + threadIdx.x < n_rp) {
-            const uint32_t r = r0 + threadIdx.x;
-            P.part_sum[((uint64_t)row * n_rp + r) * P.nblk + blockIdx.x] = s_sum[threadIdx.x][0];
-            P.part_cnt[((uint64_t)row * n_rp + r) * P.nblk + blockIdx.x] = s_cnt[threadIdx.x][0];
         }
         __syncthreads();
     }
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(&P.done[row], 1u) == P.nblk - 1) ? 1u : 0u;
+    if (threadIdx.x == 0) s_last = (atomicAdd(&P.done[row], 1u) == gridDim.x - 1) ? 1u : 0u;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // Combine the per-block partials in block order (deterministic): one warp
-    // per return period, partials staged through registers in fixed chunks.
-    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-    for (uint32_t r = wid; r < n_rp; r += blockDim.x >> 5) {
-        const double v = __longlong_as_double((long long)P.prefix[row * n_rp + r]);
-        const double* ps = P.part_sum + ((uint64_t)row * n_rp + r) * P.nblk;
-        const uint64_t* pc = P.part_cnt + ((uint64_t)row * n_rp + r) * P.nblk;
-        double s = 0.0;
-        uint64_t c = 0;
-        for (uint32_t b0 = 0; b0 < P.nblk; b0 += 32) {
-            const uint32_t b = b0 + lane;
-            const double x = b < P.nblk ? __ldcg(ps + b) : 0.0;
-            const uint64_t y = b < P.nblk ? __ldcg(pc + b) : 0ull;
-            for (uint32_t q = 0; q < 32 && b0 + q < P.nblk; ++q) {   // sequential, block order
-                s = __dadd_rn(s, __shfl_sync(0xffffffffu, x, q));
-                c += __shfl_sync(0xffffffffu, y, q);
-            }
+    // S_8 has the same 16-bit prefixes as S_2: the same sorted list
+    m4_ulist(P, S, s_u, s_uslot, &s_m);
+    const uint32_t m = s_m;
+    for (uint32_t j = wid; j < 2 * m; j += NW) {   // slot totals: fixed per-lane split + tree
+        double sm = 0.0;
+        uint64_t cn = 0;
+        for (uint32_t b = lane; b < gridDim.x; b += 32) {
+            sm = __dadd_rn(sm, __ldcg(Q.bsum + ((size_t)row * M4_SLOTS + j) * P.nblk + b));
+            cn += __ldcg(Q.bcnt + ((size_t)row * M4_SLOTS + j) * P.nblk + b);
         }
+        sm = warp_sum_tree(sm);
+        cn = warp_cnt_tree(cn);
+        if (lane == 0) { s_B[j] = sm; s_Bc[j] = cn; }
+    }
+    __syncthreads();
+    for (uint32_t r = wid; r < n_rp; r += NW) {
+        const size_t q = (size_t)row * n_rp + r;
+        double sm = 0.0;
+        uint64_t cn = 0;
+        for (uint32_t b = lane; b < gridDim.x; b += 32) {
+            sm = __dadd_rn(sm, __ldcg(P.part_sum + q * P.nblk + b));
+            cn += __ldcg(P.part_cnt + q * P.nblk + b);
+        }
+        sm = warp_sum_tree(sm);
+        cn = warp_cnt_tree(cn);
         if (lane == 0) {
-            if (P.dist) {   // this rank's share; finish_kernel completes it after the all-reduce
-                P.dsum[(uint64_t)row * n_rp + r] = s;
-                P.dcnt[(uint64_t)row * n_rp + r] = c;
+            const uint32_t idx = m4_rank(s_u, (uint32_t)(S.pre[r] >> 48)) - 1;   // u_idx == P16_r
+            double bs = 0.0;
+            uint64_t bc = 0;
+            for (int j = 2 * (int)m - 1; j > 2 * (int)idx; --j) { bs = __dadd_rn(bs, s_B[j]); bc += s_Bc[j]; }
+            sm = __dadd_rn(bs, sm);
+            cn += bc;
+            if (P.dist) {
+                P.dsum[q] = sm;
+                P.dcnt[q] = cn;
             } else {
+                const double vv = __longlong_as_double((long long)S.pre[r]);
                 const uint64_t k = P.k[r];
-                const double tail = __dadd_rn(s, __dmul_rn((double)(k - c), v));
-                P.out[((uint64_t)row * n_rp + r) * 2 + 0] = v;
-                P.out[((uint64_t)row * n_rp + r) * 2 + 1] = __ddiv_rn(tail, (double)k);
+                const double tail = __dadd_rn(sm, __dmul_rn((double)(k - cn), vv));
+                P.out[q * 2 + 0] = vv;
+                P.out[q * 2 + 1] = __ddiv_rn(tail, (double)k);
             }
         }
     }
     if (threadIdx.x == 0) P.done[row] = 0;
 }
 
-// ---------------------------------------------------------------------------
-// The same method in ONE cooperative launch (the default when the grid fits):
-// the 8 radix passes and the tail sums are separated by grid-wide barriers
-// instead of kernel boundaries and "last block" hand-offs.  Every block keeps
-// the per-(row, return period) prefixes in shared memory and selects the digit
-// itself from the global histogram after each barrier (identical inputs,
-// identical choices), so a pass costs one sweep + one barrier.  Global
-// histograms rotate over three buffers: the one a pass accumulates into was
-// zeroed two barriers earlier, after every block had finished reading it.
-struct CoopLayout {
-    uint32_t nq;          // rows * n_rp
-    size_t hist_off, pre_off, krem_off, up_off, rep_off, uq_off, nu_off, bytes;
-};
-__host__ __device__ inline CoopLayout coop_layout(uint32_t rows, uint32_t n_rp) {
-    CoopLayout L;
-    L.nq = rows * n_rp;
-    L.hist_off = 0;
-    L.pre_off = (size_t)L.nq * 256 * 4;
-    L.krem_off = L.pre_off + (size_t)L.nq * 8;
-    L.up_off = L.krem_off + (size_t)L.nq * 8;     // per row: its distinct prefixes ...
-    L.rep_off = L.up_off + (size_t)L.nq * 8;
-    L.uq_off = L.rep_off + (size_t)L.nq * 4;      // ... and their slots
-    L.nu_off = L.uq_off + (size_t)L.nq * 4;       // number of distinct prefixes per row
-    L.bytes = L.nu_off + (size_t)rows * 4;
-    return L;
+cudaError_t launch_m4(const M3Params& P, MetricsScratch& m, bool dist, ncclComm_t comm, cudaStream_t s,
+                      int* nccl_err) {
+    M4Params Q{};
+    Q.b = P;
+    const uint32_t rows = P.rows, n_rp = P.n_rp, nblk = P.nblk;
+    const uint64_t stride = (uint64_t)nblk * M3_THREADS;
+    Q.cap_w = 32 * ((P.T + stride - 1) / stride) * 1;
+    const uint64_t nreg = (uint64_t)rows * nblk * (M3_THREADS / 32);
+    const uint64_t need = nreg * Q.cap_w;
+    cudaError_t e;
+    if (m.cand_cap < need) {
+        cudaFree(m.cand);
+        m.cand = nullptr;
+        m.cand_cap = 0;
+        if ((e = cudaMalloc(&m.cand, need * sizeof(uint64_t))) != cudaSuccess) return e;
+        m.cand_cap = need;
+    }
+    if (m.cand_n_cap < nreg) {
+        cudaFree(m.cand_n);
+        m.cand_n = nullptr;
+        m.cand_n_cap = 0;
+        if ((e = cudaMalloc(&m.cand_n, nreg * sizeof(uint32_t))) != cudaSuccess) return e;
+        m.cand_n_cap = nreg;
+    }
+    const uint64_t nb = (uint64_t)rows * M4_SLOTS * nblk;
+    if (m.bpart_cap < nb) {
+        cudaFree(m.bsum);
+        cudaFree(m.bcnt);
+        m.bsum = nullptr;
+        m.bcnt = nullptr;
+        m.bpart_cap = 0;
+        if ((e = cudaMalloc(&m.bsum, nb * sizeof(double))) != cudaSuccess) return e;
+        if ((e = cudaMalloc(&m.bcnt, nb * sizeof(uint64_t))) != cudaSuccess) return e;
+        m.bpart_cap = nb;
+    }
+    Q.cand = m.cand;
+    Q.cand_n = m.cand_n;
+    Q.bsum = m.bsum;
+    Q.bcnt = m.bcnt;
+    const size_t smem = (size_t)n_rp * 256 * sizeof(uint32_t);
+    const size_t smem2 = smem + (size_t)M4_SLOTS * M3_THREADS * (sizeof(double) + sizeof(uint32_t));
+    static size_t set01 = 0, set2 = 0, setc = 0;
+    if (smem > 32 * 1024 && smem > set01) {
+        if ((e = cudaFuncSetAttribute(m4_pass01_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+        set01 = smem;
+    }
+    if (smem > 32 * 1024 && smem > setc) {
+        if ((e = cudaFuncSetAttribute(m4_cand_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess) return e;
+        setc = smem;
+    }
+    if (smem2 > set2) {
+        if ((e = cudaFuncSetAttribute(m4_pass2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2)) != cudaSuccess) return e;
+        set2 = smem2;
+    }
+    if (nccl_err) *nccl_err = 0;
+    const size_t nh = (size_t)rows * n_rp * 256;
+    const bool pdl = !comm;
+    const dim3 grid(nblk, rows), blk(M3_THREADS);
+    // ARA_METRICS_TRACE=1: events between the launches (breaks the PDL overlap), per-kernel times on stderr
+    static const bool trace = [] { const char* v = getenv("ARA_METRICS_TRACE"); return v && atoi(v); }();
+    static cudaEvent_t tev[12];
+    static bool tev_init = false;
+    int nt = 0;
+    if (trace && !tev_init) {
+        for (auto& x : tev) cudaEventCreate(&x);
+        tev_init = true;
+    }
+    auto mark = [&] { if (trace) cudaEventRecord(tev[nt++], s); };
+    auto red = [&](int pass) {
+        mark();
+        if (comm && ncclAllReduce(P.hist + pass * nh, P.hist + pass * nh, nh, ncclUint32, ncclSum, comm, s) != ncclSuccess)
+            *nccl_err = 1;
+    };
+    auto enqueue = [&]() -> cudaError_t {
+        cudaError_t r = launch_pdl(m4_pass01_kernel, grid, blk, smem, s, false, Q, 0);
+        if (r == cudaSuccess) red(0);
+        if (r == cudaSuccess && !(nccl_err && *nccl_err)) r = launch_pdl(m4_pass01_kernel, grid, blk, smem, s, pdl, Q, 1);
+        if (r == cudaSuccess && !(nccl_err && *nccl_err)) red(1);
+        if (r == cudaSuccess && !(nccl_err && *nccl_err)) r = launch_pdl(m4_pass2_kernel, grid, blk, smem2, s, pdl, Q);
+        if (r == cudaSuccess && !(nccl_err && *nccl_err)) red(2);
+        for (int pass = 3; pass < 8 && r == cudaSuccess && !(nccl_err && *nccl_err); ++pass) {
+            r = launch_pdl(m4_cand_pass_kernel, grid, blk, smem, s, pdl, Q, pass);
+            if (r == cudaSuccess) red(pass);
+        }
+        if (r == cudaSuccess && !(nccl_err && *nccl_err)) r = launch_pdl(m4_tail_kernel, grid, blk, 0, s, pdl, Q);
+        return r;
+    };
+    // Single-GPU launches go through a CUDA graph of the 9 kernels (with their
+    // programmatic-launch edges), re-captured when any argument changes.
+    const char* g_env = getenv("ARA_METRICS_GRAPH");
+    const bool use_graph = !g_env || atoi(g_env);
+    static_assert(sizeof(M4Params) <= sizeof(m.m4_key), "graph key buffer");
+    if (!comm && !trace && use_graph) {
+        unsigned char key[sizeof(m.m4_key)] = {};
+        std::memcpy(key, &Q, sizeof(Q));
+        std::memcpy(key + sizeof(Q), &s, sizeof(s));
+        if (!m.m4_exec || std::memcmp(key, m.m4_key, sizeof(key)) != 0) {
+            if (m.m4_exec) cudaGraphExecDestroy(m.m4_exec);
+            m.m4_exec = nullptr;
+            cudaGraph_t g = nullptr;
+            if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+                const cudaError_t r = enqueue();
+                const cudaError_t r2 = cudaStreamEndCapture(s, &g);
+                if (r == cudaSuccess && r2 == cudaSuccess && g &&
+                    cudaGraphInstantiate(&m.m4_exec, g, 0) == cudaSuccess)
+                    std::memcpy(m.m4_key, key, sizeof(key));
+                else
+                    m.m4_exec = nullptr;
+                if (g) cudaGraphDestroy(g);
+            }
+            cudaGetLastError();   // a stream that cannot be captured: plain launches below
+        }
+        if (m.m4_exec) e = cudaGraphLaunch(m.m4_exec, s);
+        else e = enqueue();
+    } else {
+        mark();
+        e = enqueue();
+        mark();
+    }
+    if (trace && e == cudaSuccess) {
+        cudaEventSynchronize(tev[nt - 1]);
+        fprintf(stderr, "m4 trace us:");
+        for (int i = 1; i < nt; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tev[i - 1], tev[i]);
+            fprintf(stderr, " %.1f", ms * 1e3f);
+        }
+        fprintf(stderr, "\n");
+    }
+    if (e == cudaSuccess && !(nccl_err && *nccl_err) && dist) {
+        const size_t nq = (size_t)rows * n_rp;
+        if (comm && (ncclGroupStart() != ncclSuccess || ncclAllReduce(P.dsum, P.dsum, nq, ncclDouble, ncclSum, comm, s) != ncclSuccess ||
+                     ncclAllReduce(P.dcnt, P.dcnt, nq, ncclUint64, ncclSum, comm, s) != ncclSuccess ||
+                     ncclGroupEnd() != ncclSuccess))
+            *nccl_err = 1;
+        else
+            m3_finish_kernel<<<1, 256, 0, s>>>(P);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess || (nccl_err && *nccl_err)) {
+        cudaGetLastError();
+        cudaMemsetAsync(m.hist8, 0, 8 * nh * sizeof(uint32_t), s);
+        if (e == cudaSuccess) e = cudaGetLastError();
+    }
+    return e;
 }
 
-__global__ void __launch_bounds__(256) metrics_coop_kernel(const __grid_constant__ MParams P, uint32_t rows,
-                                                           uint32_t* __restrict__ ghist /*[3][nq][256]*/) {
-    cg::grid_group grid = cg::this_grid();
-    extern __shared__ __align__(16) unsigned char dsm[];
-    const uint32_t n_rp = P.n_rp;
-    const CoopLayout Lo = coop_layout(rows, n_rp);
-    const uint32_t nq = Lo.nq;
-    uint32_t* sh = reinterpret_cast<uint32_t*>(dsm + Lo.hist_off);
-    uint64_t* s_prefix = reinterpret_cast<uint64_t*>(dsm + Lo.pre_off);
-    uint64_t* s_krem = reinterpret_cast<uint64_t*>(dsm + Lo.krem_off);
-    uint32_t* s_rep = reinterpret_cast<uint32_t*>(dsm + Lo.rep_off);
-    uint64_t* s_up = reinterpret_cast<uint64_t*>(dsm + Lo.up_off);
-    uint32_t* s_uq = reinterpret_cast<uint32_t*>(dsm + Lo.uq_off);
-    uint32_t* s_nu = reinterpret_cast<uint32_t*>(dsm + Lo.nu_off);
-    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
-    for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {
-        s_prefix[q] = 0;
-        s_krem[q] = P.k[q % n_rp];
-        s_rep[q] = q - q % n_rp;   // all prefixes of a row equal: share the row's first slot
-        s_uq[q] = q - q % n_rp;
-        s_up[q] = 0;
-    }
-    for (uint32_t row = threadIdx.x; row < rows; row += blockDim.x) s_nu[row] = 1;
-    // this block's key range (the same for every row), staged once in shared
-    // memory as sort keys: the 8 passes and the tail sums read it from there
-    const uint64_t per = (P.T + gridDim.x - 1) / gridDim.x;
-    const uint64_t i_lo = (uint64_t)blockIdx.x * per;
-    const uint64_t i_hi = i_lo + per < P.T ? i_lo + per : P.T;
-    const uint32_t nk = i_hi > i_lo ? (uint32_t)(i_hi - i_lo) : 0u;
-    uint64_t* s_key = reinterpret_cast<uint64_t*>(dsm + Lo.bytes);   // [rows][per]
-    for (uint32_t row = 0; row < rows; ++row) {
-        const double* y = P.ylt + (uint64_t)row * P.ld + i_lo;
-        for (uint32_t i = threadIdx.x; i < nk; i += blockDim.x) s_key[(uint64_t)row * per + i] = key_of(__ldcg(y + i));
-    }
-    __syncthreads();
 
-    for (int pass = 0; pass < 8; ++pass) {
-        const int shift = 56 - 8 * pass;
-        uint32_t* gh = ghist + (size_t)(pass % 3) * nq * 256;
-        for (uint32_t i = threadIdx.x; i < nq * 256u; i += blockDim.x) sh[i] = 0;
-        __syncthreads();
-        for (uint32_t row = 0; row < rows; ++row) {
-            const double* y = P.ylt + (uint64_t)row * P.ld;
-            const uint32_t q0 = row * n_rp;
-            // the row's distinct current prefixes (disjoint: a key extends at most one)
-            const uint32_t nu = s_nu[row];
-            const uint64_t* up = s_up + q0;
-            const uint32_t* uq = s_uq + q0;
-            // per-lane cache of the last (slot, digit) tag this lane added for:
-            // YLT keys concentrate in a few bins, so most adds stay in a register
-            uint32_t ctag = 0xffffffffu, ccnt = 0;
-            const uint64_t* kr = s_key + (uint64_t)row * per;
-            for (uint32_t i0 = threadIdx.x & ~31u; i0 < nk; i0 += blockDim.x) {   // warp-uniform trip count
-                const uint32_t i = i0 + lane;
-                const uint64_t key = i < nk ? kr[i] : ~0ull;
-                uint32_t which = 0xffffffffu;
-                if (key != ~0ull) {
-                    if (pass == 0) which = q0;
-                    else
-                        for (uint32_t u = 0; u < nu; ++u)
-                            if (((key ^ up[u]) >> (shift + 8)) == 0) { which = uq[u]; break; }
-                }
-                const uint32_t tag = which == 0xffffffffu ? 0xffffffffu : (which << 8) | ((uint32_t)(key >> shift) & 255u);
-                const unsigned peers = __match_any_sync(0xffffffffu, tag);
-                if (tag != 0xffffffffu && lane == (uint32_t)(__ffs(peers) - 1)) {
-                    if (tag != ctag) {
-                        if (ccnt) atomicAdd(&sh[(ctag >> 8) * 256 + (ctag & 255u)], ccnt);
-                        ctag = tag;
-                        ccnt = 0;
-                    }
-                    ccnt += (uint32_t)__popc(peers);
-                }
-            }
-            if (ccnt) atomicAdd(&sh[(ctag >> 8) * 256 + (ctag & 255u)], ccnt);
-        }
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < nq * 256u; i += blockDim.x)
-            if (sh[i]) atomicAdd(&gh[i], sh[i]);
-        grid.sync();
-        // every block: pick the digit of every (row, return period) from the global histogram
-        for (uint32_t q = wid; q < nq; q += blockDim.x >> 5) {
-            const uint32_t* h = gh + (size_t)s_rep[q] * 256;
-            const uint64_t kr = s_krem[q];
-            uint32_t c[8];
-            uint64_t tot = 0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) { c[j] = __ldcg(h + 255 - 8 * lane - j); tot += c[j]; }
-            uint64_t incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint64_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= (uint32_t)o) incl += v;
-            }
-            const uint64_t excl = incl - tot;
-            const unsigned hit = __ballot_sync(0xffffffffu, excl < kr && kr <= incl);
-            const uint32_t src = (uint32_t)(__ffs(hit) - 1);
-            uint64_t pre = 0, krn = 0;
-            if (lane == src) {
-                uint64_t cum = excl;
-                uint32_t dd = 255 - 8 * lane;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    if (kr <= cum + c[j]) { dd = 255 - 8 * lane - j; break; }
-                    cum += c[j];
-                }
-                pre = s_prefix[q] | ((uint64_t)dd << shift);
-                krn = kr - cum;
-            }
-            pre = __shfl_sync(0xffffffffu, pre, src);
-            krn = __shfl_sync(0xffffffffu, krn, src);
-            __syncwarp();
-            if (lane == 0) { s_prefix[q] = pre; s_krem[q] = krn; }
-        }
-        // the buffer pass + 2 will use was last read before this barrier: clear it
-        if (blockIdx.x == 0) {
-            uint32_t* gz = ghist + (size_t)((pass + 2) % 3) * nq * 256;
-            for (uint32_t i = threadIdx.x; i < nq * 256u; i += blockDim.x) gz[i] = 0;
-        }
-        __syncthreads();
-        for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x) {   // dedupe equal prefixes per row
-            const uint32_t q0 = q - q % n_rp;
-            uint32_t rr = q;
-            for (uint32_t j = q0; j < q; ++j)
-                if (s_prefix[j] == s_prefix[q]) { rr = j; break; }
-            s_rep[q] = rr;
-        }
-        __syncthreads();
-        for (uint32_t row = threadIdx.x; row < rows; row += blockDim.x) {   // per-row list of distinct prefixes
-            uint32_t nu = 0;
-            for (uint32_t q = row * n_rp; q < (row + 1) * n_rp; ++q)
-                if (s_rep[q] == q) { s_uq[row * n_rp + nu] = q; s_up[row * n_rp + nu] = s_prefix[q]; ++nu; }
-            s_nu[row] = nu;
-        }
-        __syncthreads();
-    }
 
-    // tail sums over this block's keys, then block 0 combines in block order
-    __shared__ double s_sum[256];
-    __shared__ uint64_t s_cnt[256];
-    for (uint32_t q = 0; q < nq; ++q) {
-        const uint32_t row = q / n_rp;
-        const uint64_t* kr = s_key + (uint64_t)row * per;
-        const uint64_t vk = s_prefix[q];
-        double sm = 0.0;
-        uint64_t c = 0;
-        for (uint32_t i = threadIdx.x; i < nk; i += blockDim.x) {   // fixed order: deterministic
-            const uint64_t key = kr[i];   // key order = value order (non-negative doubles)
-            if (key > vk) { sm = __dadd_rn(sm, __longlong_as_double((long long)key)); ++c; }
-        }
-        s_sum[threadIdx.x] = sm;
-        s_cnt[threadIdx.x] = c;
-        __syncthreads();
-        for (int w = 128; w >= 1; w >>= 1) {
-            if ((int)threadIdx.x < w) {
-                s_sum[threadIdx.x] = __dadd_rn(s_sum[threadIdx.x], s_sum[threadIdx.x + w]);
-                s_cnt[threadIdx.x] += s_cnt[threadIdx.x + w];
-            }
-            __syncthreads();
-        }
-        if (threadIdx.x == 0) {
-            P.part_sum[(uint64_t)q * gridDim.x + blockIdx.x] = s_sum[0];
-            P.part_cnt[(uint64_t)q * gridDim.x + blockIdx.x] = s_cnt[0];
-        }
-        __syncthreads();
+// The 8 passes + tail (+ the all-reduces when comm != null in distributed mode).
+cudaError_t launch_m3(const double* d_ylt, uint64_t T, uint64_t ld, uint32_t rows, uint32_t n_rp,
+                      const uint64_t* h_k, MetricsScratch& m, int nblk, bool dist, ncclComm_t comm,
+                      cudaStream_t s, int* nccl_err) {
+    M3Params P{};
+    P.ylt = d_ylt;
+    P.T = T;
+    P.ld = ld;
+    P.n_rp = n_rp;
+    P.nblk = (uint32_t)nblk;
+    P.rows = rows;
+    P.hist = m.hist8;
+    P.st = m.st;
+    P.strep = m.strep;
+    P.part_sum = m.part_sum;
+    P.part_cnt = m.part_cnt;
+    P.done = m.done;
+    P.out = m.out;
+    P.dsum = m.dsum;
+    P.dcnt = m.dcnt;
+    P.dist = dist ? 1 : 0;
+    for (uint32_t i = 0; i < n_rp; ++i) P.k[i] = h_k[i];
+    const char* m3_env = getenv("ARA_METRICS_M3");   // A/B and tests: the general path for any n_rp
+    const int m4_off = m3_env ? atoi(m3_env) : 0;
+    if (n_rp <= M4_MAXM && !m4_off) return launch_m4(P, m, dist, comm, s, nccl_err);
+    const size_t smem = (size_t)n_rp * 256 * sizeof(uint32_t);
+    static size_t smem_set = 0;
+    if (smem > 32 * 1024 && smem > smem_set) {
+        cudaError_t e = cudaFuncSetAttribute(m3_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        smem_set = smem;
     }
-    grid.sync();
-    if (blockIdx.x != 0) return;
-    for (uint32_t q = wid; q < nq; q += blockDim.x >> 5) {
-        const double v = __longlong_as_double((long long)s_prefix[q]);
-        const double* ps = P.part_sum + (uint64_t)q * gridDim.x;
-        const uint64_t* pc = P.part_cnt + (uint64_t)q * gridDim.x;
-        double sm = 0.0;
-        uint64_t c = 0;
-        for (uint32_t b0 = 0; b0 < gridDim.x; b0 += 32) {
-            const uint32_t b = b0 + lane;
-            const double x = b < gridDim.x ? __ldcg(ps + b) : 0.0;
-            const uint64_t yy = b < gridDim.x ? __ldcg(pc + b) : 0ull;
-            for (uint32_t j = 0; j < 32 && b0 + j < gridDim.x; ++j) {   // sequential, block order
-                sm = __dadd_rn(sm, __shfl_sync(0xffffffffu, x, j));
-                c += __shfl_sync(0xffffffffu, yy, j);
-            }
-        }
-        if (lane == 0) {
-            const uint64_t k = P.k[q % n_rp];
-            const double tail = __dadd_rn(sm, __dmul_rn((double)(k - c), v));
-            P.out[(uint64_t)q * 2 + 0] = v;
-            P.out[(uint64_t)q * 2 + 1] = __ddiv_rn(tail, (double)k);
+    if (nccl_err) *nccl_err = 0;
+    const size_t nh = (size_t)rows * n_rp * 256;
+    cudaError_t e = cudaSuccess;
+    for (int pass = 0; pass < 8 && e == cudaSuccess; ++pass) {
+        // PDL between our own consecutive kernels only (not after NCCL or the caller's work)
+        e = launch_pdl(m3_pass_kernel, dim3(nblk, rows), dim3(M3_THREADS), smem, s, pass > 0 && !comm, P, pass);
+        if (e == cudaSuccess && comm &&
+            ncclAllReduce(P.hist + pass * nh, P.hist + pass * nh, nh, ncclUint32, ncclSum, comm, s) != ncclSuccess) {
+            *nccl_err = 1;
+            break;
         }
     }
+    if (e == cudaSuccess && !(nccl_err && *nccl_err))
+        e = launch_pdl(m3_tail_kernel, dim3(nblk, rows), dim3(M3_THREADS), 0, s, !comm, P);
+    if (e == cudaSuccess && !(nccl_err && *nccl_err) && dist) {
+        const size_t nq = (size_t)rows * n_rp;
+        if (comm && (ncclGroupStart() != ncclSuccess || ncclAllReduce(P.dsum, P.dsum, nq, ncclDouble, ncclSum, comm, s) != ncclSuccess ||
+                     ncclAllReduce(P.dcnt, P.dcnt, nq, ncclUint64, ncclSum, comm, s) != ncclSuccess ||
+                     ncclGroupEnd() != ncclSuccess))
+            *nccl_err = 1;
+        else
+            m3_finish_kernel<<<1, 256, 0, s>>>(P);
+    }
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess || (nccl_err && *nccl_err)) {
+        // a partial sequence may leave histograms dirty: clear them for the next call
+        cudaGetLastError();
+        cudaMemsetAsync(m.hist8, 0, 8 * nh * sizeof(uint32_t), s);
+        if (e == cudaSuccess) e = cudaGetLastError();
+    }
+    return e;
 }
+
 
 }  // namespace
 
 cudaError_t launch_metrics_dist(const double* d_ylt, uint64_t T_local, uint64_t ld, uint32_t rows, uint32_t n_rp,
                                 const uint64_t* h_k, MetricsScratch& m, int nblk, ncclComm_t comm,
                                 cudaStream_t s, int* nccl_err) {
-    MParams P{};
-    P.ylt = d_ylt;
-    P.T = T_local;
-    P.ld = ld;
-    P.n_rp = n_rp;
-    P.nblk = (uint32_t)nblk;
-    P.hist = m.hist;
-    P.prefix = m.prefix;
-    P.krem = m.krem;
-    P.part_sum = m.part_sum;
-    P.part_cnt = m.part_cnt;
-    P.out = m.out;
-    P.done = m.done;
-    P.rep = m.done + rows;
-    P.dsum = m.dsum;
-    P.dcnt = m.dcnt;
-    P.dist = 1;
-    for (uint32_t i = 0; i < n_rp; ++i) P.k[i] = h_k[i];
-    const size_t smem = (size_t)n_rp * 256 * sizeof(uint32_t);
-    if (smem > 32 * 1024) {   // leaves room for the kernels' static shared memory under the 48 KB default
-        cudaError_t e = cudaFuncSetAttribute(radix_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    *nccl_err = 0;
-    init_kernel<<<rows, 256, 0, s>>>(P);
-    const size_t nh = (size_t)rows * n_rp * 256;
-    for (int pass = 0; pass < 8; ++pass) {
-        radix_pass_kernel<<<dim3(P.nblk, rows), 256, smem, s>>>(P, pass);
-        // comm == null: a single shard (world 1, ARA_METRICS_DIST / loopback): the reduce is the identity
-        if (comm && ncclAllReduce(P.hist, P.hist, nh, ncclUint32, ncclSum, comm, s) != ncclSuccess) { *nccl_err = 1; break; }
-        select_kernel<<<rows, 256, smem, s>>>(P, pass);
-    }
-    if (*nccl_err) return cudaGetLastError();
-    tail_kernel<<<dim3(P.nblk, rows), 256, 0, s>>>(P);
-    const size_t nq = (size_t)rows * n_rp;
-    if (comm && (ncclGroupStart() != ncclSuccess || ncclAllReduce(P.dsum, P.dsum, nq, ncclDouble, ncclSum, comm, s) != ncclSuccess ||
-        ncclAllReduce(P.dcnt, P.dcnt, nq, ncclUint64, ncclSum, comm, s) != ncclSuccess || ncclGroupEnd() != ncclSuccess)) {
-        *nccl_err = 1;
-        return cudaGetLastError();
-    }
-    finish_kernel<<<1, 256, 0, s>>>(P, rows);
-    return cudaGetLastError();
+    return launch_m3(d_ylt, T_local, ld, rows, n_rp, h_k, m, nblk, true, comm, s, nccl_err);
 }
 
 cudaError_t metrics_alloc(MetricsScratch& m, uint32_t rows, uint32_t n_rp, int nblk) {
@@ -584,16 +955,17 @@ cudaError_t metrics_alloc(MetricsScratch& m, uint32_t rows, uint32_t n_rp, int n
     metrics_free(m);
     const size_t rr = need;
     cudaError_t e;
-    if ((e = cudaMalloc(&m.hist, rr * 256 * sizeof(uint32_t))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&m.prefix, rr * sizeof(uint64_t) * 2 + rr * sizeof(uint32_t))) != cudaSuccess) return e;
-    m.krem = m.prefix + rr;
     if ((e = cudaMalloc(&m.part_sum, rr * nblk * sizeof(double))) != cudaSuccess) return e;
     if ((e = cudaMalloc(&m.part_cnt, rr * nblk * sizeof(uint64_t))) != cudaSuccess) return e;
     if ((e = cudaMalloc(&m.out, rr * 2 * sizeof(double))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&m.done, rows * sizeof(uint32_t) + rr * sizeof(uint32_t))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&m.coop_hist, 3 * rr * 256 * sizeof(uint32_t))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&m.done, rows * sizeof(uint32_t))) != cudaSuccess) return e;
     if ((e = cudaMalloc(&m.dsum, rr * sizeof(double))) != cudaSuccess) return e;
     if ((e = cudaMalloc(&m.dcnt, rr * sizeof(uint64_t))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&m.hist8, 8 * rr * 256 * sizeof(uint32_t))) != cudaSuccess) return e;
+    if ((e = cudaMemset(m.hist8, 0, 8 * rr * 256 * sizeof(uint32_t))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&m.st, 2 * rr * 2 * sizeof(uint64_t))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&m.strep, 2 * rr * sizeof(uint32_t))) != cudaSuccess) return e;
+    if ((e = cudaMemset(m.done, 0, rows * sizeof(uint32_t))) != cudaSuccess) return e;
     m.cap_rows_rp = need;
     m.cap_rows = rows;
     m.nblk = nblk;
@@ -601,82 +973,26 @@ cudaError_t metrics_alloc(MetricsScratch& m, uint32_t rows, uint32_t n_rp, int n
 }
 
 void metrics_free(MetricsScratch& m) {
-    cudaFree(m.hist);
-    cudaFree(m.prefix);
     cudaFree(m.part_sum);
     cudaFree(m.part_cnt);
     cudaFree(m.out);
     cudaFree(m.done);
-    cudaFree(m.coop_hist);
     cudaFree(m.dsum);
     cudaFree(m.dcnt);
+    cudaFree(m.hist8);
+    cudaFree(m.st);
+    cudaFree(m.strep);
+    cudaFree(m.cand);
+    cudaFree(m.cand_n);
+    cudaFree(m.bsum);
+    cudaFree(m.bcnt);
+    if (m.m4_exec) cudaGraphExecDestroy(m.m4_exec);
     m = MetricsScratch{};
 }
 
 cudaError_t launch_metrics(const double* d_ylt, uint64_t T, uint64_t ld, uint32_t rows,
                            uint32_t n_rp, const uint64_t* h_k, MetricsScratch& m, int nblk, cudaStream_t s) {
-    MParams P{};
-    P.ylt = d_ylt;
-    P.T = T;
-    P.ld = ld;
-    P.n_rp = n_rp;
-    P.nblk = (uint32_t)nblk;
-    P.hist = m.hist;
-    P.prefix = m.prefix;
-    P.krem = m.krem;
-    P.part_sum = m.part_sum;
-    P.part_cnt = m.part_cnt;
-    P.out = m.out;
-    P.done = m.done;
-    P.rep = m.done + rows;
-    for (uint32_t i = 0; i < n_rp; ++i) P.k[i] = h_k[i];
-    const size_t smem = (size_t)n_rp * 256 * sizeof(uint32_t);
-    if (smem > 32 * 1024) {   // leaves room for the kernels' static shared memory under the 48 KB default
-        cudaError_t e = cudaFuncSetAttribute(radix_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-    }
-    // One cooperative launch (ARA_METRICS_COOP=1, when the per-block state
-    // fits in shared memory); otherwise 10 plain launches (default).
-    const CoopLayout Lo = coop_layout(rows, n_rp);
-    static int coop_ok = -1, n_sm = 0, per_sm = 0;
-    if (coop_ok < 0) {   // measured slower than the multi-launch path on B200 (0.34 vs 0.23 ms at
-                         // 2 x 1M keys): opt-in with ARA_METRICS_COOP=1 for A/B runs
-        int dev = 0, attr = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&attr, cudaDevAttrCooperativeLaunch, dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-        coop_ok = attr ? 1 : 0;
-    }
-    const char* coop_env = getenv("ARA_METRICS_COOP");
-    const bool coop_on = coop_ok && coop_env && atoi(coop_env) != 0;
-    // Grid: two blocks per SM; each block stages rows x ceil(T / grid) keys.
-    int grid = 2 * n_sm;
-    if (grid > m.nblk) grid = m.nblk;   // partial-sum capacity
-    const uint64_t want = (T + 255) / 256;
-    if ((uint64_t)grid > want) grid = (int)want;
-    const uint64_t per = grid > 0 ? (T + grid - 1) / grid : 0;
-    const size_t cbytes = Lo.bytes + (size_t)rows * per * sizeof(uint64_t);
-    if (coop_on && grid >= 1 && cbytes <= 110 * 1024 && m.coop_hist && (size_t)rows * n_rp <= m.cap_rows_rp) {
-        cudaFuncSetAttribute(metrics_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cbytes);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, metrics_coop_kernel, 256, cbytes) != cudaSuccess)
-            per_sm = 0;
-        cudaGetLastError();
-        if ((int64_t)per_sm * n_sm >= grid) {
-            cudaError_t e = cudaMemsetAsync(m.coop_hist, 0, (size_t)3 * Lo.nq * 256 * sizeof(uint32_t), s);
-            if (e != cudaSuccess) return e;
-            uint32_t* gh = m.coop_hist;
-            void* args[] = {(void*)&P, (void*)&rows, (void*)&gh};
-            e = cudaLaunchCooperativeKernel((void*)metrics_coop_kernel, dim3(grid), dim3(256), args, cbytes, s);
-            if (e == cudaSuccess) return cudaSuccess;
-            cudaGetLastError();   // fall through to the multi-launch path
-        }
-    }
-    init_kernel<<<rows, 256, 0, s>>>(P);
-    for (int pass = 0; pass < 8; ++pass)
-        radix_pass_kernel<<<dim3(P.nblk, rows), 256, smem, s>>>(P, pass);
-    tail_kernel<<<dim3(P.nblk, rows), 256, 0, s>>>(P);
-    return cudaGetLastError();
+    return launch_m3(d_ylt, T, ld, rows, n_rp, h_k, m, nblk, false, nullptr, s, nullptr);
 }
 
 }  // namespace ara

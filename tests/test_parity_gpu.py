@@ -280,18 +280,35 @@ def test_set_elt_terms_equals_fresh_load(cuda):
 
 
 @pytest.mark.parametrize("rows_rho", [(1, 0.3), (3, 0.02)])
-def test_metrics_single_launch_path_matches_oracle(cuda, rows_rho):
-    """ARA_METRICS_COOP=1: the cooperative single-launch radix select gives the
-    oracle's PML (bit for bit) and TVaR, like the default multi-launch path."""
+@pytest.mark.parametrize("graph", [0, 1])
+def test_metrics_general_path_matches_oracle(cuda, rows_rho, graph):
+    """The two launch sequences of the radix select — the fast path (n_rp <= 11:
+    three full sweeps, then the 16-bit-prefix candidates; default) and the
+    general one (ARA_METRICS_M3=1: eight full sweeps) — each give the oracle's PML
+    (bit for bit) and TVaR, with and without the CUDA graph of the fast path."""
     n_layers, rho = rows_rho
     w = synth.get_config("tiny").with_(n_trials=5003, rho=rho, return_periods=(1, 2, 3.5, 10, 100, 1000, 5003))
     layers = tuple(synth.LayerSpec(0, 3, 2.5e4 * (i + 1), 5e5, 6.5e6 / (i + 1), 2.5e6) for i in range(n_layers))
     off, ids, elts = make_inputs(w)
     orc = run_oracle(off, ids, elts, w, layers)
-    _, _, _, met = run_gpu(off, ids, elts, w, layers, return_periods=w.return_periods, env={"ARA_METRICS_COOP": 1})
-    _, _, _, met0 = run_gpu(off, ids, elts, w, layers, return_periods=w.return_periods)
+    _, _, _, met = run_gpu(off, ids, elts, w, layers, return_periods=w.return_periods, env={"ARA_METRICS_M3": 1})
+    _, _, _, met0 = run_gpu(off, ids, elts, w, layers, return_periods=w.return_periods, env={"ARA_METRICS_GRAPH": graph})
     assert_metrics_close(met, oracle_rows(orc), orc["scale"], w.return_periods)
+    assert_metrics_close(met0, oracle_rows(orc), orc["scale"], w.return_periods)
     assert np.array_equal(met[1], met0[1]) and np.allclose(met[2], met0[2], rtol=1e-12, atol=0)
+
+
+def test_metrics_many_return_periods(cuda):
+    """n_rp = 40 (> 11: the general path) and 11 (the fast path's limit) on the
+    same YLT: PML bit for bit, TVaR within tolerance of the oracle."""
+    rps = tuple(float(x) for x in np.unique(np.geomspace(1, 5003, 40).round(2)))
+    w = synth.get_config("tiny").with_(n_trials=5003, rho=0.2, return_periods=rps)
+    off, ids, elts = make_inputs(w)
+    orc = run_oracle(off, ids, elts, w, w.layers)
+    _, _, _, met = run_gpu(off, ids, elts, w, w.layers, return_periods=rps)
+    assert_metrics_close(met, oracle_rows(orc), orc["scale"], rps)
+    _, _, _, met11 = run_gpu(off, ids, elts, w, w.layers, return_periods=rps[::4][:11])
+    assert_metrics_close(met11, oracle_rows(orc), orc["scale"], rps[::4][:11])
 
 
 def test_metrics_ties_extremes(cuda):

@@ -2,7 +2,7 @@
 mkdir -p gpurun_out
 N=$(nvidia-smi -L | wc -l)
 timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/pytest_n$N.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_n$N.log
-for n in 2 $N; do
+for n in 1 2 $N; do
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2971$n bench.py --gpus $n --steps 20 > gpurun_out/fw_n$n.json 2> gpurun_out/fw_n$n.err
   timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port 2972$n bench.py --gpus $n --steps 20 --scaling strong --no-cpu-baseline --no-e2e > gpurun_out/fs_n$n.json 2> gpurun_out/fs_n$n.err
 done
