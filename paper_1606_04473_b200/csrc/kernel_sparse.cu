@@ -281,15 +281,16 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
     // (full: the whole batch belongs to the trial -- no position masks, and
     // invalid ids are caught by a running minimum instead of a per-event test)
     uint32_t xmin = 1u;   // min over the ids of full batches (0 = an id outside [1, C])
-    // append the occupied events of one group (ballot Mj), in stream order
-    auto append = [&](uint32_t Mj, uint32_t xj) {
-        uint32_t ltm;
-        asm("mov.u32 %0, %%lanemask_lt;" : "=r"(ltm));
+    uint32_t ltm;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(ltm));
+    // append the occupied events of one group (ballot Mj; this lane's event is
+    // occupied iff own != 0), in stream order: slot tail + popc(Mj below lane)
+    auto append = [&](uint32_t Mj, uint32_t own, uint32_t xj) {
         const uint32_t slot = (tail + __popc(Mj & ltm)) & (uint32_t)(Geo::CBUF - 1);
         // predicated store (no branch around it)
         asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.shared.u32 [%0], %1;\n\t}" ::"r"(
                          cbuf + slot * 4u),
-                     "r"(xj), "r"((Mj >> lane) & 1u)
+                     "r"(xj), "r"(own)
                      : "memory");
         tail += __popc(Mj);
     };
@@ -307,15 +308,37 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
             const bool live = full || k - dlo < span;
             if (full) xmin = min(xmin, x[j]);
             else err |= (live && x[j] == 0u) ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
+            if (j < 3) {
+                // probe bit, ballot and stream-order append in one block (the
+                // predicate feeds both the vote and the store)
+                uint32_t M;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t.reg .b32 r, a;\n\t"
+                    "shf.r.wrap.b32 r, %1, %1, %2;\n\t"
+                    "and.b32 r, r, %3;\n\t"
+                    "setp.ne.u32 p, r, 0;\n\t"
+                    "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+                    "and.b32 a, %0, %4;\n\t"
+                    "popc.b32 a, a;\n\t"
+                    "add.u32 a, a, %5;\n\t"
+                    "and.b32 a, a, %6;\n\t"
+                    "mad.lo.u32 a, a, 4, %7;\n\t"
+                    "@p st.shared.u32 [a], %2;\n\t}"
+                    : "=r"(M)
+                    : "r"(wd[j]), "r"(x[j]), "r"(live ? 1u : 0u), "r"(ltm), "r"(tail), "n"(Geo::CBUF - 1), "r"(cbuf)
+                    : "memory");
+                tail += __popc(M);
+                continue;
+            }
             uint32_t r;
             asm("shf.r.wrap.b32 %0, %1, %1, %2;" : "=r"(r) : "r"(wd[j]), "r"(x[j]));
-            const bool occ = live && (r & 1u);
-            const uint32_t M = __ballot_sync(0xffffffffu, occ);
+            const uint32_t own = live ? (r & 1u) : 0u;
+            const uint32_t M = __ballot_sync(0xffffffffu, own != 0u);
             if (j == 3 && tail - head + __popc(M) > (uint32_t)Geo::CBUF) {
                 M3 = M;
                 break;
             }
-            append(M, x[j]);
+            append(M, own, x[j]);
         }
     };
     // a7 tree + a8 stores of trial t (lane 0), accumulators reset
@@ -460,7 +483,7 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
                     issue_round(i);
                 }
                 if (!M3) break;
-                append(M3, (c & 1u) ? xb[3] : xa[3]);   // the deferred group 3 now fits
+                append(M3, (M3 >> lane) & 1u, (c & 1u) ? xb[3] : xa[3]);   // the deferred group 3 now fits
                 M3 = 0;
             }
             if (fin) break;
