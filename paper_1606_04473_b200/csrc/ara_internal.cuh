@@ -46,7 +46,7 @@ struct TableGeo {
     uint32_t epb = 0;            // elements per block row
     uint32_t n_blocks = 0;
     uint64_t block_elems = 0;    // (C+1) * epb
-    uint64_t bm_words = 0;       // row-occupancy bitmap words per block (ceil((C+1)/32), padded)
+    uint64_t bm_words = 0;       // row-occupancy bitmap words per block (ceil((C+2)/32), padded)
     size_t bm_off = 0;           // byte offset of the bitmaps in the allocation
     size_t occ_off = 0;          // byte offset of the per-block occupied-row counters (u32)
     size_t pk_off = 0;           // byte offset of the packed-row slots (kPackBytes per event per block)
@@ -65,7 +65,9 @@ inline TableGeo table_geometry(uint32_t n_elts, uint32_t catalog, int fp32) {
     // record (e, j) exists for some column j of the block.  A clear bit means
     // the row is all zeros, so its lookup can be skipped (a zero row adds an
     // exact +0 to every sum: every deductible and retention is >= 0).
-    g.bm_words = (((uint64_t)catalog + 1 + 31) / 32 + 63) / 64 * 64;
+    // bits 0 .. C + 1: bit C + 1 is padding that is never set (the sparse
+    // trial kernel clamps out-of-range ids to C + 1)
+    g.bm_words = (((uint64_t)catalog + 2 + 31) / 32 + 63) / 64 * 64;
     g.bm_off = ((size_t)g.n_blocks * g.block_elems * g.esz + kTablePadBytes + 255) / 256 * 256;
     g.occ_off = g.bm_off + (size_t)g.n_blocks * g.bm_words * 4;
     // Packed rows of the sparse blocks (one 32-B sector per event, written for

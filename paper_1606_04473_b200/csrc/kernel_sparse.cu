@@ -80,6 +80,19 @@ __device__ __forceinline__ void bulk_g2s_nohint(uint32_t dst, const void* src, u
                  "l"(src), "r"(bytes), "r"(bar)
                  : "memory");
 }
+// expect_tx + bulk copy issued by one lane chosen by elect.sync: the whole
+// (converged) warp executes this with warp-uniform operands, so no branch
+// around a single lane and no per-lane loop to make the operands uniform
+__device__ __forceinline__ void bulk_g2s_elect(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                               uint64_t pol) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%3], %2;\n\t"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        "\n\t}" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(pol)
+        : "memory");
+}
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
@@ -149,7 +162,7 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(16) double2 s_term[NLB][32];
     __shared__ __align__(8) uint64_t s_bar[Geo::WARPS * Geo::NSTG + 1];
-    __shared__ uintptr_t s_stream[Geo::WARPS][2];   // per warp: the id stream's 16-B aligned byte range
+    __shared__ __align__(16) uintptr_t s_stream[Geo::WARPS][2];   // per warp: the id stream's 16-B aligned byte range
     const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
     const uint32_t sbase = pin((uint32_t)__cvta_generic_to_shared(smem));
     const uint32_t ring = sbase + wib * (uint32_t)Geo::RING;
@@ -223,9 +236,10 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
     const int64_t P0 = S0 - (int64_t)((a_s - a0) >> 2);
     if (S1 - P0 > (int64_t)0x7fffff00) { err |= ERRBIT_OFFSETS; te = tb; S1 = S0; }   // > 2^31 events in one warp
     const uint32_t nchunks = S1 > S0 ? (uint32_t)((aend - a0 + Geo::CHB - 1) / Geo::CHB) : 0u;
-    // the stream's byte range lives in shared memory (lane 0 reads it when it
-    // refills a stage), not in registers
+    // the stream's byte range lives in shared memory (read when a stage is
+    // refilled), not in registers
     if (lane == 0) { s_stream[wib][0] = a0; s_stream[wib][1] = aend; }
+    const uint32_t s_str = pin((uint32_t)__cvta_generic_to_shared(&s_stream[wib][0]));
     // chunk c goes to stage c % NSTG; only the stream's last chunk is short
     auto issue_chunk = [&](uint32_t c) {   // lane 0
         const uintptr_t b0 = s_stream[wib][0], b1 = s_stream[wib][1];
@@ -253,15 +267,21 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             const uint32_t v = lds32(ra + 128u * j);
-            const uint32_t xc = v <= C ? v : 0u;   // (0 stays 0)
+            const uint32_t xc = min(v, C + 1u);   // C + 1: a padding bit, never occupied; 0: the zero row
             x[j] = xc;
             wd[j] = probe(xc >> 5, Ws, s_bm, bm);
         }
         if (half == BPC - 1 && ch + NSTG < nchunks) {   // the chunk's last batch: refill its stage
             __syncwarp();
-            if (lane == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // our reads precede the refill
-                issue_chunk(ch + NSTG);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // our reads precede the refill
+            {
+                const uint32_t c2 = ch + NSTG;
+                uint64_t b0, b1;   // the stream's byte range (shared memory, pinned address)
+                asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(b0), "=l"(b1) : "r"(s_str) : "memory");
+                const uintptr_t src = b0 + (uintptr_t)c2 * Geo::CHB;
+                const uint32_t bytes = c2 + 1 < nchunks ? (uint32_t)Geo::CHB : (uint32_t)(b1 - src);
+                bulk_g2s_elect(ring + st * Geo::CHB, reinterpret_cast<const void*>(src), bytes, bar0 + 8u * st,
+                               policy_evict_first());
             }
         }
     };
@@ -279,8 +299,8 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
     // scan the current batch over its positions [dlo, dhi): append the
     // occupied events in stream order
     // (full: the whole batch belongs to the trial -- no position masks, and
-    // invalid ids are caught by a running minimum instead of a per-event test)
-    uint32_t xmin = 1u;   // min over the ids of full batches (0 = an id outside [1, C])
+    // invalid ids are caught by a running maximum of id - 1 instead of a per-event test)
+    uint32_t idm1 = 0u;   // max of id - 1 over the ids of full batches (>= C: an id outside [1, C])
     uint32_t ltm;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(ltm));
     // append the occupied events of one group (ballot Mj; this lane's event is
@@ -306,8 +326,8 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
         for (int j = 0; j < 4; ++j) {
             const uint32_t k = 32u * j + lane;
             const bool live = full || k - dlo < span;
-            if (full) xmin = min(xmin, x[j]);
-            else err |= (live && x[j] == 0u) ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
+            if (full) idm1 = max(idm1, x[j] - 1u);   // x - 1 >= C (unsigned): an id outside [1, C]
+            else err |= (live && x[j] - 1u >= C) ? (uint32_t)ERRBIT_EVENT_RANGE : 0u;
             if (j < 3) {
                 // probe bit, ballot and stream-order append in one block (the
                 // predicate feeds both the vote and the store)
@@ -380,7 +400,8 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
             uint32_t mm = mask;
 #pragma unroll
             for (int v = 0; v < CAP; ++v) {
-                if (!__any_sync(0xffffffffu, mm != 0u)) break;
+                // (a round always holds an occupied event, mask != 0: v = 0 needs no vote)
+                if (v > 0 && !__any_sync(0xffffffffu, mm != 0u)) break;
                 const uint32_t b = (uint32_t)(__ffs(mm) - 1);   // 0xffffffff when mm == 0
                 mm &= mm - 1u;
                 const uint32_t j = b - p.pk_col0;                // window element (wraps when b < col0)
@@ -508,7 +529,7 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
     const uint32_t loaded = waited_ch < nchunks ? waited_ch : nchunks;
     const uint32_t issued = NSTG + (c + 2) / BPC < nchunks ? NSTG + (c + 2) / BPC : nchunks;
     for (uint32_t cc = loaded; cc < issued; ++cc) mbar_wait(bar0 + 8u * (cc & (NSTG - 1)), (cc / NSTG) & 1u);
-    if (xmin == 0u) err |= ERRBIT_EVENT_RANGE;
+    if (idm1 >= C) err |= ERRBIT_EVENT_RANGE;
     if (lane == 0 && p.n_gathered && tail) atomicAdd(p.n_gathered, (unsigned long long)tail);   // queue entries = gathers
     peer_fence(p);
     if (err) atomicOr(p.err, err);
