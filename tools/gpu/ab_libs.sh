@@ -1,5 +1,5 @@
 # A/B of several builds of libara.so on one box: every ab/*.so (plus the
-# in-tree build as "tree"): oracle checks (tools/bc_check.py), then timings
+# in-tree build as "tree"): oracle checks (tests/gpu_check_bc.py), then timings
 # interleaved over REPS rounds.  EXTRA_CFG: more prof_ara.py argument sets,
 # separated by ';' (e.g. "--config tower;--precision f32").
 mkdir -p gpurun_out
@@ -8,7 +8,7 @@ mkdir -p gpurun_out
 LIBS="$(ls $PWD/ab/*.so 2>/dev/null) $PWD/paper_1606_04473_b200/libara.so"
 for lib in $LIBS; do
   n=$(basename $(dirname $lib))_$(basename $lib .so)
-  ARA_LIB_PATH=$lib timeout 400 python tools/bc_check.py 30 > gpurun_out/ab_check_$n.log 2>&1
+  ARA_LIB_PATH=$lib timeout 400 python tests/gpu_check_bc.py 30 > gpurun_out/ab_check_$n.log 2>&1
   echo "$n check rc=$? $(tail -1 gpurun_out/ab_check_$n.log)" >> gpurun_out/ab_summary.txt
 done
 IFS=';' read -ra CFGS <<< "${EXTRA_CFG:-}"

@@ -1,8 +1,8 @@
 # trial_kernel_bc shared-memory filter A/B: exact + pair words (default) vs
 # exact words only (ARA_BC_NO_PAIRS=1, the rest probed in L1/L2); oracle checks first.
 mkdir -p gpurun_out
-timeout 400 python tools/bc_check.py 30 > gpurun_out/pairs_check.log 2>&1; echo "check rc=$? $(tail -1 gpurun_out/pairs_check.log)"
-ARA_BC_NO_PAIRS=1 timeout 400 python tools/bc_check.py 30 > gpurun_out/pairs_check_nopairs.log 2>&1; echo "check nopairs rc=$? $(tail -1 gpurun_out/pairs_check_nopairs.log)"
+timeout 400 python tests/gpu_check_bc.py 30 > gpurun_out/pairs_check.log 2>&1; echo "check rc=$? $(tail -1 gpurun_out/pairs_check.log)"
+ARA_BC_NO_PAIRS=1 timeout 400 python tests/gpu_check_bc.py 30 > gpurun_out/pairs_check_nopairs.log 2>&1; echo "check nopairs rc=$? $(tail -1 gpurun_out/pairs_check_nopairs.log)"
 : > gpurun_out/pairs_ab.jsonl
 for rep in 1 2; do
   for env in "ARA_BC_NO_PAIRS=0" "ARA_BC_NO_PAIRS=1"; do
