@@ -168,8 +168,11 @@ struct MetricsScratch {
     double* bsum = nullptr;         // slot partial sums / counts per block (fast path)
     uint64_t* bcnt = nullptr;
     uint64_t cand_cap = 0, cand_n_cap = 0, bpart_cap = 0;
-    cudaGraphExec_t m4_exec = nullptr;   // the fast path's launch sequence, keyed by its arguments
-    unsigned char m4_key[1024] = {};
+    // the fast path's launch sequences, keyed by their arguments: two entries,
+    // because consecutive multi-GPU runs alternate between two global-YLT buffers
+    cudaGraphExec_t m4_exec[2] = {nullptr, nullptr};
+    unsigned char m4_key[2][1024] = {};
+    int m4_next = 0;                     // the entry a new capture replaces
     size_t cap_rows_rp = 0;
     uint32_t cap_rows = 0;
     int nblk = 0;                   // capacity in blocks

@@ -811,34 +811,58 @@ cudaError_t launch_m4(const M3Params& P, MetricsScratch& m, bool dist, ncclComm_
             if (r == cudaSuccess) red(pass);
         }
         if (r == cudaSuccess && !(nccl_err && *nccl_err)) r = launch_pdl(m4_tail_kernel, grid, blk, 0, s, pdl, Q);
+        if (r == cudaSuccess && !(nccl_err && *nccl_err) && dist) {   // the all-reduced tail sums -> TVaR
+            const size_t nq = (size_t)rows * n_rp;
+            if (comm && (ncclGroupStart() != ncclSuccess ||
+                         ncclAllReduce(P.dsum, P.dsum, nq, ncclDouble, ncclSum, comm, s) != ncclSuccess ||
+                         ncclAllReduce(P.dcnt, P.dcnt, nq, ncclUint64, ncclSum, comm, s) != ncclSuccess ||
+                         ncclGroupEnd() != ncclSuccess))
+                *nccl_err = 1;
+            else
+                m3_finish_kernel<<<1, 256, 0, s>>>(P);
+            r = cudaGetLastError();
+        }
         return r;
     };
-    // Single-GPU launches go through a CUDA graph of the 9 kernels (with their
-    // programmatic-launch edges), re-captured when any argument changes.
+    // Launches without NCCL go through a CUDA graph of the kernels (with their
+    // programmatic-launch edges), re-captured when any argument changes.  The
+    // distributed select with NCCL all-reduces between the passes is launched
+    // eagerly: captured into a graph it hung at N = 4 (profiles/README.md).
     const char* g_env = getenv("ARA_METRICS_GRAPH");
     const bool use_graph = !g_env || atoi(g_env);
-    static_assert(sizeof(M4Params) <= sizeof(m.m4_key), "graph key buffer");
+    static_assert(sizeof(M4Params) + sizeof(cudaStream_t) + sizeof(ncclComm_t) + 1 <= sizeof(m.m4_key[0]),
+                  "graph key buffer");
     if (!comm && !trace && use_graph) {
-        unsigned char key[sizeof(m.m4_key)] = {};
+        unsigned char key[sizeof(m.m4_key[0])] = {};
         std::memcpy(key, &Q, sizeof(Q));
         std::memcpy(key + sizeof(Q), &s, sizeof(s));
-        if (!m.m4_exec || std::memcmp(key, m.m4_key, sizeof(key)) != 0) {
-            if (m.m4_exec) cudaGraphExecDestroy(m.m4_exec);
-            m.m4_exec = nullptr;
+        std::memcpy(key + sizeof(Q) + sizeof(s), &comm, sizeof(comm));
+        key[sizeof(Q) + sizeof(s) + sizeof(comm)] = dist ? 1 : 0;
+        int hit = -1;
+        for (int q = 0; q < 2; ++q)
+            if (m.m4_exec[q] && std::memcmp(key, m.m4_key[q], sizeof(key)) == 0) hit = q;
+        if (hit < 0) {
+            const int q = m.m4_next;
+            m.m4_next ^= 1;
+            if (m.m4_exec[q]) cudaGraphExecDestroy(m.m4_exec[q]);
+            m.m4_exec[q] = nullptr;
             cudaGraph_t g = nullptr;
             if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
                 const cudaError_t r = enqueue();
                 const cudaError_t r2 = cudaStreamEndCapture(s, &g);
+                if (nccl_err && *nccl_err) *nccl_err = 0;   // retried below without the graph
                 if (r == cudaSuccess && r2 == cudaSuccess && g &&
-                    cudaGraphInstantiate(&m.m4_exec, g, 0) == cudaSuccess)
-                    std::memcpy(m.m4_key, key, sizeof(key));
-                else
-                    m.m4_exec = nullptr;
+                    cudaGraphInstantiate(&m.m4_exec[q], g, 0) == cudaSuccess) {
+                    std::memcpy(m.m4_key[q], key, sizeof(key));
+                    hit = q;
+                } else {
+                    m.m4_exec[q] = nullptr;
+                }
                 if (g) cudaGraphDestroy(g);
             }
             cudaGetLastError();   // a stream that cannot be captured: plain launches below
         }
-        if (m.m4_exec) e = cudaGraphLaunch(m.m4_exec, s);
+        if (hit >= 0) e = cudaGraphLaunch(m.m4_exec[hit], s);
         else e = enqueue();
     } else {
         mark();
@@ -854,15 +878,6 @@ cudaError_t launch_m4(const M3Params& P, MetricsScratch& m, bool dist, ncclComm_
             fprintf(stderr, " %.1f", ms * 1e3f);
         }
         fprintf(stderr, "\n");
-    }
-    if (e == cudaSuccess && !(nccl_err && *nccl_err) && dist) {
-        const size_t nq = (size_t)rows * n_rp;
-        if (comm && (ncclGroupStart() != ncclSuccess || ncclAllReduce(P.dsum, P.dsum, nq, ncclDouble, ncclSum, comm, s) != ncclSuccess ||
-                     ncclAllReduce(P.dcnt, P.dcnt, nq, ncclUint64, ncclSum, comm, s) != ncclSuccess ||
-                     ncclGroupEnd() != ncclSuccess))
-            *nccl_err = 1;
-        else
-            m3_finish_kernel<<<1, 256, 0, s>>>(P);
     }
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess || (nccl_err && *nccl_err)) {
@@ -986,7 +1001,8 @@ void metrics_free(MetricsScratch& m) {
     cudaFree(m.cand_n);
     cudaFree(m.bsum);
     cudaFree(m.bcnt);
-    if (m.m4_exec) cudaGraphExecDestroy(m.m4_exec);
+    for (auto& x : m.m4_exec)
+        if (x) cudaGraphExecDestroy(x);
     m = MetricsScratch{};
 }
 
