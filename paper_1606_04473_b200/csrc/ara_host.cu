@@ -1329,9 +1329,12 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
     // Distributed select (F4) on large global YLTs: every rank histograms only
     // its own shard and the histograms are all-reduced, instead of every rank
     // sweeping the whole global YLT (which grows with N under weak scaling).
+    // Crossover measured at N = 4 weak (4M trials): the graph-launched global
+    // sweep 0.198 ms vs the eager distributed select 0.274 ms, so the
+    // distributed form starts at 6M trials (profiles/r02_final2_fw_n4*.json).
     // (world 1 with ARA_METRICS_DIST=1 or loopback: the same passes with an identity reduce)
     const bool dist = ctx->lb_world > 0 || ctx->metrics_dist > 0 ||
-                      (ctx->world > 1 && ctx->metrics_dist < 0 && T >= 3000000);
+                      (ctx->world > 1 && ctx->metrics_dist < 0 && T >= 6000000);
     if (dist) {
         int nerr = 0;
         const uint64_t Tl = ctx->run_T_local;
