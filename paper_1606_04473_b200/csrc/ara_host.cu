@@ -11,6 +11,7 @@
 #include <cstring>
 #include <cstdlib>
 #include <new>
+#include <chrono>
 #include <thread>
 
 #include <nvtx3/nvToolsExt.h>
@@ -23,9 +24,19 @@ namespace {
 
 // NVTX range around each API call and each streamed chunk (host side: the
 // enqueue structure; an nsys timeline pairs it with the copy / kernel rows)
+// ARA_HOST_TRACE=1: host timestamps (us) of the API calls' phases on stderr,
+// to see where a step's GPU idle time comes from (diagnostic only)
+inline void host_trace(const char* what) {
+    static const bool on = [] { const char* v = getenv("ARA_HOST_TRACE"); return v && atoi(v); }();
+    if (!on) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    fprintf(stderr, "HT %.1f %s\n", us, what);
+}
+
 struct Nvtx {
-    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
-    ~Nvtx() { nvtxRangePop(); }
+    explicit Nvtx(const char* name) : name_(name) { nvtxRangePushA(name); host_trace(name_); }
+    ~Nvtx() { nvtxRangePop(); host_trace("return"); }
+    const char* name_;
     Nvtx(const Nvtx&) = delete;
     Nvtx& operator=(const Nvtx&) = delete;
 };
@@ -375,6 +386,7 @@ ara_status densify_local(ara_ctx* ctx, uint32_t n_elts, uint64_t nrec, const Spa
     if (ast != ARA_OK) return ast;
     // a table whose non-zero rows are all marked in its bitmaps (a previous
     // densify) is cleared row by row; otherwise the whole allocation is zeroed
+    host_trace("densify_local");
     if (ctx->table_clean) CK(launch_clear_rows(ctx->d_table, ctx->geo, ctx->catalog, ctx->stream));
     else CK(cudaMemsetAsync(ctx->d_table, 0, ctx->geo.pk_off, ctx->stream));   // packed slots: written before read
     ctx->table_clean = false;
@@ -388,7 +400,9 @@ ara_status densify_local(ara_ctx* ctx, uint32_t n_elts, uint64_t nrec, const Spa
     uint32_t* h_occ = reinterpret_cast<uint32_t*>(ctx->h_small + 16);
     const bool small = nb <= 96;
     if (small) CK(cudaMemcpyAsync(h_occ, d_occ, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    host_trace("densify launched");
     CK(cudaStreamSynchronize(ctx->stream));
+    host_trace("densify synced");
     ctx->occ_rows.assign(nb, 0u);
     if (small) std::memcpy(ctx->occ_rows.data(), h_occ, nb * sizeof(uint32_t));
     else CK(cudaMemcpy(ctx->occ_rows.data(), d_occ, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost));
@@ -903,6 +917,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         groups.push_back({l, 1, q0, q1 - q0, wide});
     }
     cudaStream_t s = ctx->stream;
+    host_trace("run prepared");
     CK(cudaEventRecord(ctx->ev[0], s));
     CK(cudaMemsetAsync(ctx->d_err, 0, 16, s));   // error word + the sparse kernel's gathered-slot counter
 
@@ -1250,7 +1265,9 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         CK(cudaMemcpyAsync(ctx->h_small + 2, ctx->d_off + T_local, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     }
     CK(cudaEventRecord(ctx->ev[5], s));
+    host_trace("run launched");
     CK(cudaStreamSynchronize(s));
+    host_trace("run synced");
     if (stream_in) CK(cudaStreamSynchronize(ctx->copy_stream));
     const uint32_t bits = (uint32_t)(ctx->h_small[world == 1 ? 4 : 0] & 0xffffffffu);   // world > 1: all-reduced
     st = device_errors(ctx, bits);
@@ -1350,7 +1367,9 @@ extern "C" ara_status ara_metrics(ara_ctx* ctx, uint32_t n_rp, const double* ret
     CK(cudaEventRecord(ctx->ev[1], s));
     std::vector<double> out((size_t)rows * n_rp * 2);
     CK(cudaMemcpyAsync(out.data(), ctx->ms.out, out.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+    host_trace("metrics launched");
     CK(cudaStreamSynchronize(s));
+    host_trace("metrics synced");
     for (uint32_t r = 0; r < rows; ++r)
         for (uint32_t q = 0; q < n_rp; ++q) {
             pml[(size_t)r * n_rp + q] = out[((size_t)r * n_rp + q) * 2 + 0];

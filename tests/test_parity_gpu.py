@@ -539,3 +539,35 @@ def test_l2_persisting_window(cuda, rho, precision):
     assert np.array_equal(lossy, orc["lossy"])
     ref, ref_lossy, _, _ = run_gpu(off, ids, elts, w, w.layers, precision=precision)
     assert np.array_equal(ylt, ref) and np.array_equal(lossy, ref_lossy)
+
+
+@pytest.mark.parametrize("rho", [0.02, 0.3])
+@pytest.mark.parametrize("catalog", [10_014, 10_000])
+def test_out_of_range_ids_everywhere(cuda, rho, catalog):
+    """A14: an id outside [1, C] -- 0, C + 1 (the sparse kernel's clamp target,
+    a never-set padding bit of the bitmap), C + 2 and 2^32 - 1 -- is reported
+    wherever it sits: a trial's first or last event (partially covered
+    batches) or the middle of a trial (fully covered batches), with C + 2 a
+    multiple of 32 (the padding bit is the first bit of a word) or not.  The
+    context stays usable and matches the oracle afterwards."""
+    ara = _ara()
+    w = synth.get_config("tiny").with_(rho=rho, catalog=catalog)
+    off, ids, elts = make_inputs(w)
+    C = w.catalog
+    t = 37
+    positions = (int(off[t]), int(off[t + 1]) - 1, int(off[t]) + (int(off[t + 1]) - int(off[t])) // 2)
+    with ara.Context(C) as ctx:
+        ctx.load_elts(*elts, terms=w.elt_terms())
+        for bad in (0, C + 1, C + 2, 0xFFFFFFFF):
+            for pos in positions:
+                bi = ids.copy()
+                bi[pos] = bad
+                ctx.load_yet(w.n_trials, 0, off, bi)
+                with pytest.raises(ara.AraError) as e:
+                    ctx.run(w.layers)
+                assert e.value.status == ara.ARA_ERR_OUT_OF_RANGE, (bad, pos)
+        ctx.load_yet(w.n_trials, 0, off, ids)
+        ylt, lossy, _ = ctx.run_host(w.layers)
+    orc = run_oracle(off, ids, elts, w, w.layers)
+    assert_ylt_close(ylt, orc)
+    assert np.array_equal(lossy, orc["lossy"])
