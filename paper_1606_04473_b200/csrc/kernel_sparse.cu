@@ -35,6 +35,7 @@
 //    (partition and alignment invariant; A18/A21) and exact on
 //    integer-valued data (P10).
 #include <cstdlib>
+#include <mutex>
 
 #include "ara_device.cuh"
 
@@ -559,13 +560,29 @@ cudaError_t launch_trials_bc(const TrialParams& p, int fp32, int grid, cudaStrea
     int warps = 16, fixed = 0;
     void* fn = fp32 ? pick_bc<float>((int)p.n_layers, &warps, &fixed)
                     : pick_bc<double>((int)p.n_layers, &warps, &fixed);
-    int dev = 0, optin = 0;
+    // the device's opt-in limit and the kernel's static shared memory, queried
+    // once per kernel and device (host time between the calls of a step is GPU
+    // idle time)
+    struct AttrCache { void* fn; int dev, optin, stat, dyn_set; };
+    static AttrCache cache[16] = {};
+    static std::mutex mu;   // contexts may launch from several host threads
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa{};
-    cudaError_t e = cudaFuncGetAttributes(&fa, fn);
-    if (e != cudaSuccess) return e;
-    const int64_t avail = (int64_t)optin - (int64_t)fa.sharedSizeBytes - fixed;
+    AttrCache* ac = nullptr;
+    for (auto& x : cache)
+        if (x.fn == fn && x.dev == dev) { ac = &x; break; }
+    if (!ac) {
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncAttributes fa{};
+        cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+        if (e != cudaSuccess) return e;
+        for (auto& x : cache)
+            if (!x.fn) { x = AttrCache{fn, dev, optin, (int)fa.sharedSizeBytes, -1}; ac = &x; break; }
+        if (!ac) { static AttrCache spill; spill = AttrCache{fn, dev, optin, (int)fa.sharedSizeBytes, -1}; ac = &spill; }
+    }
+    const int64_t avail = (int64_t)ac->optin - (int64_t)ac->stat - fixed;
     uint64_t ws = avail > 0 ? (uint64_t)avail / 16 * 4 : 0;   // words, 16-B multiple
     const uint64_t need = (((uint64_t)p.catalog + 1 + 31) / 32 + 3) / 4 * 4;   // within the padded bitmap
     if (ws > need) ws = need;
@@ -576,8 +593,11 @@ cudaError_t launch_trials_bc(const TrialParams& p, int fp32, int grid, cudaStrea
     TrialParams q = p;
     q.bm_smem_words = (uint32_t)ws;
     const size_t dyn = (size_t)fixed + ws * 4;
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    if (e != cudaSuccess) return e;
+    if (ac->dyn_set < (int)dyn) {
+        const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (e != cudaSuccess) return e;
+        ac->dyn_set = (int)dyn;
+    }
     void* args[] = {(void*)&q};
     return cudaLaunchKernel(fn, dim3(grid > 0 ? grid : 1), dim3(warps * 32), args, dyn, s);
 }
