@@ -932,6 +932,12 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         chunks.push_back({0, T_local});
     }
     std::vector<cudaEvent_t> chunk_ev;
+    // ARA_TIMELINE=<file>: a chunked run writes its copy/compute timeline (per
+    // chunk: H2D copy start/end on the copy stream, kernels start/end on the
+    // compute stream, ms from the first copy) as JSON -- the B200 analogue of
+    // the paper's transfer/compute life-cycle grids
+    static const char* tl_path = getenv("ARA_TIMELINE");
+    std::vector<cudaEvent_t> tl_c0, tl_k0, tl_k1;   // chunk_ev is the copy end
     std::vector<uint64_t> ho_chunk;   // event index (relative) of each chunk boundary
     uint64_t h2d_bytes = 0;
     if (stream_in) {
@@ -954,7 +960,8 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         }
         chunk_ev.resize(chunks.size());
         for (size_t c = 0; c < chunks.size(); ++c) {
-            if (cudaEventCreateWithFlags(&chunk_ev[c], cudaEventDisableTiming) != cudaSuccess) {
+            if (cudaEventCreateWithFlags(&chunk_ev[c], tl_path ? cudaEventDefault : cudaEventDisableTiming) !=
+                cudaSuccess) {
                 for (size_t q = 0; q < c; ++q) cudaEventDestroy(chunk_ev[q]);
                 return fail(ctx, ARA_ERR_CUDA, "cudaEventCreate failed");
             }
@@ -967,6 +974,12 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
         const uint64_t words_all = pb ? ara_packed_words(nev_all, pb) : 0;
         for (size_t c = 0; c < chunks.size(); ++c) {
             const uint64_t e0 = ho[chunks[c].first] - ho[0], e1 = ho[chunks[c].second] - ho[0];
+            if (tl_path) {   // timeline: the chunk's copy start
+                cudaEvent_t ev0 = nullptr;
+                CK(cudaEventCreate(&ev0));
+                tl_c0.push_back(ev0);
+                CK(cudaEventRecord(ev0, ctx->copy_stream));
+            }
             if (ctx->h_ids && e1 > e0) {
                 CK(cudaMemcpyAsync(ctx->d_ids_own + e0, ctx->h_ids + e0, (e1 - e0) * sizeof(uint32_t),
                                    cudaMemcpyHostToDevice, ctx->copy_stream));
@@ -1099,9 +1112,18 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
             ++launches;
         }
     }
+    const bool tl = tl_path && stream_in && tl_c0.size() == chunks.size();
+    auto tl_mark = [&](std::vector<cudaEvent_t>& v) -> cudaError_t {
+        cudaEvent_t e = nullptr;
+        cudaError_t r = cudaEventCreate(&e);
+        if (r == cudaSuccess) { v.push_back(e); r = cudaEventRecord(e, s); }
+        return r;
+    };
     for (size_t c = 0; c < chunks.size(); ++c) {
         Nvtx nvtx_chunk(stream_in ? "ara_run chunk" : "ara_run launch");
+        if (tl && c > 0) CK(tl_mark(tl_k1));   // the previous chunk's kernels are done
         if (stream_in) CK(cudaStreamWaitEvent(s, chunk_ev[c], 0));
+        if (tl) CK(tl_mark(tl_k0));
         if (stream_in && ctx->h_packed) {   // F3: unpack this chunk's ids on the device
             const uint64_t e0 = ho_chunk[c], e1 = ho_chunk[c + 1];
             CK(launch_unpack(ctx->d_packed_own, ctx->pack_bits, e0, e1, ctx->d_ids_own, s));
@@ -1186,6 +1208,7 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
             ++launches;
         }
     }
+    if (tl && !chunks.empty()) CK(tl_mark(tl_k1));
     if (n_programs) {   // program rows from the layer rows (Alg. 1 l.1)
         uint32_t* d_pl = nullptr;
         CK(cudaMallocAsync(&d_pl, (n_programs + 1) * sizeof(uint32_t), s));
@@ -1197,7 +1220,8 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     CK(cudaEventRecord(ctx->ev[2], s));
     if (ctx->l2_persist) set_l2_window(ctx, nullptr, 0);   // the stream may be the caller's
     for (void* q : wide_free) CK(cudaFreeAsync(q, s));
-    for (auto e : chunk_ev) cudaEventDestroy(e);   // safe: destruction defers until complete
+    if (!tl)
+        for (auto e : chunk_ev) cudaEventDestroy(e);   // safe: destruction defers until complete
     if (stream_in) {
         ctx->chunked_pending = false;   // later runs reuse the device copy
     }
@@ -1269,6 +1293,23 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
     CK(cudaStreamSynchronize(s));
     host_trace("run synced");
     if (stream_in) CK(cudaStreamSynchronize(ctx->copy_stream));
+    if (tl && tl_k0.size() == chunks.size() && tl_k1.size() == chunks.size()) {
+        if (FILE* f = fopen(tl_path, "w")) {
+            auto rel = [&](cudaEvent_t e) { float ms = 0.f; cudaEventElapsedTime(&ms, tl_c0[0], e); return ms; };
+            fprintf(f, "{\"chunks\": [");
+            for (size_t c = 0; c < chunks.size(); ++c)
+                fprintf(f, "%s{\"chunk\": %zu, \"trials\": [%llu, %llu], \"copy_ms\": [%.4f, %.4f], \"kernel_ms\": [%.4f, %.4f]}",
+                        c ? ", " : "", c, (unsigned long long)chunks[c].first, (unsigned long long)chunks[c].second,
+                        rel(tl_c0[c]), rel(chunk_ev[c]), rel(tl_k0[c]), rel(tl_k1[c]));
+            fprintf(f, "]}\n");
+            fclose(f);
+        }
+    }
+    if (tl)
+        for (auto e : chunk_ev) cudaEventDestroy(e);
+    for (auto e : tl_c0) cudaEventDestroy(e);
+    for (auto e : tl_k0) cudaEventDestroy(e);
+    for (auto e : tl_k1) cudaEventDestroy(e);
     const uint32_t bits = (uint32_t)(ctx->h_small[world == 1 ? 4 : 0] & 0xffffffffu);   // world > 1: all-reduced
     st = device_errors(ctx, bits);
     if (st != ARA_OK) {
