@@ -1093,6 +1093,10 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                     p.term[q][w] = make_double2(INFINITY, INFINITY);   // contributes exactly +0
             }
         }
+        p.same_terms = 1u;
+        for (uint32_t q = 1; q < g.nl; ++q)
+            for (uint32_t w = 0; w < (uint32_t)kMaxWin; ++w)
+                if (std::memcmp(&p.term[q][w], &p.term[0][w], sizeof(double2)) != 0) p.same_terms = 0u;
     };
     const uint32_t n_chunks_fold = (n_layers + nlc - 1) / nlc;
     const uint64_t fold_rows = (uint64_t)ctx->catalog + 1;

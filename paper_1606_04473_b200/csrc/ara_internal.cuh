@@ -121,6 +121,7 @@ struct TrialParams {
     // pk_col0 .. (pk_wmask's bits), i.e. window element j = block column pk_col0 + j
     const void* pk;
     uint32_t pk_col0, pk_wmask;
+    uint32_t same_terms;        // every layer of the launch has layer 0's per-ELT terms (a tower over one ELT set)
     uint64_t peer_ld;           // = T_global
     uint64_t peer_t0;           // global index of local trial 0 (this rank's first trial)
     uint32_t bm_smem_words;     // trial_kernel_bc: leading bitmap words staged in shared memory (set by the launcher)

@@ -383,6 +383,17 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
 #pragma unroll
         for (int l = 0; l < NLB; ++l) le[l] = 0.0;
         auto add = [&](double xv, uint32_t j) {
+            // a tower whose layers share the per-ELT terms (same ELT set): the
+            // terms of a looked-up loss are evaluated once and added to every
+            // layer's event loss -- identical inputs, identical f_j
+            if (NLB > 1 && p.same_terms) {
+                const double2 tc = lds_f64x2(s_tm + j * 16u);
+                const double f = terms(xv, tc.x, tc.y);
+#pragma unroll
+                for (int l = 0; l < NLB; ++l)
+                    if (l == 0 || l < (int)p.n_layers) le[l] = __dadd_rn(le[l], f);
+                return;
+            }
 #pragma unroll
             for (int l = 0; l < NLB; ++l) {
                 if (l == 0 || l < (int)p.n_layers) {
