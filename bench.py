@@ -277,6 +277,22 @@ def l2_gather_peak():
         return None
 
 
+def issue_roofline(trec, k_ms, clk, dev):
+    """Instruction-issue roofline of the dominant kernel: warp instructions per
+    launch (ncu, profiles/ara_kernel_traffic.json, same kernel and launch size)
+    over the kernel time, against 4 warp instructions per SM per cycle (one per
+    SM sub-partition) x SMs x the SM clock sampled during the timed region."""
+    if not trec or not trec.get("warp_instructions_per_launch") or not clk or not clk.get("sm_mhz"):
+        return None
+    import torch
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    achieved = trec["warp_instructions_per_launch"] / (k_ms / 1e3)
+    peak = 4.0 * n_sm * clk["sm_mhz"] * 1e6
+    return {"achieved": achieved, "peak": peak, "unit": "warp instructions/s", "frac": achieved / peak,
+            "instructions_per_launch": trec["warp_instructions_per_launch"], "sms": n_sm,
+            "sm_mhz": clk["sm_mhz"], "source": trec.get("source")}
+
+
 def load_traffic(w, precision, variant, n_trials_launch):
     """DRAM bytes and L2->SM sectors per launch of the ARA kernel from the
     committed ncu --set full capture of the same kernel variant AT THE SAME
@@ -629,7 +645,11 @@ def main():
                                                / 1e6 / k_ms) if (trec and l2pk) else None,
                          "note": ("frac = north-star bytes (YET ids + the 32-B ELT sectors actually gathered "
                                   "+ offsets/YLT) / kernel time / HBM peak; occupancy probes are index_bytes, "
-                                  "not HBM bytes")},
+                                  "not HBM bytes"),
+                         # the kernel's binding limit is instruction issue, not HBM: warp instructions
+                         # per launch (same ncu capture) / kernel time vs one warp instruction per
+                         # cycle per SM sub-partition (4 per SM) at the SM clock sampled in the run
+                         "issue": issue_roofline(trec, k_ms, clk, dev)},
             "breakdown_ms": {"ara_kernel": k_ms, "allgather": float(np.mean(ag_ms)), "metrics": float(np.mean(met_ms)),
                              "step": ms,
                              "calls": {k: float(np.median([p[i] for p in part_ms]))
