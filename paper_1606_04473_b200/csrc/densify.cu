@@ -55,18 +55,17 @@ __global__ void __launch_bounds__(256) densify_kernel(const uint64_t* __restrict
 __global__ void __launch_bounds__(256) clear_rows_kernel(unsigned char* __restrict__ tab, const uint32_t* __restrict__ bm,
                                                          uint64_t bm_words, uint32_t n_blocks, uint32_t catalog,
                                                          uint32_t row_bytes, uint64_t block_bytes) {
+    // one warp per bitmap word, lane l clears row 32 * word + l when its bit
+    // is set (the word is a warp broadcast; the rows are independent stores)
     const uint64_t n = (uint64_t)n_blocks * bm_words;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t w = bm[i];
-        const uint64_t b = i / bm_words, e0 = (i % bm_words) * 32;
-        while (w) {
-            const uint32_t bit = __ffs(w) - 1;
-            w &= w - 1;
-            const uint64_t e = e0 + bit;
-            if (e > catalog) break;
-            uint4* row = reinterpret_cast<uint4*>(tab + b * block_bytes + e * row_bytes);
-            for (uint32_t c = 0; c < row_bytes / 16; ++c) row[c] = make_uint4(0, 0, 0, 0);
-        }
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x / 32);
+    for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n; i += nw) {
+        const uint32_t w = __ldg(bm + i);
+        const uint64_t b = i / bm_words, e = (i % bm_words) * 32 + lane;
+        if (!((w >> lane) & 1u) || e > catalog) continue;
+        uint4* row = reinterpret_cast<uint4*>(tab + b * block_bytes + e * row_bytes);
+        for (uint32_t c = 0; c < row_bytes / 16; ++c) row[c] = make_uint4(0, 0, 0, 0);
     }
 }
 
@@ -169,9 +168,9 @@ cudaError_t launch_unpack(const uint32_t* packed, uint32_t bits, uint64_t e0, ui
 }
 
 cudaError_t launch_clear_rows(void* d_table, const TableGeo& geo, uint32_t catalog, cudaStream_t s) {
-    const uint64_t n = (uint64_t)geo.n_blocks * geo.bm_words;
-    uint64_t blocks = (n + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
+    const uint64_t n = (uint64_t)geo.n_blocks * geo.bm_words;   // bitmap words = warps
+    uint64_t blocks = (n + 7) / 8;
+    if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
     clear_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(static_cast<unsigned char*>(d_table),
                                                        reinterpret_cast<const uint32_t*>(static_cast<char*>(d_table) + geo.bm_off),
@@ -179,8 +178,8 @@ cudaError_t launch_clear_rows(void* d_table, const TableGeo& geo, uint32_t catal
                                                        geo.block_elems * geo.esz);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    // bitmaps and occupied-row counters
-    return cudaMemsetAsync(static_cast<char*>(d_table) + geo.bm_off, 0, geo.bytes - geo.bm_off, s);
+    // bitmaps and occupied-row counters (not the packed slots: written before they are read)
+    return cudaMemsetAsync(static_cast<char*>(d_table) + geo.bm_off, 0, geo.pk_off - geo.bm_off, s);
 }
 
 cudaError_t launch_densify(const uint64_t* d_eoff, const uint32_t* d_ev, const double* d_loss,
