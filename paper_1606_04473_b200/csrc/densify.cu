@@ -34,15 +34,23 @@ __global__ void __launch_bounds__(256) densify_kernel(const uint64_t* __restrict
          k += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t e = ev[k];
         const double x = loss[k];
-        if (e == 0u || e > catalog) { bad |= ERRBIT_ELT_RANGE; continue; }
-        if (k > lo && ev[k - 1] >= e) bad |= ERRBIT_ELT_ORDER;
-        if (!(x >= 0.0) || !(x <= DBL_MAX) || (sizeof(TV) == 4 && x > (double)FLT_MAX)) {
-            bad |= ERRBIT_ELT_LOSS;
-            continue;
+        bool newrow = false;
+        if (e == 0u || e > catalog) {
+            bad |= ERRBIT_ELT_RANGE;
+        } else {
+            if (k > lo && ev[k - 1] >= e) bad |= ERRBIT_ELT_ORDER;
+            if (!(x >= 0.0) || !(x <= DBL_MAX) || (sizeof(TV) == 4 && x > (double)FLT_MAX)) {
+                bad |= ERRBIT_ELT_LOSS;
+            } else {
+                tab[(uint64_t)(j / epb) * block_elems + (uint64_t)e * epb + j % epb] = (TV)(x + 0.0);   // canonical +0 (A16)
+                const uint32_t bit = 1u << (e & 31u);   // row e of column block j / epb is occupied
+                newrow = !(atomicOr(bm + (uint64_t)(j / epb) * bm_words + (e >> 5), bit) & bit);
+            }
         }
-        tab[(uint64_t)(j / epb) * block_elems + (uint64_t)e * epb + j % epb] = (TV)(x + 0.0);   // canonical +0 (A16)
-        const uint32_t bit = 1u << (e & 31u);   // row e of column block j / epb is occupied
-        if (!(atomicOr(bm + (uint64_t)(j / epb) * bm_words + (e >> 5), bit) & bit)) atomicAdd(occ + j / epb, 1u);
+        // the block's occupied-row counter: one atomic per warp (j is uniform in the block)
+        const uint32_t am = __activemask();
+        const uint32_t nm = __ballot_sync(am, newrow);
+        if (nm && (threadIdx.x & 31u) == (uint32_t)(__ffs(am) - 1)) atomicAdd(occ + j / epb, (uint32_t)__popc(nm));
     }
     if (bad) atomicOr(err, bad);
 }
@@ -50,22 +58,29 @@ __global__ void __launch_bounds__(256) densify_kernel(const uint64_t* __restrict
 // Reload without the full-table memset: every non-zero element of the table
 // lies in a row whose occupancy bit is set (densify sets the bit with every
 // store), so zeroing exactly those rows -- ~15 % of the rows at the paper's ELT
-// density, 38 MB instead of 256 MB -- restores an all-zero table.  One thread
-// per bitmap word; the caller then clears the bitmaps and counters.
+// density, 38 MB instead of 256 MB -- restores an all-zero table.  One warp per
+// 8 bitmap words, one lane per row; the caller then clears the bitmaps and counters.
 __global__ void __launch_bounds__(256) clear_rows_kernel(unsigned char* __restrict__ tab, const uint32_t* __restrict__ bm,
                                                          uint64_t bm_words, uint32_t n_blocks, uint32_t catalog,
                                                          uint32_t row_bytes, uint64_t block_bytes) {
-    // one warp per bitmap word, lane l clears row 32 * word + l when its bit
-    // is set (the word is a warp broadcast; the rows are independent stores)
+    // one warp per 8 consecutive bitmap words (loaded first, independently),
+    // lane l clears row 32 * word + l of each word when its bit is set
+    constexpr int WPW = 8;
     const uint64_t n = (uint64_t)n_blocks * bm_words;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t nw = (uint64_t)gridDim.x * (blockDim.x / 32);
-    for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < n; i += nw) {
-        const uint32_t w = __ldg(bm + i);
-        const uint64_t b = i / bm_words, e = (i % bm_words) * 32 + lane;
-        if (!((w >> lane) & 1u) || e > catalog) continue;
-        uint4* row = reinterpret_cast<uint4*>(tab + b * block_bytes + e * row_bytes);
-        for (uint32_t c = 0; c < row_bytes / 16; ++c) row[c] = make_uint4(0, 0, 0, 0);
+    for (uint64_t i0 = ((uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5)) * WPW; i0 < n; i0 += nw * WPW) {
+        uint32_t w[WPW];
+#pragma unroll
+        for (int k = 0; k < WPW; ++k) w[k] = i0 + k < n ? __ldg(bm + i0 + k) : 0u;
+#pragma unroll
+        for (int k = 0; k < WPW; ++k) {
+            const uint64_t i = i0 + k;
+            const uint64_t b = i / bm_words, e = (i % bm_words) * 32 + lane;
+            if (!((w[k] >> lane) & 1u) || e > catalog) continue;
+            uint4* row = reinterpret_cast<uint4*>(tab + b * block_bytes + e * row_bytes);
+            for (uint32_t c = 0; c < row_bytes / 16; ++c) row[c] = make_uint4(0, 0, 0, 0);
+        }
     }
 }
 
@@ -168,8 +183,8 @@ cudaError_t launch_unpack(const uint32_t* packed, uint32_t bits, uint64_t e0, ui
 }
 
 cudaError_t launch_clear_rows(void* d_table, const TableGeo& geo, uint32_t catalog, cudaStream_t s) {
-    const uint64_t n = (uint64_t)geo.n_blocks * geo.bm_words;   // bitmap words = warps
-    uint64_t blocks = (n + 7) / 8;
+    const uint64_t n = (uint64_t)geo.n_blocks * geo.bm_words;   // 8 bitmap words per warp
+    uint64_t blocks = (n + 63) / 64;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
     clear_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(static_cast<unsigned char*>(d_table),
