@@ -825,9 +825,11 @@ cudaError_t launch_m4(const M3Params& P, MetricsScratch& m, bool dist, ncclComm_
         return r;
     };
     // Launches without NCCL go through a CUDA graph of the kernels (with their
-    // programmatic-launch edges), re-captured when any argument changes.  The
-    // distributed select with NCCL all-reduces between the passes is launched
-    // eagerly: captured into a graph it hung at N = 4 (profiles/README.md).
+    // programmatic-launch edges), kept in a two-entry cache keyed by every
+    // argument (consecutive multi-GPU runs alternate two global-YLT buffers).
+    // The distributed select with NCCL all-reduces between the passes is
+    // launched eagerly: captured into a graph it hung at N = 4 (DESIGN.md
+    // section 7).
     const char* g_env = getenv("ARA_METRICS_GRAPH");
     const bool use_graph = !g_env || atoi(g_env);
     static_assert(sizeof(M4Params) + sizeof(cudaStream_t) + sizeof(ncclComm_t) + 1 <= sizeof(m.m4_key[0]),
