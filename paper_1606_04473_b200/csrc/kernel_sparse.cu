@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
         }
 #pragma unroll
         for (int l = 0; l < NLB; ++l) {
-            if (l >= (int)p.n_layers) break;
+            if (l > 0 && l >= (int)p.n_layers) break;   // (a launch has >= 1 layer)
             const double o = terms(le[l], p.lw[l].occ_r, p.lw[l].occ_l);
             G[l] = __dadd_rn(G[l], o);
             m[l] += (o > 0.0) ? 1u : 0u;
