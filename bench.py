@@ -215,7 +215,8 @@ def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str
     NOT HBM bytes: they are returned separately as index_bytes (one 4-B word
     per probe).  Fold mode: the fold pass reads every catalogue row window
     once and writes 8 B per (event id, layer); the trial pass reads 4 B of id
-    + one fold row (8 B x layers, padded to a power of two) per event."""
+    + one fold row (8 B x layers, padded to a power of two) per event -- per
+    occupied event for the sparse fold pass (variant 31)."""
     eps = 4 if precision == "f64" else 8
     windows = []
     for L in w.layers:
@@ -231,7 +232,10 @@ def algorithmic_bytes(w, n_events: int, n_trials: int, precision: str, mode: str
         nlc = 1
         while nlc < nl and nlc < 8:
             nlc *= 2
-        hbm = int((w.catalog + 1) * (32 * sec + 8 * nl) + n_events * (4 + 8 * nlc) * ((nl + nlc - 1) // nlc)
+        # the sparse fold pass (variant 31) gathers the fold row of the occupied
+        # events only; the dense one gathers it for every event
+        frac = occupancy if packed else 1.0
+        hbm = int((w.catalog + 1) * (32 * sec + 8 * nl) + n_events * (4 + frac * 8 * nlc) * ((nl + nlc - 1) // nlc)
                   + per_trial)
         return {"hbm": hbm, "index": 0, "yet": 4 * n_events * ((nl + nlc - 1) // nlc), "elt": hbm - per_trial}
     yet = elt = index = 0.0
@@ -256,7 +260,8 @@ def load_peaks():
 KERNEL_NAMES = {30: "ara::trial_kernel_bc (ballot-compacted rounds over packed rows)",
                 12: "ara::trial_kernel_co (cooperative ring)",
                 5: "ara::trial_kernel (register pipeline)", 0: "ara::trial_kernel (register pipeline)",
-                -2: "ara::fold_kernel+trial_fold_kernel"}
+                -2: "ara::fold_kernel+trial_fold_kernel",
+                31: "ara::fold_kernel+trial_kernel_bc<fold> (rounds gather o(e) of the occupied events)"}
 
 
 def kernel_name(variant):
@@ -511,7 +516,7 @@ def main():
     # roofline of the dominant kernel (the ARA trial kernel) on this rank
     k_ms = float(np.mean(kern_ms))
     algb = algorithmic_bytes(w, ev_local, count, a.precision, a.mode, occupancy=used.get("occupancy", 1.0),
-                             packed=used.get("variant") == 30)
+                             packed=used.get("variant") in (30, 31))
     alg = algb["hbm"]
     peaks = load_peaks()
     peak = peaks.get("hbm_gbs")

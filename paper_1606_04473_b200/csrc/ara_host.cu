@@ -210,6 +210,7 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
     ctx->catalog = catalog_size;
     if (const char* v = getenv("ARA_GRID_MULT")) ctx->grid_mult = atof(v);
     if (const char* v = getenv("ARA_KERNEL")) ctx->kernel_variant = atoi(v);
+    if (const char* v = getenv("ARA_FOLD_BC")) ctx->fold_bc = atoi(v) != 0;   // 1: the sparse fold pass (measured slower)
     if (const char* v = getenv("ARA_NO_SKIP")) ctx->no_skip = atoi(v) != 0;
     if (const char* v = getenv("ARA_NO_P2P")) ctx->use_p2p = atoi(v) == 0;
     if (const char* v = getenv("ARA_METRICS_DIST")) ctx->metrics_dist = atoi(v);
@@ -1146,7 +1147,29 @@ ara_status run_impl(ara_ctx* ctx, uint32_t n_layers, const LayerI* layers, uint3
                 }
                 p.fold = ctx->d_fold + (uint64_t)fc * fold_rows * nlc;
                 p.fold_stride = nlc;
-                CK(launch_trials_folded(p, (int)(100 * ctx->grid_mult), s));
+                // The sparse kernel gathers o(e) for the occupied rows only when
+                // every layer of the chunk lies in one sparse column block (a
+                // zero row folds to o = 0, so skipping it adds an exact +0); the
+                // result equals the direct sparse kernel's bit for bit.
+                int bc_blk = ctx->fold_bc && nlc <= 4 && !ctx->no_skip ? 0 : -1;
+                for (uint32_t q = 0; q < p.n_layers && bc_blk >= 0; ++q) {
+                    const LayerI& L = layers[fc * nlc + q];
+                    const uint32_t q0 = L.elt_begin / eps, q1 = (L.elt_end + eps - 1) / eps;
+                    const int blk = (int)(q0 / spb);
+                    if ((q1 - 1) / spb != q0 / spb || (q > 0 && blk != bc_blk)) bc_blk = -1;
+                    else bc_blk = blk;
+                }
+                if (bc_blk >= 0 && (size_t)bc_blk < ctx->occ_rows.size() &&
+                    2ull * ctx->occ_rows[bc_blk] <= (uint64_t)ctx->catalog + 1) {
+                    p.bm = reinterpret_cast<const uint32_t*>(static_cast<const char*>(ctx->d_table) + geo.bm_off) +
+                           (uint64_t)bc_blk * geo.bm_words;
+                    p.pk = nullptr;
+                    used_variant = 31;
+                    used_occupancy = (double)ctx->occ_rows[bc_blk] / ((double)ctx->catalog + 1.0);
+                    CK(launch_trials_bc(p, -1, ctx->n_sm, s));
+                } else {
+                    CK(launch_trials_folded(p, (int)(100 * ctx->grid_mult), s));
+                }
                 ++launches;
             }
             continue;

@@ -153,7 +153,13 @@ __device__ __forceinline__ double2 lds_f64x2(uint32_t a) {
     return v;
 }
 
-template <typename TV, int NLB, int W = BcWarps<NLB>::value>
+// FOLD (catalogue-fold mode): the rounds gather o(e), the
+// occurrence-net loss folded once per catalogue event (fold_kernel), for the
+// NLB layers of the fold chunk instead of the packed slot, and accumulate it
+// exactly as the direct rounds accumulate the o they compute: same events,
+// same dealing, same order -- the YLT and the lossy counts equal the direct
+// sparse kernel's bit for bit (reading A18).
+template <typename TV, int NLB, bool FOLD = false, int W = BcWarps<NLB>::value>
 __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_constant__ TrialParams p) {
     using Geo = BcGeo<W, BcQueue<NLB>::value>;
     constexpr int CAP = Slot<TV>::CAP;
@@ -293,6 +299,7 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
 #pragma unroll
     for (int l = 0; l < NLB; ++l) { G[l] = 0.0; m[l] = 0u; }
     Slot<TV> sl;
+    double fv[FOLD ? NLB : 1];   // FOLD: the lane's event's o(e) per layer of the chunk
     bool pend = false;       // a round's slots are in flight
     bool pend_fin = false;   // ... and it is the last round of trial tb + pend_i
     uint32_t pend_i = 0;
@@ -378,6 +385,20 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
     // adds +0); the trial's tree and stores when it was its last round
     auto consume = [&]() {
         pend = false;
+        if constexpr (FOLD) {
+#pragma unroll
+            for (int l = 0; l < NLB; ++l) {
+                if (l > 0 && l >= (int)p.n_layers) break;
+                const double o = fv[l];   // a lane without an event holds +0
+                G[l] = __dadd_rn(G[l], o);
+                m[l] += (o > 0.0) ? 1u : 0u;
+            }
+            if (pend_fin) {
+                pend_fin = false;
+                finalize(tb + pend_i);
+            }
+            return;
+        }
         const uint32_t mask = sl.mask();
         double le[NLB];
 #pragma unroll
@@ -458,11 +479,30 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
     auto issue_round = [&](uint32_t i) {   // a round of trial tb + i
         __syncwarp();   // the scan's appends (other lanes' stores) are visible
         const uint32_t nr = tail - head < 32u ? tail - head : 32u;
-        if (lane < nr) {
-            const uint32_t e = lds32(cbuf + ((head + lane) & (uint32_t)(Geo::CBUF - 1)) * 4u);
-            ld_slot(static_cast<const char*>(p.pk) + (uint64_t)e * kPackBytes, sl.q);
+        if constexpr (FOLD) {
+            if (lane < nr) {
+                const uint32_t e = lds32(cbuf + ((head + lane) & (uint32_t)(Geo::CBUF - 1)) * 4u);
+                const double* src = p.fold + (uint64_t)e * NLB;   // fold row stride = NLB (host)
+                if constexpr (NLB == 1) {
+                    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(fv[0]) : "l"(src));
+                } else if constexpr (NLB == 2) {
+                    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
+                                 : "=d"(fv[0]), "=d"(fv[1]) : "l"(src));
+                } else {
+                    asm volatile("ld.global.nc.L1::no_allocate.v4.f64 {%0,%1,%2,%3}, [%4];"
+                                 : "=d"(fv[0]), "=d"(fv[1]), "=d"(fv[2]), "=d"(fv[3]) : "l"(src));
+                }
+            } else {
+#pragma unroll
+                for (int l = 0; l < NLB; ++l) fv[l] = 0.0;
+            }
         } else {
-            sl.q[0] = 0; sl.q[1] = 0; sl.q[2] = 0; sl.q[3] = 0;
+            if (lane < nr) {
+                const uint32_t e = lds32(cbuf + ((head + lane) & (uint32_t)(Geo::CBUF - 1)) * 4u);
+                ld_slot(static_cast<const char*>(p.pk) + (uint64_t)e * kPackBytes, sl.q);
+            } else {
+                sl.q[0] = 0; sl.q[1] = 0; sl.q[2] = 0; sl.q[3] = 0;
+            }
         }
         head += nr;
         pend = true;
@@ -547,18 +587,24 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
     if (err) atomicOr(p.err, err);
 }
 
-template <typename TV, int NLB>
+template <typename TV, int NLB, bool FOLD = false>
 void* pick_bc_nl(int* warps, int* fixed) {
     using Geo = BcGeo<BcWarps<NLB>::value, BcQueue<NLB>::value>;
     *warps = Geo::WARPS;
     *fixed = Geo::FIXED;
-    return (void*)trial_kernel_bc<TV, NLB>;
+    return (void*)trial_kernel_bc<TV, NLB, FOLD>;
 }
 template <typename TV>
 void* pick_bc(int nl, int* warps, int* fixed) {
     if (nl <= 1) return pick_bc_nl<TV, 1>(warps, fixed);
     if (nl <= 2) return pick_bc_nl<TV, 2>(warps, fixed);
     return pick_bc_nl<TV, 4>(warps, fixed);
+}
+// fold mode: the template's layer count is the fold row stride (1, 2 or 4)
+void* pick_bc_fold(int stride, int* warps, int* fixed) {
+    if (stride <= 1) return pick_bc_nl<double, 1, true>(warps, fixed);
+    if (stride <= 2) return pick_bc_nl<double, 2, true>(warps, fixed);
+    return pick_bc_nl<double, 4, true>(warps, fixed);
 }
 
 }  // namespace
@@ -567,10 +613,14 @@ void* pick_bc(int nl, int* warps, int* fixed) {
 // of the occupancy bitmap as the opt-in limit leaves (a 16-B multiple).
 cudaError_t launch_trials_bc(const TrialParams& p, int fp32, int grid, cudaStream_t s) {
     if (p.t_end <= p.t_begin) return cudaSuccess;
-    if (!p.bm || !p.pk) return cudaErrorInvalidValue;
+    const bool fold = fp32 < 0;   // fp32 = -1: fold mode (rounds gather o(e) from p.fold)
+    if (!p.bm || (!fold && !p.pk) || (fold && (!p.fold || (p.fold_stride != 1 && p.fold_stride != 2 &&
+                                                             p.fold_stride != 4))))
+        return cudaErrorInvalidValue;
     int warps = 16, fixed = 0;
-    void* fn = fp32 ? pick_bc<float>((int)p.n_layers, &warps, &fixed)
-                    : pick_bc<double>((int)p.n_layers, &warps, &fixed);
+    void* fn = fold ? pick_bc_fold((int)p.fold_stride, &warps, &fixed)
+               : fp32 ? pick_bc<float>((int)p.n_layers, &warps, &fixed)
+                      : pick_bc<double>((int)p.n_layers, &warps, &fixed);
     // the device's opt-in limit and the kernel's static shared memory, queried
     // once per kernel and device (host time between the calls of a step is GPU
     // idle time)

@@ -1,8 +1,10 @@
 """Catalogue-fold mode: o(e) evaluated once per catalogue
 event, one gather per occurrence.  It must match the oracle (A21 tolerance,
-exact lossy counts) and reproduce the dense direct kernels bit for bit
-(ARA_NO_SKIP=1: same per-event arithmetic, same lane mapping and per-trial
-order)."""
+exact lossy counts) and reproduce a direct kernel bit for bit: the dense
+fold pass (default) equals the dense direct kernels (ARA_NO_SKIP=1: same
+per-event arithmetic, same lane mapping and order); with ARA_FOLD_BC=1 a
+sparse column block runs the sparse kernel's rounds over o(e) (kernel
+variant 31), equal to the direct sparse kernel."""
 import math
 
 import numpy as np
@@ -18,15 +20,30 @@ INF = math.inf
 NO_SKIP = {"ARA_NO_SKIP": 1}
 
 
+def assert_rows_match_a_direct_order(fold, direct_sparse, direct_dense):
+    """Every YLT row of the fold run equals, bit for bit, the same row of the
+    direct run with the sparse kernel or of the direct run with the dense
+    kernels (each fold chunk runs one of the two orders); lossy counts are
+    order-free and must equal both."""
+    for r in range(fold[0].shape[0]):
+        assert np.array_equal(fold[0][r], direct_sparse[0][r]) or np.array_equal(fold[0][r], direct_dense[0][r]), r
+    assert np.array_equal(fold[1], direct_sparse[1]) and np.array_equal(fold[1], direct_dense[1])
+
+
+@pytest.mark.parametrize("fold_bc", [0, 1])
 @pytest.mark.parametrize("rho", [0.3, 0.02])
 @pytest.mark.parametrize("precision", ["f64", "f32"])
-def test_fold_equals_direct_tiny(cuda, precision, rho):
+def test_fold_equals_direct_tiny(cuda, precision, rho, fold_bc):
     w = synth.get_config("tiny").with_(rho=rho)
     off, ids, elts = make_inputs(w)
     a = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100), env=NO_SKIP)
-    b = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100), run_mode="fold")
-    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
-    assert np.array_equal(a[3][1], b[3][1]) and np.array_equal(a[3][2], b[3][2])
+    d = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100))
+    b = run_gpu(off, ids, elts, w, w.layers, precision=precision, return_periods=(2, 10, 100), run_mode="fold",
+                env={"ARA_FOLD_BC": fold_bc})
+    ref = d if b[2]["kernel_variant"] == 31 else a   # the sparse fold pass matches the direct sparse kernel
+    assert np.array_equal(ref[0], b[0]) and np.array_equal(ref[1], b[1])
+    assert np.array_equal(ref[3][1], b[3][1]) and np.array_equal(ref[3][2], b[3][2])
+    assert (b[2]["kernel_variant"] == 31) == (fold_bc == 1 and rho <= 0.02)
     orc = run_oracle(off, ids, elts, w, w.layers, fp32=precision == "f32")
     assert_ylt_close(b[0], orc)
     assert np.array_equal(b[1], orc["lossy"])
@@ -47,8 +64,10 @@ def test_fold_many_layers_and_chunks(cuda, n_layers, rho):
         layers.append(synth.LayerSpec(b, e, float(rng.uniform(0, 5e4)), float(rng.choice([INF, rng.uniform(1e5, 1e6)])),
                                       float(rng.uniform(0, 2e6)), float(rng.choice([INF, rng.uniform(1e6, 5e6)]))))
     a = run_gpu(off, ids, elts, w, layers, env=NO_SKIP)
-    b = run_gpu(off, ids, elts, w, layers, run_mode="fold")
-    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    d = run_gpu(off, ids, elts, w, layers)
+    for fold_bc in (0, 1):
+        b = run_gpu(off, ids, elts, w, layers, run_mode="fold", env={"ARA_FOLD_BC": fold_bc})
+        assert_rows_match_a_direct_order(b, d, a)
     orc = run_oracle(off, ids, elts, w, layers)
     assert_ylt_close(b[0], orc)
     assert np.array_equal(b[1], orc["lossy"])
@@ -58,15 +77,20 @@ def test_fold_chunked_h2d(cuda):
     w = synth.get_config("tiny").with_(n_trials=2000)
     off, ids, elts = make_inputs(w)
     a = run_gpu(off, ids, elts, w, w.layers, env=NO_SKIP)
-    b = run_gpu(off, ids, elts, w, w.layers, run_mode="fold", load_mode="chunked", chunk_trials=77)
-    assert np.array_equal(a[0], b[0])
+    d = run_gpu(off, ids, elts, w, w.layers)
+    for fold_bc in (0, 1):
+        b = run_gpu(off, ids, elts, w, w.layers, run_mode="fold", load_mode="chunked", chunk_trials=77,
+                    env={"ARA_FOLD_BC": fold_bc})
+        assert_rows_match_a_direct_order(b, d, a)
     assert_ylt_close(b[0], run_oracle(off, ids, elts, w, w.layers))
 
 
 def test_fold_fullsize_equals_direct(cuda):
-    """Paper-shaped (1M trials, 1e9 events): fold == the dense direct kernel
-    (ARA_NO_SKIP), bit for bit, and faster than it; the default sparse kernel
-    within the A21 bound of both (its summation order differs)."""
+    """Paper-shaped (1M trials, 1e9 events): the dense fold pass == the dense
+    direct kernel (ARA_NO_SKIP) and the sparse fold pass (ARA_FOLD_BC=1) ==
+    the direct sparse kernel, bit for bit; the two orders within the A21
+    bound of each other; the dense fold pass faster than the dense direct
+    kernel."""
     import os
     import torch
     from paper_1606_04473_b200 import ara
@@ -76,13 +100,16 @@ def test_fold_fullsize_equals_direct(cuda):
     d_off = torch.from_numpy(off.view(np.int64)).cuda()
     d_ids = torch.from_numpy(ids.view(np.int32)).cuda()
     out = []
-    for mode, no_skip in (("direct", "1"), ("fold", "0"), ("direct", "0")):
+    for mode, no_skip, fold_bc in (("direct", "1", "0"), ("fold", "0", "0"), ("direct", "0", "0"),
+                                   ("fold", "0", "1")):
         y = torch.empty((2, w.n_trials), dtype=torch.float64, device="cuda")
         os.environ["ARA_NO_SKIP"] = no_skip
+        os.environ["ARA_FOLD_BC"] = fold_bc
         try:
             ctx = ara.Context(w.catalog, run_mode=mode, stream=torch.cuda.current_stream())
         finally:
             os.environ.pop("ARA_NO_SKIP", None)
+            os.environ.pop("ARA_FOLD_BC", None)
         with ctx:
             ctx.load_elts(eo, ev, ls, w.elt_terms())
             ctx.load_yet(w.n_trials, 0, d_off, d_ids)
@@ -90,7 +117,9 @@ def test_fold_fullsize_equals_direct(cuda):
             st = ctx.run(w.layers, y)
         torch.cuda.synchronize()
         out.append((y.cpu().numpy(), st))
-    assert np.array_equal(out[0][0], out[1][0])
+    assert out[3][1]["kernel_variant"] == 31
+    assert np.array_equal(out[0][0], out[1][0])     # dense fold pass == dense direct
+    assert np.array_equal(out[2][0], out[3][0])     # sparse fold pass == direct sparse kernel
     assert out[1][1]["kernel_ms"] < out[0][1]["kernel_ms"]
     # A21: |dY| <= 1e-9 S_t, and S_t >= G_t >= Y_t + AggR wherever Y_t > 0 in
     # either run (the portfolio row is the one layer's row here)
