@@ -210,7 +210,7 @@ extern "C" ara_status ara_create(uint32_t catalog_size, const ara_config* cfg, a
     ctx->catalog = catalog_size;
     if (const char* v = getenv("ARA_GRID_MULT")) ctx->grid_mult = atof(v);
     if (const char* v = getenv("ARA_KERNEL")) ctx->kernel_variant = atoi(v);
-    if (const char* v = getenv("ARA_FOLD_BC")) ctx->fold_bc = atoi(v) != 0;   // 1: the sparse fold pass (measured slower)
+    if (const char* v = getenv("ARA_FOLD_BC")) ctx->fold_bc = atoi(v) != 0;   // 0: the dense fold pass (A/B)
     if (const char* v = getenv("ARA_NO_SKIP")) ctx->no_skip = atoi(v) != 0;
     if (const char* v = getenv("ARA_NO_P2P")) ctx->use_p2p = atoi(v) == 0;
     if (const char* v = getenv("ARA_METRICS_DIST")) ctx->metrics_dist = atoi(v);

@@ -284,7 +284,7 @@ struct ara_ctx {
     double grid_mult = 1.0;           // ARA_GRID_MULT
     int kernel_variant = -1;          // ARA_KERNEL (-1 auto; see pick_kernel in ara_kernel.cu)
     bool no_skip = false;             // ARA_NO_SKIP=1: never skip zero rows via the occupancy bitmap (A/B)
-    bool fold_bc = false;             // ARA_FOLD_BC=1: fold mode on sparse blocks runs the sparse kernel's rounds over o(e) (4.7 ms vs the dense fold pass's 3.9 ms, unexplained)
+    bool fold_bc = true;              // fold mode on sparse blocks: the sparse kernel's rounds over o(e) (ARA_FOLD_BC=0: the dense fold pass)
     std::vector<uint32_t> occ_rows;   // occupied rows per column block (from densify)
     bool table_clean = false;         // table content is exactly described by its occupancy bitmaps
     cudaEvent_t ev[8] = {};

@@ -28,10 +28,31 @@ __global__ void __launch_bounds__(kThreads) fold_kernel(const __grid_constant__ 
             s_term[i / kMaxWin][i % kMaxWin] = p.term[i / kMaxWin][i % kMaxWin];
         __syncthreads();
     }
+    // The table is streamed once: its lines are read with an L2::evict_first
+    // policy, so that they do not stay in L2 ahead of the data the trial pass
+    // gathers next (the YET ids it streams are evict-first too, so stale
+    // normal-priority table lines would otherwise hold most of L2 through the
+    // whole trial pass).
+    const uint64_t pol = policy_evict_first();
     for (uint64_t e = (uint64_t)blockIdx.x * kThreads + threadIdx.x; e <= p.catalog;
          e += (uint64_t)gridDim.x * kThreads) {
         Row<TV, NSEC> r;
-        r.load(p, (uint32_t)e);
+        {
+            const TV* tab = static_cast<const TV*>(p.table) + (uint64_t)e * p.row_stride;
+#pragma unroll
+            for (int sct = 0; sct < NSEC; ++sct) {
+                const TV* q = tab + p.sec_off[sct];
+                if constexpr (sizeof(TV) == 8)
+                    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                        : "=d"(r.x[sct][0]), "=d"(r.x[sct][1]), "=d"(r.x[sct][2]), "=d"(r.x[sct][3])
+                        : "l"(q), "l"(pol));
+                else
+                    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                        : "=f"(r.x[sct][0]), "=f"(r.x[sct][1]), "=f"(r.x[sct][2]), "=f"(r.x[sct][3]),
+                          "=f"(r.x[sct][4]), "=f"(r.x[sct][5]), "=f"(r.x[sct][6]), "=f"(r.x[sct][7])
+                        : "l"(q), "l"(pol));
+            }
+        }
 #pragma unroll
         for (int l = 0; l < NLB; ++l) {
             if (l >= (int)p.n_layers) break;
