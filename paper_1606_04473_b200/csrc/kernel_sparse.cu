@@ -536,13 +536,13 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
 #pragma unroll 1
         for (;;) {
             const uint32_t bs = c * CHE;
-            const uint32_t dlo = rlo > bs ? rlo - bs : 0u;            // <= CHE
-            const uint32_t dhi = rhi - bs < CHE ? rhi - bs : CHE;
-            if (dhi > dlo) {
-                if (dhi - dlo == CHE) {
-                    if (c & 1u) scan(true, 0u, CHE, xb, wb);
-                    else scan(true, 0u, CHE, xa, wa);
-                } else {
+            if (rlo <= bs && rhi >= bs + CHE) {   // the whole batch belongs to the trial
+                if (c & 1u) scan(true, 0u, CHE, xb, wb);
+                else scan(true, 0u, CHE, xa, wa);
+            } else {
+                const uint32_t dlo = rlo > bs ? rlo - bs : 0u;            // <= CHE
+                const uint32_t dhi = rhi - bs < CHE ? rhi - bs : CHE;
+                if (dhi > dlo) {
                     if (c & 1u) scan(false, dlo, dhi, xb, wb);
                     else scan(false, dlo, dhi, xa, wa);
                 }
