@@ -550,8 +550,10 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
             const bool fin = rhi <= bs + CHE;   // the trial ends in this batch
 #pragma unroll 1
             for (;;) {
+                // full rounds; at the trial's end (no group deferred) every queued entry
+                const uint32_t need = (fin && !M3) ? 1u : 32u;
 #pragma unroll 1
-                while (tail - head >= 32u || (fin && tail != head && !M3)) {
+                while (tail - head >= need) {
                     if (pend) consume();
                     issue_round(i);
                 }
