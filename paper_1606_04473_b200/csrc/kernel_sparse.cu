@@ -424,7 +424,10 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
             }
         };
         const bool fits = __popc(mask) <= CAP;
-        if (__all_sync(0xffffffffu, fits)) {
+        // the round's longest row: one reduction decides both whether every row
+        // fits its slot and how many walk steps the round needs (no vote per step)
+        const uint32_t vmax = __reduce_max_sync(0xffffffffu, (uint32_t)__popc(mask));
+        if (vmax <= (uint32_t)CAP) {
             // every lane's slot holds all of its row's non-zeros (the common
             // case): walk them in column order, the v-th from slot value v --
             // unrolled, so v is a register name, and branch-free: a lane whose
@@ -433,8 +436,7 @@ __global__ void __launch_bounds__(W * 32, 1) trial_kernel_bc(const __grid_consta
             uint32_t mm = mask;
 #pragma unroll
             for (int v = 0; v < CAP; ++v) {
-                // (a round always holds an occupied event, mask != 0: v = 0 needs no vote)
-                if (v > 0 && !__any_sync(0xffffffffu, mm != 0u)) break;
+                if ((uint32_t)v >= vmax) break;   // (vmax >= 1: a round holds an occupied event)
                 const uint32_t b = (uint32_t)(__ffs(mm) - 1);   // 0xffffffff when mm == 0
                 mm &= mm - 1u;
                 const uint32_t j = b - p.pk_col0;                // window element (wraps when b < col0)
